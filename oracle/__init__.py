@@ -1,0 +1,153 @@
+"""ctypes wrapper of the float64 CPU oracle (oracle/srmra_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` legs, never by the product package.  See the header of
+srmra_oracle.c for the passages of PAPER.md each step follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "srmra_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_fp = ctypes.POINTER(ctypes.c_float)
+_ip = ctypes.POINTER(ctypes.c_int64)
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O3 -march=native -fopenmp; no -ffast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared",
+                               "-std=c11", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.oracle_em_iter.restype = ctypes.c_int
+        lib.oracle_em_iter.argtypes = [_fp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_double, _dp, _dp, _dp, ctypes.c_int, ctypes.c_double,
+                                       _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        lib.oracle_posterior.restype = ctypes.c_double
+        lib.oracle_posterior.argtypes = [_fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                         _dp, _dp, _dp, _dp]
+        lib.oracle_loglik_obs.restype = ctypes.c_int
+        lib.oracle_loglik_obs.argtypes = [_fp, _ip, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_double, _dp, _dp, _dp, _dp]
+        lib.oracle_project.restype = None
+        lib.oracle_project.argtypes = [_dp, ctypes.c_int, _dp]
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+@dataclass
+class IterResult:
+    x: np.ndarray        # float64 [L][L]   (after projection if requested)
+    rho1: np.ndarray     # float64 [L]
+    rho2: np.ndarray
+    loglik: float        # LL at the input theta
+    b: np.ndarray        # float64 [L][L]   numerator of eq:x_EM
+    A: np.ndarray        # float64 [L][L]   diagonal of A in eq:x_EM
+    colsum: np.ndarray   # float64 [L][L]   sum_i w^{i,s}
+    ll_obs: np.ndarray   # float64 [N]
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def em_iter(y, L_low, K, sigma, x, rho1, rho2, project=True, tau=None) -> IterResult:
+    """One EM iteration (eq:weights_EM, eq:x_EM, eq:rho_EM) + optional stand-in projection."""
+    lib = _load()
+    y = _f32(y)
+    N = y.shape[0]
+    L = L_low * K
+    x = _f64(x).reshape(L, L)
+    rho1 = _f64(rho1)
+    rho2 = _f64(rho2)
+    if tau is None:
+        tau = 1e-12 * N
+    xo = np.empty((L, L)); r1 = np.empty(L); r2 = np.empty(L); ll = np.empty(1)
+    b = np.empty((L, L)); A = np.empty((L, L)); cs = np.empty((L, L)); llo = np.empty(N)
+    rc = lib.oracle_em_iter(_p(y, _fp), N, L, L_low, K, float(sigma), _p(x, _dp), _p(rho1, _dp),
+                            _p(rho2, _dp), int(bool(project)), float(tau), _p(xo, _dp), _p(r1, _dp),
+                            _p(r2, _dp), _p(ll, _dp), _p(b, _dp), _p(A, _dp), _p(cs, _dp), _p(llo, _dp))
+    if rc != 0:
+        raise ValueError(f"oracle_em_iter failed rc={rc}")
+    return IterResult(xo, r1, r2, float(ll[0]), b, A, cs, llo)
+
+
+def run(y, L_low, K, sigma, x0, rho1_0, rho2_0, iters, proj_every=1, tau=None):
+    """`iters` iterations of Algorithm 2 with the stand-in projection applied
+    after iteration t when (t+1) % proj_every == 0 (proj_every=0: never).  Returns
+    (x, rho1, rho2, [LL_0..LL_{iters-1}])."""
+    x, r1, r2 = _f64(x0), _f64(rho1_0), _f64(rho2_0)
+    trace = []
+    for t in range(iters):
+        proj = proj_every > 0 and (t + 1) % proj_every == 0
+        r = em_iter(y, L_low, K, sigma, x, r1, r2, project=proj, tau=tau)
+        x, r1, r2 = r.x, r.rho1, r.rho2
+        trace.append(r.loglik)
+    return x, r1, r2, trace
+
+
+def posterior(yi, L_low, K, sigma, x, rho1, rho2):
+    """(w [L][L], log-likelihood term) of one observation."""
+    lib = _load()
+    yi = _f32(yi)
+    L = L_low * K
+    w = np.empty((L, L))
+    lse = lib.oracle_posterior(_p(yi, _fp), L, L_low, K, float(sigma), _p(_f64(x), _dp),
+                               _p(_f64(rho1), _dp), _p(_f64(rho2), _dp), _p(w, _dp))
+    return w, float(lse)
+
+
+def loglik_obs(y, idx, L_low, K, sigma, x, rho1, rho2):
+    """Per-observation log-likelihood terms for observation indices `idx`."""
+    lib = _load()
+    y = _f32(y)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.empty(idx.shape[0])
+    rc = lib.oracle_loglik_obs(_p(y, _fp), _p(idx, _ip), idx.shape[0], L_low * K, L_low, K,
+                               float(sigma), _p(_f64(x), _dp), _p(_f64(rho1), _dp),
+                               _p(_f64(rho2), _dp), _p(out, _dp))
+    if rc != 0:
+        raise ValueError(f"oracle_loglik_obs rc={rc}")
+    return out
+
+
+def project(x):
+    """3x3 circular box filter + clamp[-1,1] (north_star stand-in for the denoiser)."""
+    lib = _load()
+    x = _f64(x)
+    L = x.shape[0]
+    out = np.empty_like(x)
+    lib.oracle_project(_p(x, _dp), L, _p(out, _dp))
+    return out

@@ -1,0 +1,368 @@
+"""Pins of the float64 oracle against things other than itself (CPU only).
+
+Each test constructs its expectation independently of oracle/srmra_oracle.c:
+dense P / R_s matrices written from the definitions, closed forms, the
+paper's invariances, EM monotonicity, the sigma -> 0 limit,
+textbook K = 1 MRA EM, and hand-enumerated index examples (tests/golden/).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ----------------------------------------------------------------------- independent helpers
+def R_matrix(L, s):
+    """Dense 2-D circular translation, (R_s x)[n] = x[n - s] (PAPER.md:28 'R_s denotes a 2-D
+    circular translation'), acting on row-major vec(x)."""
+    M = np.zeros((L * L, L * L))
+    for n1 in range(L):
+        for n2 in range(L):
+            M[n1 * L + n2, ((n1 - s[0]) % L) * L + (n2 - s[1]) % L] = 1.0
+    return M
+
+
+def P_matrix(L, K):
+    """Dense down-sampling, (P x)[n] = x[n K] (PAPER.md:29 'collects L_low x L_low equally-spaced
+    samples')."""
+    Ll = L // K
+    M = np.zeros((Ll * Ll, L * L))
+    for n1 in range(Ll):
+        for n2 in range(Ll):
+            M[n1 * Ll + n2, (n1 * K) * L + n2 * K] = 1.0
+    return M
+
+
+def dense_em(y, K, sigma, x, rho1, rho2):
+    """EM iteration in the paper's matrix form (eq:likelihood_EM, eq:weights_EM, eq:x_EM with
+    P^{-1} := P^T, eq:rho_EM marginals), dense and brute force."""
+    N, Ll, _ = y.shape
+    L = Ll * K
+    P = P_matrix(L, K)
+    Rs = {(a, b): R_matrix(L, (a, b)) for a in range(L) for b in range(L)}
+    xv = x.reshape(-1)
+    A = np.zeros((L * L, L * L))
+    bvec = np.zeros(L * L)
+    colsum = np.zeros((L, L))
+    LL = 0.0
+    W = np.zeros((N, L, L))
+    for i in range(N):
+        yi = y[i].reshape(-1).astype(np.float64)
+        ell = np.full((L, L), -np.inf)
+        for (a, b), R in Rs.items():
+            r = yi - P @ R @ xv
+            with np.errstate(divide="ignore"):
+                ell[a, b] = np.log(rho1[a]) + np.log(rho2[b]) - r @ r / (2 * sigma ** 2)
+        m = ell.max()
+        lse = m + np.log(np.exp(ell - m).sum())
+        LL += lse
+        w = np.exp(ell - lse)
+        W[i] = w
+        colsum += w
+        for (a, b), R in Rs.items():
+            A += w[a, b] * R.T @ P.T @ P @ R
+            bvec += w[a, b] * R.T @ P.T @ yi
+    return dict(A=A, b=bvec, colsum=colsum, LL=LL, W=W,
+                rho1=colsum.sum(1) / colsum.sum(), rho2=colsum.sum(0) / colsum.sum())
+
+
+def box_clamp_dense(x):
+    L = x.shape[0]
+    out = np.zeros_like(x)
+    for d1 in (-1, 0, 1):
+        for d2 in (-1, 0, 1):
+            out += np.roll(x, (-d1, -d2), axis=(0, 1))
+    return np.clip(out / 9.0, -1.0, 1.0)
+
+
+def tiny(L_low=2, K=2, N=5, sigma=0.7, seed=0, zeros=0):
+    return synth.make_random(L_low, K, N, sigma, seed, rho_zeros=zeros)
+
+
+# ----------------------------------------------------------------------- golden index examples
+def test_golden_index_convention():
+    g = json.load(open(os.path.join(GOLDEN, "index_convention.json")))
+    for ex in g["shift_examples"] + g["downsample_examples"]:
+        x = np.array(ex["x"], dtype=np.float64)
+        K = ex["K"]
+        y = synth.observe(x, np.array([ex["s"]]), K, 0.0, None)[0]
+        np.testing.assert_array_equal(y, np.array(ex["out"], dtype=np.float32))
+        # the dense operators used by the brute-force pin agree with the same examples
+        L = x.shape[0]
+        yd = (P_matrix(L, K) @ R_matrix(L, ex["s"]) @ x.reshape(-1)).reshape(L // K, L // K)
+        np.testing.assert_array_equal(yd, np.array(ex["out"], dtype=np.float64))
+
+
+# ----------------------------------------------------------------------- (1) brute force
+@pytest.mark.parametrize("seed,zeros", [(0, 0), (1, 0), (2, 1)])
+def test_bruteforce_dense_4x4(oracle_mod, seed, zeros):
+    p = tiny(seed=seed, zeros=zeros)
+    x = p.x0.astype(np.float64)
+    d = dense_em(p.y, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+    r = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=False, tau=0.0)
+    # A from the matrix form is diagonal (consequence of P^{-1} := P^T)
+    A = d["A"]
+    assert np.abs(A - np.diag(np.diag(A))).max() == 0.0
+    np.testing.assert_allclose(r.A.reshape(-1), np.diag(A), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(r.b.reshape(-1), d["b"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(r.colsum, d["colsum"], rtol=1e-12, atol=1e-14)
+    assert abs(r.loglik - d["LL"]) <= 1e-12 * abs(d["LL"])
+    np.testing.assert_allclose(r.rho1, d["rho1"], rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(r.rho2, d["rho2"], rtol=1e-12, atol=1e-15)
+    xs = np.linalg.solve(A, d["b"]).reshape(x.shape)       # A x = b (eq:x_EM)
+    np.testing.assert_allclose(r.x, xs, rtol=1e-11, atol=1e-12)
+    # per-observation posterior (eq:weights_EM)
+    for i in range(p.N):
+        w, lse = oracle_mod.posterior(p.y[i], p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+        np.testing.assert_allclose(w, d["W"][i], rtol=1e-11, atol=1e-15)
+    # projection of the same iterate
+    rp = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=True, tau=0.0)
+    np.testing.assert_allclose(rp.x, box_clamp_dense(xs), rtol=1e-11, atol=1e-12)
+
+
+def test_bruteforce_dense_8x8_K4(oracle_mod):
+    p = synth.make_random(2, 4, 3, 0.5, 5)
+    x = p.x0.astype(np.float64)
+    d = dense_em(p.y, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+    r = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=False, tau=0.0)
+    np.testing.assert_allclose(r.A.reshape(-1), np.diag(d["A"]), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(r.b.reshape(-1), d["b"], rtol=1e-12, atol=1e-13)
+    assert abs(r.loglik - d["LL"]) <= 1e-12 * abs(d["LL"])
+
+
+# ----------------------------------------------------------------------- (2) normalisation
+def test_posteriors_sum_to_one(oracle_mod):
+    p = synth.make_random(4, 2, 40, 0.3, 3, rho_zeros=2)
+    x = p.x0.astype(np.float64)
+    for i in range(0, p.N, 7):
+        w, _ = oracle_mod.posterior(p.y[i], p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+        assert abs(w.sum() - 1.0) < 1e-12
+        assert np.all(np.isfinite(w)) and np.all(w >= 0)
+    r = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=False)
+    assert abs(r.colsum.sum() - p.N) < 1e-10 * p.N
+    assert abs(r.rho1.sum() - 1) < 1e-13 and abs(r.rho2.sum() - 1) < 1e-13
+    # zero prior mass stays zero (log 0 = -inf contributes weight 0, never NaN)
+    assert np.all(r.rho1[p.rho1_0 == 0] == 0) and np.all(r.rho2[p.rho2_0 == 0] == 0)
+    # mass conservation (independent of x): sum_p b[p] = sum_{i,n} y_i[n]; sum_p A = N L_low^2
+    assert abs(r.b.sum() - p.y.astype(np.float64).sum()) < 1e-9 * np.abs(p.y).sum()
+    assert abs(r.A.sum() - p.N * p.L_low ** 2) < 1e-9 * p.N * p.L_low ** 2
+
+
+# ----------------------------------------------------------------------- (3) EM monotone
+def test_loglik_monotone_without_projection(oracle_mod):
+    p = synth.make_random(4, 2, 60, 0.4, 11)
+    _, _, _, trace = oracle_mod.run(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0,
+                                    iters=20, proj_every=0)
+    for a, b in zip(trace[:-1], trace[1:]):
+        assert b >= a - 1e-9 * abs(a), (a, b)
+    assert trace[-1] > trace[0]
+
+
+# ----------------------------------------------------------------------- (4) sigma -> 0 recovery
+def test_exact_recovery_sigma_to_zero(oracle_mod):
+    L_low, K, N = 4, 2, 60
+    L = L_low * K
+    rng = np.random.default_rng(5)
+    x_true = rng.standard_normal((L, L)).astype(np.float32).astype(np.float64)
+    rho1 = rng.dirichlet(np.ones(L)); rho2 = rng.dirichlet(np.ones(L))
+    shifts = np.stack([rng.choice(L, N, p=rho1), rng.choice(L, N, p=rho2)], 1)
+    y = synth.observe(x_true, shifts, K, 0.0, None)        # noiseless
+    sigma = 1e-3
+    r = oracle_mod.em_iter(y, L_low, K, sigma, x_true, rho1, rho2, project=False)
+    # posterior collapses on the true shift
+    for i in range(0, N, 9):
+        w, _ = oracle_mod.posterior(y[i], L_low, K, sigma, x_true, rho1, rho2)
+        assert np.unravel_index(np.argmax(w), w.shape) == tuple(shifts[i])
+        assert w.max() > 1 - 1e-12
+    np.testing.assert_allclose(r.x, x_true, rtol=0, atol=1e-12)
+    h1 = np.bincount(shifts[:, 0], minlength=L) / N
+    h2 = np.bincount(shifts[:, 1], minlength=L) / N
+    np.testing.assert_allclose(r.rho1, h1, atol=1e-12)
+    np.testing.assert_allclose(r.rho2, h2, atol=1e-12)
+
+
+# ----------------------------------------------------------------------- closed forms / limits
+def test_constant_image_closed_form(oracle_mod):
+    p = synth.make_random(4, 2, 30, 0.5, 7)
+    c = 0.3
+    x = np.full((p.L_high, p.L_high), c)
+    r = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=False)
+    yy = p.y.astype(np.float64)
+    ll = -(((yy - c) ** 2).sum(axis=(1, 2))) / (2 * p.sigma ** 2)
+    np.testing.assert_allclose(r.ll_obs, ll, rtol=1e-12)
+    w, _ = oracle_mod.posterior(p.y[0], p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+    np.testing.assert_allclose(w, np.outer(p.rho1_0, p.rho2_0), rtol=1e-11)
+    # posterior = prior for every i  =>  rho' = rho (up to rounding)
+    np.testing.assert_allclose(r.rho1, p.rho1_0, rtol=1e-11)
+
+
+def test_large_sigma_posterior_is_prior(oracle_mod):
+    p = synth.make_random(4, 2, 4, 0.5, 8)
+    x = p.x0.astype(np.float64)
+    w, _ = oracle_mod.posterior(p.y[1], p.L_low, p.K, 1e6, x, p.rho1_0, p.rho2_0)
+    assert np.abs(w - np.outer(p.rho1_0, p.rho2_0)).max() < 1e-6
+
+
+def test_point_mass_rho_stays_point_mass(oracle_mod):
+    p = synth.make_random(4, 2, 20, 0.5, 9)
+    L = p.L_high
+    r1 = np.zeros(L); r1[3] = 1.0
+    r2 = np.zeros(L); r2[5] = 1.0
+    r = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, p.x0, r1, r2, project=False)
+    np.testing.assert_array_equal(r.rho1, r1)
+    np.testing.assert_array_equal(r.rho2, r2)
+
+
+# ----------------------------------------------------------------------- invariances
+def test_global_shift_invariance(oracle_mod):
+    p = synth.make_random(4, 2, 25, 0.4, 12)
+    x = p.x0.astype(np.float64)
+    base = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=False)
+    u = (3, 6)
+    xu = np.roll(x, u, axis=(0, 1))                       # R_u x
+    r1u = np.roll(p.rho1_0, -u[0]); r2u = np.roll(p.rho2_0, -u[1])   # rho'(k) = rho(k + u)
+    sh = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, xu, r1u, r2u, project=False)
+    assert abs(sh.loglik - base.loglik) <= 1e-11 * abs(base.loglik)
+
+
+def test_theorem1_separable_invariance(oracle_mod):
+    """permuting sub-images and shifting each one on the low-res grid leaves
+    the likelihood unchanged.  Separable version (per-axis class permutation pi_k and per-class
+    shift tau_k) so that the product prior stays a product."""
+    rng = np.random.default_rng(21)
+    L_low, K = 4, 2
+    L = L_low * K
+    p = synth.make_random(L_low, K, 30, 0.4, 13)
+    x = p.x0.astype(np.float64)
+    base = oracle_mod.em_iter(p.y, L_low, K, p.sigma, x, p.rho1_0, p.rho2_0, project=False)
+    for _ in range(5):
+        pi = [rng.permutation(K), rng.permutation(K)]
+        tau = [rng.integers(0, L_low, K), rng.integers(0, L_low, K)]
+        xn = np.zeros_like(x)
+        for r1 in range(K):
+            for r2 in range(K):
+                # x_r[m] = x[(K m - r) mod L];  x'_{pi(r)}[m] = x_r[m - tau(r)]
+                for m1 in range(L_low):
+                    for m2 in range(L_low):
+                        src = x[(K * ((m1 - tau[0][r1]) % L_low) - r1) % L,
+                                (K * ((m2 - tau[1][r2]) % L_low) - r2) % L]
+                        xn[(K * m1 - pi[0][r1]) % L, (K * m2 - pi[1][r2]) % L] = src
+        rn = []
+        for k, rho in enumerate((p.rho1_0, p.rho2_0)):
+            out = np.zeros(L)
+            for r in range(K):
+                for t in range(L_low):
+                    out[pi[k][r] + K * ((t - tau[k][r]) % L_low)] = rho[r + K * t]
+            rn.append(out)
+        got = oracle_mod.em_iter(p.y, L_low, K, p.sigma, xn, rn[0], rn[1], project=False)
+        assert abs(got.loglik - base.loglik) <= 1e-11 * abs(base.loglik)
+
+
+def test_observation_permutation_invariance(oracle_mod):
+    p = synth.make_random(4, 2, 33, 0.4, 14)
+    x = p.x0.astype(np.float64)
+    a = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+    perm = np.random.default_rng(0).permutation(p.N)
+    b = oracle_mod.em_iter(p.y[perm], p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+    np.testing.assert_allclose(b.x, a.x, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(b.rho1, a.rho1, rtol=1e-12, atol=1e-15)
+    assert abs(a.loglik - b.loglik) <= 1e-12 * abs(a.loglik)
+    np.testing.assert_allclose(b.ll_obs, a.ll_obs[perm], rtol=1e-13)
+
+
+# ----------------------------------------------------------------------- M-step = argmax Q
+def test_mstep_maximises_Q(oracle_mod):
+    p = synth.make_random(4, 2, 20, 0.5, 15)
+    x = p.x0.astype(np.float64)
+    L, K = p.L_high, p.K
+    r = oracle_mod.em_iter(p.y, p.L_low, K, p.sigma, x, p.rho1_0, p.rho2_0, project=False)
+    W = np.stack([oracle_mod.posterior(p.y[i], p.L_low, K, p.sigma, x, p.rho1_0, p.rho2_0)[0]
+                  for i in range(p.N)])
+    P = P_matrix(L, K)
+    Rs = [[R_matrix(L, (a, b)) for b in range(L)] for a in range(L)]
+
+    def Q(xc, r1, r2):   # eq:Q
+        tot = 0.0
+        for i in range(p.N):
+            yi = p.y[i].reshape(-1).astype(np.float64)
+            for a in range(L):
+                for b in range(L):
+                    w = W[i, a, b]
+                    if w == 0:
+                        continue
+                    res = yi - P @ Rs[a][b] @ xc.reshape(-1)
+                    tot += w * (np.log(r1[a]) + np.log(r2[b]) - res @ res / (2 * p.sigma ** 2))
+        return tot
+
+    q0 = Q(r.x, r.rho1, r.rho2)
+    rng = np.random.default_rng(1)
+    for _ in range(6):
+        d = 1e-3 * rng.standard_normal(r.x.shape)
+        assert Q(r.x + d, r.rho1, r.rho2) < q0
+        e1 = rng.dirichlet(np.ones(L)); e2 = rng.dirichlet(np.ones(L))
+        assert Q(r.x, 0.9 * r.rho1 + 0.1 * e1, 0.9 * r.rho2 + 0.1 * e2) < q0
+    assert q0 >= Q(x, p.rho1_0, p.rho2_0)     # ascent from theta_t
+
+
+# ----------------------------------------------------------------------- K = 1: textbook MRA EM
+def test_K1_reduces_to_textbook_mra(oracle_mod):
+    L, N, sigma = 6, 15, 0.6
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((L, L))
+    r1 = rng.dirichlet(np.ones(L)); r2 = rng.dirichlet(np.ones(L))
+    y = (rng.standard_normal((N, L, L))).astype(np.float32)
+    yy = y.astype(np.float64)
+    xn = np.zeros((L, L)); LL = 0.0; cs = np.zeros((L, L))
+    for i in range(N):
+        ell = np.zeros((L, L))
+        for a in range(L):
+            for b in range(L):
+                ell[a, b] = (np.log(r1[a]) + np.log(r2[b])
+                             - ((yy[i] - np.roll(x, (a, b), axis=(0, 1))) ** 2).sum() / (2 * sigma ** 2))
+        m = ell.max(); lse = m + np.log(np.exp(ell - m).sum()); LL += lse
+        w = np.exp(ell - lse); cs += w
+        for a in range(L):
+            for b in range(L):
+                xn += w[a, b] * np.roll(yy[i], (-a, -b), axis=(0, 1))   # R_{-s} y_i
+    xn /= N
+    r = oracle_mod.em_iter(y, L, 1, sigma, x, r1, r2, project=False)
+    np.testing.assert_allclose(r.x, xn, rtol=1e-11, atol=1e-13)
+    assert abs(r.loglik - LL) <= 1e-12 * abs(LL)
+    np.testing.assert_allclose(r.rho1, cs.sum(1) / N, rtol=1e-11)
+
+
+# ----------------------------------------------------------------------- projection
+def test_projection_stand_in(oracle_mod):
+    L = 8
+    np.testing.assert_allclose(oracle_mod.project(np.full((L, L), 0.25)), 0.25, rtol=1e-15)
+    np.testing.assert_array_equal(oracle_mod.project(np.full((L, L), 2.0)), 1.0)
+    np.testing.assert_array_equal(oracle_mod.project(np.full((L, L), -3.0)), -1.0)
+    imp = np.zeros((L, L)); imp[0, 0] = 0.9
+    out = oracle_mod.project(imp)
+    exp = np.zeros((L, L))
+    for d1 in (-1, 0, 1):
+        for d2 in (-1, 0, 1):
+            exp[d1 % L, d2 % L] = 0.1
+    np.testing.assert_allclose(out, exp, atol=1e-16)
+    z = np.random.default_rng(0).standard_normal((L, L))
+    np.testing.assert_allclose(oracle_mod.project(z), box_clamp_dense(z), atol=1e-15)
+
+
+def test_unobserved_class_keeps_previous_value(oracle_mod):
+    """Reading R6: A[p] <= tau keeps x_t[p].  rho concentrated on even shifts leaves odd classes
+    of pixels unobserved (pixel p is sampled under s iff s = -p mod K)."""
+    p = synth.make_random(4, 2, 10, 0.5, 16)
+    L = p.L_high
+    r1 = np.zeros(L); r1[::2] = 1.0; r1 /= r1.sum()
+    r2 = np.zeros(L); r2[::2] = 1.0; r2 /= r2.sum()
+    x = p.x0.astype(np.float64)
+    r = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, r1, r2, project=False)
+    odd = np.ones((L, L), bool); odd[::2, ::2] = False
+    assert np.all(r.A[odd] == 0)
+    np.testing.assert_array_equal(r.x[odd], x[odd])
+    assert np.all(r.A[::2, ::2] > 0)
