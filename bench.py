@@ -1,0 +1,290 @@
+#!/usr/bin/env python
+"""Benchmark: one projected-EM iteration of 2-D SR-MRA (E-step + M-step over all N observations and
+all L_high^2 shifts, finalize, projection) per step, through libsrmra.so's C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+Metric (BASELINE.json): obs x shift likelihoods per second per EM iteration, N * L_high^2 / t.
+Workload: BASELINE.json configs[1] (c1: L_high=64, L_low=32, K=2, N=10,000, sigma=0.25), seeded
+synthetic data (synth/).  Multi-GPU (torchrun): weak scaling, every rank holds its own N
+observations (global N = N * world) and one NCCL all-reduce of the sufficient statistics runs per
+iteration.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "obs×shift likelihoods/sec per EM iteration (N·L_high^2/t), % of roofline"
+UNIT = "obs*shift/s"
+# FP32 SIMT peak: 148 SMs x 128 FP32 lanes x 2 FLOP (FMA) x 1.965 GHz (B200_PROFILING.md SM count and
+# clocks.max.sm).
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+FLUSH_BYTES = 256 << 20
+
+
+def flop_per_unit(path: str, L_low: int) -> float:
+    """Algorithmic FLOP per (observation, shift) unit."""
+    if path == "fft":
+        return 10.0 * np.log2(L_low) + 17.0
+    return 4.0 * L_low * L_low  # direct / gemm: 2 L_low^2 (E-step dot) + 2 L_low^2 (M-step)
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(p) -> dict:
+    return {"workload": p.name, "L_high": p.L_high, "L_low": p.L_low, "K": p.K, "N_per_rank": p.N,
+            "sigma": p.sigma}
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- oracle (CPU) legs
+def oracle_rate(p, seconds: float, n_max: int | None = None):
+    """Time the float64 oracle (as it stands) on a bounded sample of observations of p: one EM
+    iteration from theta_0 on the first n observations, n sized for ~`seconds` of work."""
+    import oracle
+    oracle.build()
+    n_probe = min(p.N, 64)
+    t0 = time.perf_counter()
+    oracle.em_iter(p.y[:n_probe], p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    per_obs = (time.perf_counter() - t0) / n_probe
+    n = int(max(n_probe, min(n_max or p.N, p.N, seconds / max(per_obs, 1e-9))))
+    t0 = time.perf_counter()
+    oracle.em_iter(p.y[:n], p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    dt = time.perf_counter() - t0
+    return n * p.L_high ** 2 / dt, n, dt, oracle.max_threads()
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    p = synth.make_config(args.config)
+    # per-step sample sized so warmup + steps finish in about `budget` seconds
+    budget = float(os.environ.get("SRMRA_REF_BUDGET_S", 150))
+    n_probe = min(p.N, 32)
+    t0 = time.perf_counter()
+    oracle.em_iter(p.y[:n_probe], p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    per_obs = (time.perf_counter() - t0) / n_probe
+    n = int(max(8, min(p.N, budget / (args.steps + args.warmup) / per_obs)))
+    ys = p.y[:n]
+    for _ in range(args.warmup):
+        oracle.em_iter(ys, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.em_iter(ys, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * p.L_high ** 2 * args.steps / tot
+    sample = f"first {n} of {p.N} observations of {p.name}, one EM iteration from theta_0 per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload(p),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_04754_b200 as srm
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [srm.srmra_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    p = synth.make_config(args.config, seed_offset=1000 * rank if world > 1 else 0)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=args.path,
+                      proj_every=1, device=local, rank=rank, world=world, nccl_id=nccl_id,
+                      stream=stream.cuda_stream)
+    path = ctx.path
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            ctx.em_iter(1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    ctx.profile(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with torch.cuda.stream(stream):
+        for a, b in evs:
+            flush.zero_()          # L2 flush (256 MiB write), outside the timed events
+            a.record(stream)
+            ctx.em_iter(1)
+            b.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    em_ms, iter_ms, n_prof = ctx.profile_read()
+    ctx.profile(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms, em_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, em_max = float(t[0]), float(t[1])
+    units_step = p.N * world * p.L_high ** 2
+    value = units_step * args.steps / (tot_ms / 1e3)
+
+    # roofline of the dominant kernel (measured live: events around it inside the library, same stream)
+    fpu = flop_per_unit(path, p.L_low)
+    em_avg_s = em_ms / 1e3 / max(n_prof, 1)
+    achieved = fpu * p.N * p.L_high ** 2 / em_avg_s / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+            "kernel": {"fft": "k_fft_em", "direct": "k_direct_em", "gemm": "k_gemm_em"}.get(path, path),
+            "flop_per_unit": fpu, "kernel_ms_avg": em_avg_s * 1e3,
+            "kernel_share_of_step": em_ms / max(iter_ms, 1e-12),
+            "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md)"}
+
+    # end-to-end through the public API with pinned host buffers: load (H2D) + cfg.iters iterations + D2H
+    e2e = None
+    if args.e2e_jobs > 0:
+        y_pin = torch.from_numpy(p.y).pin_memory()
+        y_np = y_pin.numpy()
+        jt = []
+        for j in range(args.e2e_jobs + 1):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            ctx.load(y_np, p.x0, p.rho1_0, p.rho2_0)
+            ctx.em_iter(p.iters)
+            ctx.get_estimate()
+            dt = time.perf_counter() - t0
+            if j > 0:
+                jt.append(dt)
+        tj = float(np.mean(jt))
+        if world > 1:
+            t = torch.tensor([tj], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tj = float(t[0])
+        e2e = {"value": units_step * p.iters / tj, "unit": UNIT,
+               "h2d_bytes_per_step": int(p.y.nbytes + 4 * p.L_high ** 2 + 16 * p.L_high),
+               "d2h_bytes_per_step": int(4 * p.L_high ** 2 + 16 * p.L_high + 16),
+               "step": f"srmra_load (pinned host y, x0, rho) + {p.iters} x srmra_em_iter + srmra_get_estimate",
+               "timer": "host perf_counter, max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, dt, cores = oracle_rate(p, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {n} of {p.N} observations of {p.name}, one EM iteration from theta_0 "
+                         f"({dt:.1f} s)"}
+
+    launches = ctx.launches_per_iter() * args.steps
+    ctx.close()
+    if rank == 0:
+        cfg = workload(p)
+        cfg.update({"path": path, "l2": "flushed before every timed step (256 MiB write, outside the events)",
+                    "iters_per_step": 1, "global_N": p.N * world})
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk, "step_ms_median": statistics.median(step_ms)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c1", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="auto", choices=["auto", "fft", "direct", "gemm"])
+    ap.add_argument("--e2e-jobs", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

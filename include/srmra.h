@@ -1,0 +1,164 @@
+/*
+ * srmra.h — C ABI of libsrmra.so: B200-native (sm_100a) projected EM for 2-D super-resolution
+ * multi-reference alignment (Shani, Giryes, Bendory, arXiv 2204.04754).
+ *
+ * The problem statement the arguments mirror (§I eq:model_1 and its explicit
+ * form):   y_i[n1,n2] = x[(n1 K - s_i^1) mod L_high, (n2 K - s_i^2) mod L_high] + eps_i[n1,n2],
+ *          i = 1..N, n in Z_{L_low}^2, K = L_high / L_low an integer, eps ~ N(0, sigma^2) i.i.d.,
+ *          s^1 ~ rho1, s^2 ~ rho2 i.i.d..  theta = (x, rho1, rho2).
+ *
+ * One call of srmra_em_iter(ctx, 1) is one iteration of Algorithm 2:
+ *   E-step  eq:weights_EM over all N observations and all L_high^2 shifts,
+ *   M-step  eq:x_EM (P^{-1} read as P^T so A is diagonal) and eq:rho_EM
+ *           (separable marginals: rho1'[s1] = sum_{s2} sum_i w^{i,s} / sum w),
+ *   the log-likelihood eq:likelihood_EM ("up to a constant": the Gaussian
+ *           normaliser is omitted) at the iteration's INPUT theta,
+ *   and, every proj_every-th iteration, the projection x <- D(x) with the fixed
+ *           stand-in denoiser D = 3x3 circular box filter followed by clamping to [-1, 1].
+ * Shifts are s = (s1, s2) in Z_{L_high}^2, s1 acting on the first (row) index; flattened
+ * row-major s = s1 * L_high + s2.  All arrays are row-major and C-contiguous.
+ *
+ * Ownership: the caller owns every host buffer passed in or out; srmra_init / srmra_load copy
+ * their inputs into library-owned device memory, so the caller may free them on return.  The
+ * context owns all device memory, its stream (unless one was supplied) and the NCCL
+ * communicator until srmra_free.  A context is not thread-safe; separate contexts are
+ * independent.  No C++ exception crosses this ABI.
+ *
+ * Errors: every int-returning call returns SRMRA_OK (0) or a negative SRMRA_ERR_* code and
+ * records a message readable with srmra_last_error(ctx) (ctx == NULL: the calling thread's last
+ * srmra_init failure).  After SRMRA_ERR_CUDA / SRMRA_ERR_NCCL the context is failed and every
+ * later call returns SRMRA_ERR_STATE.
+ */
+#ifndef SRMRA_H_
+#define SRMRA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SRMRA_API __attribute__((visibility("default")))
+#else
+#define SRMRA_API
+#endif
+
+#define SRMRA_OK 0
+#define SRMRA_ERR_INVALID_ARG (-1) /* K*L_low != L_high, size <= 0, sigma <= 0 or non-finite, non-finite
+                                      y/x0/rho, rho negative or |sum rho - 1| > 1e-6, bad option    */
+#define SRMRA_ERR_UNSUPPORTED (-2) /* shape outside the compiled specialisations / no sm_100 device  */
+#define SRMRA_ERR_CUDA (-3)
+#define SRMRA_ERR_NCCL (-4)
+#define SRMRA_ERR_OOM (-5)
+#define SRMRA_ERR_STATE (-6)       /* call on a failed context                                        */
+#define SRMRA_ERR_NUMERIC (-7)     /* non-finite log-likelihood or estimate detected by finalize      */
+
+/* E-step / M-step implementation ("path") */
+#define SRMRA_PATH_AUTO 0   /* per-shape choice from measurement ("Path choice")        */
+#define SRMRA_PATH_GEMM 1   /* S = Y T(x)^T and Z = W^T Y on tcgen05 tensor cores, 3xTF32             */
+#define SRMRA_PATH_FFT 2    /* batched polyphase FFT correlation (K^2 correlations of L_low x L_low)  */
+#define SRMRA_PATH_DIRECT 3 /* direct SIMT correlation (small shapes)                                 */
+
+typedef struct srmra_ctx srmra_ctx; /* opaque, owned by the library */
+
+typedef struct {
+    int32_t path;        /* SRMRA_PATH_*; default AUTO                                              */
+    int32_t proj_every;  /* F: project after iteration t (0-based, counted over the context's life)
+                            when (t+1) % F == 0; 0 = never; default 1                                */
+    double floor_tau;    /* pixel p keeps x_t[p] when its coverage A[p] <= floor_tau;
+                            < 0 selects the default 1e-12 * N_global                                 */
+    int32_t device;      /* CUDA ordinal; < 0 = the calling thread's current device                 */
+    int32_t rank;        /* this process's rank in [0, world)                                         */
+    int32_t world;       /* number of ranks sharing the observations; 1 = no NCCL                     */
+    const void* nccl_id; /* world > 1: the 128-byte ncclUniqueId from srmra_nccl_unique_id() on rank 0,
+                            broadcast by the caller (e.g. torch.distributed); ignored if world == 1  */
+    void* stream;        /* cudaStream_t to enqueue on, or NULL: the context creates its own          */
+    int32_t trace_cap;   /* capacity of the on-device log-likelihood trace; default 4096              */
+} srmra_options;
+
+/* Fill *opt with the defaults above. */
+SRMRA_API void srmra_default_options(srmra_options* opt);
+
+/*
+ * Create a context for this rank's shard of the observations and stage theta_0.
+ *   y       host, float32 [n_local][L_low][L_low]: observations y_i of this rank (copied).
+ *   n_local number of observations on this rank (>= 0; the global N is the sum over ranks).
+ *   L_high, L_low, K   image side, observation side, K = L_high / L_low (must hold exactly).
+ *   sigma   noise standard deviation (> 0, finite), known.
+ *   x0      host, float32 [L_high][L_high]: initial image estimate (copied).
+ *   rho1_0, rho2_0   host, float64 [L_high]: initial shift marginals (>= 0, each summing to 1
+ *           within 1e-6; renormalised in float64).
+ *   opt     NULL for defaults.
+ * Errors: INVALID_ARG, UNSUPPORTED, CUDA, NCCL, OOM.  On error *out is NULL.
+ */
+SRMRA_API int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high, int32_t L_low,
+               int32_t K, double sigma, const float* x0, const double* rho1_0, const double* rho2_0,
+               const srmra_options* opt);
+
+/* Replace the observations (same n_local and shape) and theta with new host data, reusing the
+ * context's device memory; resets the iteration counter and the trace. */
+SRMRA_API int srmra_load(srmra_ctx* ctx, const float* y, const float* x0, const double* rho1_0,
+               const double* rho2_0);
+
+/* Enqueue n_iters >= 0 EM iterations on the context stream; asynchronous (no host sync).
+ * With world > 1 each iteration performs one NCCL all-reduce of the sufficient statistics. */
+SRMRA_API int srmra_em_iter(srmra_ctx* ctx, int32_t n_iters);
+
+/*
+ * Synchronise the stream and copy the current estimate to caller-owned host buffers (any may be
+ * NULL): x_out float32 [L_high][L_high], rho1_out / rho2_out float64 [L_high], *loglik_out the
+ * log-likelihood at the INPUT of the last iteration (NaN if none ran), *iters_done the number of
+ * iterations run since init/load.  Returns SRMRA_ERR_NUMERIC if any iteration produced a
+ * non-finite log-likelihood or estimate.
+ */
+SRMRA_API int srmra_get_estimate(srmra_ctx* ctx, float* x_out, double* rho1_out, double* rho2_out,
+                       double* loglik_out, int32_t* iters_done);
+
+/* Copy up to cap entries of the per-iteration log-likelihood trace (LL_0, LL_1, ...) into out;
+ * *n receives the number of iterations recorded (may exceed cap). Synchronises. */
+SRMRA_API int srmra_get_loglik_trace(srmra_ctx* ctx, double* out, int32_t cap, int32_t* n);
+
+/* Test hook: the global (all-reduced) sufficient statistics of the last iteration, float64:
+ * b [L_high^2] numerator of eq:x_EM, class_mass [K^2] (A[p] = class_mass[(-p1 mod K)*K + (-p2 mod K)]),
+ * marg1 / marg2 [L_high] un-normalised marginals sum_i sum_{s2} w^{i,s} / sum_i sum_{s1} w^{i,s}.
+ * Any pointer may be NULL.  Synchronises. */
+SRMRA_API int srmra_get_stats(srmra_ctx* ctx, double* b, double* class_mass, double* marg1, double* marg2);
+
+/* Test hook: per-observation log-likelihood terms log sum_s rho[s] exp(-||y_i - P R_s x||^2/(2 sigma^2))
+ * of this rank's observations at the input of the last iteration, float64 [n_local]. */
+SRMRA_API int srmra_get_obs_loglik(srmra_ctx* ctx, double* out);
+
+/* Test hook: compute this rank's LOCAL (not all-reduced) packed statistics at the current theta
+ * without updating it: out float64 [L_high^2 + K^2 + 2 L_high + 1] = b | class_mass | marg1 |
+ * marg2 | LL.  Used to check that shard statistics sum to the full-data statistics. */
+SRMRA_API int srmra_local_stats(srmra_ctx* ctx, double* out);
+
+/* The path the context runs (SRMRA_PATH_GEMM / FFT / DIRECT), or a negative error code. */
+SRMRA_API int srmra_get_path(const srmra_ctx* ctx);
+
+/* Number of kernel launches one srmra_em_iter(ctx, 1) enqueues (for launch accounting). */
+SRMRA_API int srmra_launches_per_iter(const srmra_ctx* ctx);
+
+/* Profiling: enable != 0 starts recording CUDA events on the context stream around each
+ * iteration and around its dominant E/M kernel (clearing earlier records); 0 stops. */
+SRMRA_API int srmra_profile(srmra_ctx* ctx, int32_t enable);
+
+/* Synchronise and return, over the iterations recorded since srmra_profile(ctx, 1): the summed
+ * duration of the dominant E/M kernel launches (*em_kernel_ms), of whole iterations (*iter_ms),
+ * and the number of iterations (*n_iters).  Any pointer may be NULL.  Clears the records. */
+SRMRA_API int srmra_profile_read(srmra_ctx* ctx, double* em_kernel_ms, double* iter_ms, int32_t* n_iters);
+
+/* Write a fresh 128-byte ncclUniqueId into out (rank 0 calls this before srmra_init). */
+SRMRA_API int srmra_nccl_unique_id(void* out128);
+
+/* Release all device memory, the stream (if owned) and the NCCL communicator.  NULL is a no-op. */
+SRMRA_API void srmra_free(srmra_ctx* ctx);
+
+/* Last error message of ctx (or of the calling thread's last failed srmra_init when ctx is NULL). */
+SRMRA_API const char* srmra_last_error(const srmra_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRMRA_H_ */

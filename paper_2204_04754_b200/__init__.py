@@ -1,0 +1,278 @@
+"""Python binding of libsrmra.so — B200-native projected EM for 2-D SR-MRA (arXiv 2204.04754).
+
+Argument marshalling only: every step of the EM iteration runs in the CUDA kernels of
+libsrmra.so (csrc/), behind the C ABI declared in include/srmra.h.  The module-level functions
+carry the ABI's names; `Context` is a thin owner of one srmra_ctx.  There is no CPU fallback:
+importing this package without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsrmra.so")
+
+SRMRA_OK = 0
+SRMRA_ERR_INVALID_ARG = -1
+SRMRA_ERR_UNSUPPORTED = -2
+SRMRA_ERR_CUDA = -3
+SRMRA_ERR_NCCL = -4
+SRMRA_ERR_OOM = -5
+SRMRA_ERR_STATE = -6
+SRMRA_ERR_NUMERIC = -7
+
+PATH_AUTO, PATH_GEMM, PATH_FFT, PATH_DIRECT = 0, 1, 2, 3
+PATH_NAMES = {PATH_AUTO: "auto", PATH_GEMM: "gemm", PATH_FFT: "fft", PATH_DIRECT: "direct"}
+PATH_IDS = {v: k for k, v in PATH_NAMES.items()}
+
+# every symbol include/srmra.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_iter", "srmra_get_estimate",
+               "srmra_get_loglik_trace", "srmra_get_stats", "srmra_get_obs_loglik", "srmra_local_stats",
+               "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read",
+               "srmra_nccl_unique_id", "srmra_free",
+               "srmra_last_error")
+
+
+class SrmraError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libsrmra error {code}: {msg}")
+        self.code = code
+
+
+class srmra_options(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("proj_every", ctypes.c_int32), ("floor_tau", ctypes.c_double),
+                ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("trace_cap", ctypes.c_int32)]
+
+
+_fp = ctypes.POINTER(ctypes.c_float)
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int32)
+_ctxp = ctypes.c_void_p
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    sig = {
+        "srmra_default_options": (None, [ctypes.POINTER(srmra_options)]),
+        "srmra_init": (ctypes.c_int, [ctypes.POINTER(_ctxp), _fp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_double, _fp, _dp, _dp, ctypes.POINTER(srmra_options)]),
+        "srmra_load": (ctypes.c_int, [_ctxp, _fp, _fp, _dp, _dp]),
+        "srmra_em_iter": (ctypes.c_int, [_ctxp, ctypes.c_int32]),
+        "srmra_get_estimate": (ctypes.c_int, [_ctxp, _fp, _dp, _dp, _dp, _ip]),
+        "srmra_get_loglik_trace": (ctypes.c_int, [_ctxp, _dp, ctypes.c_int32, _ip]),
+        "srmra_get_stats": (ctypes.c_int, [_ctxp, _dp, _dp, _dp, _dp]),
+        "srmra_get_obs_loglik": (ctypes.c_int, [_ctxp, _dp]),
+        "srmra_local_stats": (ctypes.c_int, [_ctxp, _dp]),
+        "srmra_get_path": (ctypes.c_int, [_ctxp]),
+        "srmra_launches_per_iter": (ctypes.c_int, [_ctxp]),
+        "srmra_profile": (ctypes.c_int, [_ctxp, ctypes.c_int32]),
+        "srmra_profile_read": (ctypes.c_int, [_ctxp, _dp, _dp, _ip]),
+        "srmra_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+        "srmra_free": (None, [_ctxp]),
+        "srmra_last_error": (ctypes.c_char_p, [_ctxp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _check(rc: int, ctx=None):
+    if rc != SRMRA_OK:
+        msg = _lib.srmra_last_error(ctx)
+        raise SrmraError(rc, msg.decode() if msg else "")
+    return rc
+
+
+# ------------------------------------------------------------------ ABI-named functions
+def srmra_default_options() -> srmra_options:
+    o = srmra_options()
+    _lib.srmra_default_options(ctypes.byref(o))
+    return o
+
+
+def srmra_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.srmra_nccl_unique_id(buf))
+    return buf.raw
+
+
+def srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, opt: srmra_options | None = None):
+    """Returns the opaque context handle (int).  y: float32 [n][L_low][L_low] host array."""
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    x0 = np.ascontiguousarray(x0, dtype=np.float32)
+    r1 = np.ascontiguousarray(rho1_0, dtype=np.float64)
+    r2 = np.ascontiguousarray(rho2_0, dtype=np.float64)
+    h = _ctxp()
+    rc = _lib.srmra_init(ctypes.byref(h), _ptr(y, _fp), int(y.shape[0]), int(L_high), int(L_low), int(K),
+                         float(sigma), _ptr(x0, _fp), _ptr(r1, _dp), _ptr(r2, _dp),
+                         ctypes.byref(opt) if opt is not None else None)
+    _check(rc, None)
+    return h.value
+
+
+def srmra_load(ctx, y, x0, rho1_0, rho2_0):
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    _check(_lib.srmra_load(ctx, _ptr(y, _fp), _ptr(np.ascontiguousarray(x0, dtype=np.float32), _fp),
+                           _ptr(np.ascontiguousarray(rho1_0, dtype=np.float64), _dp),
+                           _ptr(np.ascontiguousarray(rho2_0, dtype=np.float64), _dp)), ctx)
+
+
+def srmra_em_iter(ctx, n_iters: int = 1):
+    _check(_lib.srmra_em_iter(ctx, int(n_iters)), ctx)
+
+
+def srmra_get_estimate(ctx, L_high: int):
+    x = np.empty((L_high, L_high), np.float32)
+    r1 = np.empty(L_high)
+    r2 = np.empty(L_high)
+    ll = ctypes.c_double()
+    it = ctypes.c_int32()
+    _check(_lib.srmra_get_estimate(ctx, _ptr(x, _fp), _ptr(r1, _dp), _ptr(r2, _dp), ctypes.byref(ll),
+                                   ctypes.byref(it)), ctx)
+    return x, r1, r2, ll.value, it.value
+
+
+def srmra_get_loglik_trace(ctx, cap: int = 4096):
+    out = np.empty(cap)
+    n = ctypes.c_int32()
+    _check(_lib.srmra_get_loglik_trace(ctx, _ptr(out, _dp), cap, ctypes.byref(n)), ctx)
+    return out[:min(n.value, cap)].copy()
+
+
+def srmra_get_stats(ctx, L_high: int, K: int):
+    b = np.empty((L_high, L_high)); cm = np.empty((K, K)); m1 = np.empty(L_high); m2 = np.empty(L_high)
+    _check(_lib.srmra_get_stats(ctx, _ptr(b, _dp), _ptr(cm, _dp), _ptr(m1, _dp), _ptr(m2, _dp)), ctx)
+    return b, cm, m1, m2
+
+
+def srmra_get_obs_loglik(ctx, n_local: int):
+    out = np.empty(n_local)
+    _check(_lib.srmra_get_obs_loglik(ctx, _ptr(out, _dp)), ctx)
+    return out
+
+
+def srmra_local_stats(ctx, L_high: int, K: int):
+    out = np.empty(L_high * L_high + K * K + 2 * L_high + 1)
+    _check(_lib.srmra_local_stats(ctx, _ptr(out, _dp)), ctx)
+    return out
+
+
+def srmra_get_path(ctx) -> int:
+    return int(_lib.srmra_get_path(ctx))
+
+
+def srmra_launches_per_iter(ctx) -> int:
+    return int(_lib.srmra_launches_per_iter(ctx))
+
+
+def srmra_profile(ctx, enable: bool = True):
+    _check(_lib.srmra_profile(ctx, int(bool(enable))), ctx)
+
+
+def srmra_profile_read(ctx):
+    """(summed E/M-kernel ms, summed iteration ms, iterations) since srmra_profile(ctx, True)."""
+    em = ctypes.c_double()
+    it = ctypes.c_double()
+    n = ctypes.c_int32()
+    _check(_lib.srmra_profile_read(ctx, ctypes.byref(em), ctypes.byref(it), ctypes.byref(n)), ctx)
+    return em.value, it.value, n.value
+
+
+def srmra_free(ctx):
+    _lib.srmra_free(ctx)
+
+
+def srmra_last_error(ctx=None) -> str:
+    m = _lib.srmra_last_error(ctx)
+    return m.decode() if m else ""
+
+
+# ------------------------------------------------------------------ thin owner
+class Context:
+    """Owns one srmra_ctx for this rank's shard.  Methods map 1:1 onto the ABI."""
+
+    def __init__(self, y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, path="auto", proj_every=1,
+                 floor_tau=-1.0, device=-1, rank=0, world=1, nccl_id: bytes | None = None, stream=None,
+                 trace_cap=4096):
+        o = srmra_default_options()
+        o.path = PATH_IDS[path] if isinstance(path, str) else int(path)
+        o.proj_every = int(proj_every)
+        o.floor_tau = float(floor_tau)
+        o.device = int(device)
+        o.rank, o.world = int(rank), int(world)
+        self._id_buf = None
+        if nccl_id is not None:
+            self._id_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._id_buf, ctypes.c_void_p)
+        o.stream = stream
+        o.trace_cap = int(trace_cap)
+        self.L_high, self.L_low, self.K = int(L_high), int(L_low), int(K)
+        self.n_local = int(np.asarray(y).shape[0])
+        self.handle = srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, o)
+
+    @property
+    def path(self) -> str:
+        return PATH_NAMES[srmra_get_path(self.handle)]
+
+    def load(self, y, x0, rho1_0, rho2_0):
+        srmra_load(self.handle, y, x0, rho1_0, rho2_0)
+
+    def em_iter(self, n_iters=1):
+        srmra_em_iter(self.handle, n_iters)
+
+    def get_estimate(self):
+        return srmra_get_estimate(self.handle, self.L_high)
+
+    def loglik_trace(self, cap=4096):
+        return srmra_get_loglik_trace(self.handle, cap)
+
+    def stats(self):
+        return srmra_get_stats(self.handle, self.L_high, self.K)
+
+    def obs_loglik(self):
+        return srmra_get_obs_loglik(self.handle, self.n_local)
+
+    def local_stats(self):
+        return srmra_local_stats(self.handle, self.L_high, self.K)
+
+    def profile(self, enable=True):
+        srmra_profile(self.handle, enable)
+
+    def profile_read(self):
+        return srmra_profile_read(self.handle)
+
+    def launches_per_iter(self):
+        return srmra_launches_per_iter(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            srmra_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,479 @@
+// srmra_api.cu — the C ABI of libsrmra.so (declared and documented in include/srmra.h).
+// Host-side: argument validation, device buffers, path choice, the per-iteration launch
+// sequence (prep -> E/M path kernel -> pack -> [NCCL all-reduce] -> finalize/projection) and
+// the NCCL communicator (libnccl.so.2 is dlopen'ed on first use, so single-GPU use has no NCCL
+// dependency and, inside a PyTorch process, the already-loaded NCCL is reused).
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "srmra_internal.cuh"
+
+using namespace srmra;
+
+static thread_local std::string g_init_err;
+
+cudaEvent_t srmra_ctx::prof_event() {
+    if (ev_used == ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+namespace {
+struct NcclApi {
+    bool loaded = false;
+    std::string err;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.loaded && api.err.empty()) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+            return api;
+        }
+        api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+        api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+        api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+        api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+        if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString)
+            api.err = "libnccl.so.2 lacks a required symbol";
+        else
+            api.loaded = true;
+    }
+    return api;
+}
+
+int fail(srmra_ctx* c, int code, const std::string& msg) {
+    if (c) {
+        c->err = msg;
+        if (code == SRMRA_ERR_CUDA || code == SRMRA_ERR_NCCL) c->failed = true;
+    } else {
+        g_init_err = msg;
+    }
+    return code;
+}
+
+int cuda_fail(srmra_ctx* c, cudaError_t e, const char* where) {
+    std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+    if (e == cudaErrorMemoryAllocation) return fail(c, SRMRA_ERR_OOM, m);
+    return fail(c, SRMRA_ERR_CUDA, m);
+}
+
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, #call);     \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+    if (count == 0) count = 1;
+    return cudaMalloc((void**)p, sizeof(T) * count);
+}
+
+bool all_finite_f(const float* a, size_t n) {
+    for (size_t k = 0; k < n; ++k)
+        if (!isfinite(a[k])) return false;
+    return true;
+}
+
+int check_rho(const double* r, int L, std::vector<double>& out) {
+    double s = 0;
+    for (int k = 0; k < L; ++k) {
+        if (!isfinite(r[k]) || r[k] < 0) return -1;
+        s += r[k];
+    }
+    if (fabs(s - 1.0) > 1e-6) return -1;
+    out.resize(L);
+    for (int k = 0; k < L; ++k) out[k] = r[k] / s;
+    return 0;
+}
+
+int choose_path(int requested, int L, int Ll, int K) {
+    if (requested == SRMRA_PATH_DIRECT) return direct_supported(L, Ll, K) ? SRMRA_PATH_DIRECT : -1;
+    if (requested == SRMRA_PATH_FFT) return fft_supported(L, Ll, K) ? SRMRA_PATH_FFT : -1;
+    if (requested == SRMRA_PATH_GEMM) return -1;  // not built yet
+    // AUTO: measured choice ("Path choice")
+    if (fft_supported(L, Ll, K)) return SRMRA_PATH_FFT;
+    if (direct_supported(L, Ll, K)) return SRMRA_PATH_DIRECT;
+    return -1;
+}
+
+// Upload y and theta_0 (host) and run the per-observation init kernels.
+int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<double>& r1,
+           const std::vector<double>& r2) {
+    const size_t ny = (size_t)c->n_local * c->Ll2;
+    // pinned caller buffers give an asynchronous DMA; pageable ones are staged by the driver
+    if (ny) CK(cudaMemcpyAsync(c->d_y, y, sizeof(float) * ny, cudaMemcpyHostToDevice, c->stream));
+    std::vector<double> x64(c->L2), rho(2 * c->L);
+    for (int k = 0; k < c->L2; ++k) x64[k] = (double)x0[k];
+    for (int k = 0; k < c->L; ++k) { rho[k] = r1[k]; rho[c->L + k] = r2[k]; }
+    CK(cudaMemcpyAsync(c->d_x64, x64.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_x32, x0, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    CK(launch_init_obs(c));
+    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_init(c));
+    CK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
+    c->iters_done = 0;
+    return SRMRA_OK;
+}
+
+int allreduce_pack(srmra_ctx* c) {
+    if (c->opt.world <= 1) return SRMRA_OK;
+    NcclApi& api = nccl();
+    ncclResult_t r = api.AllReduce(c->d_pack, c->d_pack, (size_t)c->pk.total, ncclFloat64, ncclSum,
+                                   (ncclComm_t)c->nccl_comm, c->stream);
+    if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    return SRMRA_OK;
+}
+
+int record(srmra_ctx* c) {
+    if (!c->prof) return SRMRA_OK;
+    cudaEvent_t e = c->prof_event();
+    if (!e) return fail(c, SRMRA_ERR_CUDA, "cudaEventCreate failed");
+    CK(cudaEventRecord(e, c->stream));
+    return SRMRA_OK;
+}
+
+// E + M over the local shard at the current theta: prep, path kernel, pack (no all-reduce).
+// With profiling on, events bracket the dominant E/M kernel (records 2 and 3 of the quadruple).
+int local_estep_mstep(srmra_ctx* c) {
+    int rc;
+    CK(launch_prep(c));
+    if (c->path == SRMRA_PATH_FFT) {
+        CK(launch_fft_prep(c));
+        if ((rc = record(c))) return rc;
+        CK(launch_fft_em(c));
+        if ((rc = record(c))) return rc;
+        CK(launch_fft_fold(c));
+    } else if (c->path == SRMRA_PATH_DIRECT) {
+        if ((rc = record(c))) return rc;
+        CK(launch_direct_em(c));
+        if ((rc = record(c))) return rc;
+    } else {
+        return fail(c, SRMRA_ERR_UNSUPPORTED, "path not available");
+    }
+    CK(launch_pack(c));
+    return SRMRA_OK;
+}
+
+}  // namespace
+
+// ==================================================================== ABI
+extern "C" {
+
+void srmra_default_options(srmra_options* o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->path = SRMRA_PATH_AUTO;
+    o->proj_every = 1;
+    o->floor_tau = -1.0;
+    o->device = -1;
+    o->rank = 0;
+    o->world = 1;
+    o->nccl_id = nullptr;
+    o->stream = nullptr;
+    o->trace_cap = 4096;
+}
+
+const char* srmra_last_error(const srmra_ctx* ctx) { return ctx ? ctx->err.c_str() : g_init_err.c_str(); }
+
+int srmra_nccl_unique_id(void* out128) {
+    if (!out128) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "out128 is NULL");
+    NcclApi& api = nccl();
+    if (!api.loaded) return fail(nullptr, SRMRA_ERR_NCCL, api.err);
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, SRMRA_ERR_NCCL, api.GetErrorString(r));
+    memcpy(out128, &id, sizeof(id));
+    return SRMRA_OK;
+}
+
+int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high, int32_t L_low, int32_t K,
+               double sigma, const float* x0, const double* rho1_0, const double* rho2_0,
+               const srmra_options* opt_in) {
+    srmra_ctx* c = nullptr;  // errors before the context exists go to g_init_err
+    if (!out) return fail(c, SRMRA_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    srmra_options opt;
+    srmra_default_options(&opt);
+    if (opt_in) opt = *opt_in;
+    if (L_high <= 0 || L_low <= 0 || K <= 0 || n_local < 0)
+        return fail(c, SRMRA_ERR_INVALID_ARG, "sizes must be positive (n_local >= 0)");
+    if ((int64_t)K * L_low != L_high) return fail(c, SRMRA_ERR_INVALID_ARG, "K * L_low != L_high");
+    if (!(sigma > 0) || !isfinite(sigma)) return fail(c, SRMRA_ERR_INVALID_ARG, "sigma must be finite and > 0");
+    if (!x0 || !rho1_0 || !rho2_0 || (n_local > 0 && !y)) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
+    if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(c, SRMRA_ERR_INVALID_ARG, "bad rank/world");
+    if (opt.world > 1 && !opt.nccl_id) return fail(c, SRMRA_ERR_INVALID_ARG, "world > 1 needs nccl_id");
+    if (opt.proj_every < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "proj_every < 0");
+    if (opt.trace_cap < 1) opt.trace_cap = 4096;
+    if (!all_finite_f(x0, (size_t)L_high * L_high)) return fail(c, SRMRA_ERR_INVALID_ARG, "x0 not finite");
+    if (n_local > 0 && !all_finite_f(y, (size_t)n_local * L_low * L_low))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
+    std::vector<double> r1, r2;
+    if (check_rho(rho1_0, L_high, r1) || check_rho(rho2_0, L_high, r2))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "rho must be >= 0, finite and sum to 1 (within 1e-6)");
+    if (K * K > 256 || L_high > 4096) return fail(c, SRMRA_ERR_UNSUPPORTED, "K^2 > 256 or L_high > 4096");
+    const int path = choose_path(opt.path, L_high, L_low, K);
+    if (path < 0) return fail(c, SRMRA_ERR_UNSUPPORTED, "no compiled path supports this shape / path request");
+
+    int dev = opt.device;
+    cudaError_t ce;
+    if (dev < 0) {
+        if ((ce = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(c, ce, "cudaGetDevice");
+    }
+    cudaDeviceProp prop;
+    if ((ce = cudaGetDeviceProperties(&prop, dev)) != cudaSuccess) return cuda_fail(c, ce, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(c, SRMRA_ERR_UNSUPPORTED, "libsrmra is built for sm_100a (B200); device is sm_" +
+                                                  std::to_string(prop.major) + std::to_string(prop.minor));
+    if ((ce = cudaSetDevice(dev)) != cudaSuccess) return cuda_fail(c, ce, "cudaSetDevice");
+
+    c = new srmra_ctx();
+    c->opt = opt;
+    c->device = dev;
+    c->num_sms = prop.multiProcessorCount;
+    c->L = L_high; c->Ll = L_low; c->K = K; c->KK = K * K;
+    c->L2 = L_high * L_high; c->Ll2 = L_low * L_low; c->Lh = L_low / 2 + 1;
+    c->n_local = n_local;
+    c->sigma = sigma;
+    c->inv_s2 = 1.0 / (sigma * sigma);
+    c->inv_2s2 = 0.5 / (sigma * sigma);
+    c->path = path;
+    c->pk.b = 0;
+    c->pk.cmass = c->L2;
+    c->pk.m1 = c->pk.cmass + c->KK;
+    c->pk.m2 = c->pk.m1 + c->L;
+    c->pk.ll = c->pk.m2 + c->L;
+    c->pk.total = c->pk.ll + 1;
+
+    auto bail = [&](int code) { g_init_err = c->err; srmra_free(c); return code; };
+    int rc;
+#define CKI(call)                                                                   \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) return bail(cuda_fail(c, e_, #call));               \
+    } while (0)
+
+    if (opt.stream) {
+        c->stream = (cudaStream_t)opt.stream;
+    } else {
+        CKI(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    const size_t ny = (size_t)n_local * c->Ll2;
+    CKI(dalloc(&c->d_y, ny));
+    CKI(dalloc(&c->d_ynorm, n_local));
+    CKI(dalloc(&c->d_llobs, n_local));
+    CKI(dalloc(&c->d_x64, c->L2));
+    CKI(dalloc(&c->d_x32, c->L2));
+    CKI(dalloc(&c->d_xtmp, c->L2));
+    CKI(dalloc(&c->d_rho, 2 * c->L));
+    CKI(dalloc(&c->par.f32, 2 * c->L + c->KK));
+    CKI(dalloc(&c->par.f64, c->KK + 2));
+    CKI(dalloc(&c->d_colsum, c->L2));
+    CKI(dalloc(&c->d_pack, c->pk.total));
+    CKI(dalloc(&c->d_trace, opt.trace_cap));
+    CKI(dalloc(&c->d_flag, 1));
+    if (path == SRMRA_PATH_FFT) {
+        CKI(dalloc(&c->d_yhat, (size_t)n_local * c->Ll * c->Lh));
+        CKI(dalloc(&c->d_xhat, (size_t)c->KK * c->Ll * c->Lh));
+        CKI(dalloc(&c->d_bhat, (size_t)c->KK * c->Ll * c->Lh * 2));
+    }
+    CKI(cudaMemsetAsync(c->d_llobs, 0, sizeof(double) * (n_local ? n_local : 1), c->stream));
+
+    // global N and the NCCL communicator
+    c->n_global = n_local;
+    if (opt.world > 1) {
+        NcclApi& api = nccl();
+        if (!api.loaded) return bail(fail(c, SRMRA_ERR_NCCL, api.err));
+        ncclUniqueId id;
+        memcpy(&id, opt.nccl_id, sizeof(id));
+        ncclComm_t comm;
+        ncclResult_t r = api.CommInitRank(&comm, opt.world, id, opt.rank);
+        if (r != ncclSuccess) return bail(fail(c, SRMRA_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
+        c->nccl_comm = comm;
+        double* d_n = c->d_pack;  // scratch for the one-off N all-reduce
+        double hn = (double)n_local;
+        CKI(cudaMemcpyAsync(d_n, &hn, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        r = api.AllReduce(d_n, d_n, 1, ncclFloat64, ncclSum, comm, c->stream);
+        if (r != ncclSuccess) return bail(fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce(N): ") + api.GetErrorString(r)));
+        CKI(cudaMemcpyAsync(&hn, d_n, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CKI(cudaStreamSynchronize(c->stream));
+        c->n_global = (int64_t)llround(hn);
+    }
+    c->tau = opt.floor_tau >= 0 ? opt.floor_tau : 1e-12 * (double)c->n_global;
+
+    if ((rc = upload(c, y, x0, r1, r2)) != SRMRA_OK) return bail(rc);
+    *out = c;
+    return SRMRA_OK;
+}
+
+int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1_0, const double* rho2_0) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (!x0 || !rho1_0 || !rho2_0 || (c->n_local > 0 && !y)) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
+    if (!all_finite_f(x0, (size_t)c->L2)) return fail(c, SRMRA_ERR_INVALID_ARG, "x0 not finite");
+    if (c->n_local > 0 && !all_finite_f(y, (size_t)c->n_local * c->Ll2)) return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
+    std::vector<double> r1, r2;
+    if (check_rho(rho1_0, c->L, r1) || check_rho(rho2_0, c->L, r2))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "rho must be >= 0, finite and sum to 1 (within 1e-6)");
+    return upload(c, y, x0, r1, r2);
+}
+
+int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
+    for (int it = 0; it < n_iters; ++it) {
+        const int t = c->iters_done;
+        int rc;
+        if ((rc = record(c)) != SRMRA_OK) return rc;
+        if ((rc = local_estep_mstep(c)) != SRMRA_OK) return rc;
+        if ((rc = allreduce_pack(c)) != SRMRA_OK) return rc;
+        const int F = c->opt.proj_every;
+        const int project = F > 0 && ((t + 1) % F == 0);
+        CK(launch_finalize(c, t, project));
+        if ((rc = record(c)) != SRMRA_OK) return rc;
+        c->iters_done++;
+    }
+    return SRMRA_OK;
+}
+
+int srmra_profile(srmra_ctx* c, int32_t enable) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    CK(cudaStreamSynchronize(c->stream));
+    c->prof = enable != 0;
+    c->ev_used = 0;
+    return SRMRA_OK;
+}
+
+int srmra_profile_read(srmra_ctx* c, double* em_ms, double* iter_ms, int32_t* n_iters) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    CK(cudaStreamSynchronize(c->stream));
+    double em = 0, tot = 0;
+    int n = 0;
+    for (size_t k = 0; k + 4 <= c->ev_used; k += 4, ++n) {
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, c->ev_pool[k + 1], c->ev_pool[k + 2]));
+        CK(cudaEventElapsedTime(&b, c->ev_pool[k], c->ev_pool[k + 3]));
+        em += a;
+        tot += b;
+    }
+    c->ev_used = 0;
+    if (em_ms) *em_ms = em;
+    if (iter_ms) *iter_ms = tot;
+    if (n_iters) *n_iters = n;
+    return SRMRA_OK;
+}
+
+int srmra_get_estimate(srmra_ctx* c, float* x_out, double* rho1_out, double* rho2_out, double* loglik_out,
+                       int32_t* iters_done) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x32, sizeof(float) * c->L2, cudaMemcpyDeviceToHost, c->stream));
+    if (rho1_out) CK(cudaMemcpyAsync(rho1_out, c->d_rho, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
+    if (rho2_out) CK(cudaMemcpyAsync(rho2_out, c->d_rho + c->L, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
+    double ll = NAN;
+    int flag = 0;
+    const int t = c->iters_done;
+    if (t > 0 && t <= c->opt.trace_cap)
+        CK(cudaMemcpyAsync(&ll, c->d_trace + (t - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (loglik_out) *loglik_out = ll;
+    if (iters_done) *iters_done = t;
+    if (flag) return fail(c, SRMRA_ERR_NUMERIC, "non-finite log-likelihood or estimate");
+    return SRMRA_OK;
+}
+
+int srmra_get_loglik_trace(srmra_ctx* c, double* out, int32_t cap, int32_t* n) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    int m = c->iters_done < c->opt.trace_cap ? c->iters_done : c->opt.trace_cap;
+    if (m > cap) m = cap;
+    if (m > 0 && out) CK(cudaMemcpyAsync(out, c->d_trace, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (n) *n = c->iters_done;
+    return SRMRA_OK;
+}
+
+int srmra_get_stats(srmra_ctx* c, double* b, double* cmass, double* m1, double* m2) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (b) CK(cudaMemcpyAsync(b, c->d_pack + c->pk.b, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream));
+    if (cmass) CK(cudaMemcpyAsync(cmass, c->d_pack + c->pk.cmass, sizeof(double) * c->KK, cudaMemcpyDeviceToHost, c->stream));
+    if (m1) CK(cudaMemcpyAsync(m1, c->d_pack + c->pk.m1, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
+    if (m2) CK(cudaMemcpyAsync(m2, c->d_pack + c->pk.m2, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
+
+int srmra_get_obs_loglik(srmra_ctx* c, double* out) {
+    if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (c->n_local) CK(cudaMemcpyAsync(out, c->d_llobs, sizeof(double) * c->n_local, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
+
+int srmra_local_stats(srmra_ctx* c, double* out) {
+    if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
+    if (c->failed) return SRMRA_ERR_STATE;
+    const bool prof = c->prof;
+    c->prof = false;  // keep the profiling records aligned to whole iterations
+    int rc = local_estep_mstep(c);
+    c->prof = prof;
+    if (rc != SRMRA_OK) return rc;
+    CK(cudaMemcpyAsync(out, c->d_pack, sizeof(double) * c->pk.total, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
+
+int srmra_get_path(const srmra_ctx* c) { return c ? c->path : SRMRA_ERR_INVALID_ARG; }
+
+int srmra_launches_per_iter(const srmra_ctx* c) {
+    if (!c) return SRMRA_ERR_INVALID_ARG;
+    int n = 3;  // prep, pack, finalize
+    if (c->path == SRMRA_PATH_DIRECT) n += c->n_local > 0 ? 1 : 0;
+    if (c->path == SRMRA_PATH_FFT) n += fft_launches_per_iter(c);
+    return n;
+}
+
+void srmra_free(srmra_ctx* c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->nccl_comm) {
+        NcclApi& api = nccl();
+        if (api.loaded) api.CommDestroy((ncclComm_t)c->nccl_comm);
+    }
+    void* bufs[] = {c->d_y, c->d_yhat, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
+                    c->par.f32, c->par.f64, c->d_xhat, c->d_colsum, c->d_bhat, c->d_pack, c->d_trace, c->d_flag};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// srmra_internal.cuh — context layout, launch declarations and device helpers shared by the
+// kernels of libsrmra.so.  Notation follows PAPER.md §I/§II-C and SURVEY.md §8(a):
+//   L = L_high, Ll = L_low, K = L/Ll, s = (s1, s2) in Z_L^2 flattened s1*L + s2,
+//   class r(s) = (s1 mod K, s2 mod K), low-res shift t(s) = (s1 / K, s2 / K), s = r + K t,
+//   polyphase component x_r[m] = x[(K m1 - r1) mod L, (K m2 - r2) mod L]   (PAPER.md:127-131,
+//   relabelled), so that (P R_s x)[n] = x_r[n - t] and ||P R_s x||^2 = E_r := ||x_r||^2.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/srmra.h"
+
+namespace srmra {
+
+// Per-iteration small parameters, written by k_prep and read by the E/M kernels.
+// fp32 part (bias of the logits) and fp64 part (constants of the log-likelihood).
+struct IterParams {
+    // float32 (device), laid out contiguously: lr1[L] | lr2[L] | beta[K^2]
+    float* f32;
+    // float64 (device): E[K^2] | E_min | (unused)
+    double* f64;
+};
+
+struct PackLayout {  // packed statistics  b | class_mass | marg1 | marg2 | LL
+    int64_t b, cmass, m1, m2, ll, total;
+};
+
+}  // namespace srmra
+
+struct srmra_ctx {
+    // shape
+    int L = 0, Ll = 0, K = 0, KK = 0, L2 = 0, Ll2 = 0, Lh = 0;  // Lh = Ll/2+1 (rfft width)
+    int64_t n_local = 0, n_global = 0;
+    double sigma = 0, inv_s2 = 0, inv_2s2 = 0, tau = 0;
+    srmra_options opt{};
+    int path = 0;
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool failed = false;
+    std::string err;
+
+    // observation-side buffers (this rank's shard)
+    float* d_y = nullptr;       // [n][Ll][Ll]             (direct / gemm paths)
+    float2* d_yhat = nullptr;   // [n][Ll][Lh]             (fft path: rfft2 of y_i, float32)
+    double* d_ynorm = nullptr;  // [n]  ||y_i||^2, float64
+    double* d_llobs = nullptr;  // [n]  per-observation log-likelihood of the last iteration
+
+    // theta
+    double* d_x64 = nullptr;  // [L2]
+    float* d_x32 = nullptr;   // [L2]
+    double* d_rho = nullptr;  // [2L] rho1 | rho2
+    double* d_xtmp = nullptr; // [L2] finalize scratch
+
+    // per-iteration
+    srmra::IterParams par{};
+    float2* d_xhat = nullptr;   // [KK][Ll][Lh] rfft2 of x_r (fft path)
+    double* d_colsum = nullptr; // [L2] sum_i w^{i,s}
+    double* d_bhat = nullptr;   // [KK][Ll][Lh][2] frequency-domain numerator (fft path)
+    double* d_pack = nullptr;   // packed statistics, see PackLayout
+    srmra::PackLayout pk{};
+    double* d_trace = nullptr;  // [trace_cap]
+    int* d_flag = nullptr;      // [1] numeric error flag
+    int iters_done = 0;
+
+    // multi-GPU
+    void* nccl_comm = nullptr;
+
+    // profiling (srmra_profile): per-iteration event quadruples
+    //   [iteration start, E/M kernel start, E/M kernel end, iteration end]
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t prof_event();
+};
+
+namespace srmra {
+
+// ---------------------------------------------------------------- launches (k_common.cu)
+cudaError_t launch_init_obs(srmra_ctx* c);      // ||y||^2 (+ Yhat for the fft path)
+cudaError_t launch_prep(srmra_ctx* c);          // theta -> IterParams (+ Xhat), zero accumulators
+cudaError_t launch_pack(srmra_ctx* c);          // colsum (+ Bhat) -> packed b | cmass | marg | LL
+cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
+// ---------------------------------------------------------------- path kernels
+cudaError_t launch_direct_em(srmra_ctx* c);     // k_direct.cu
+bool direct_supported(int L, int Ll, int K);
+cudaError_t launch_fft_em(srmra_ctx* c);        // k_fft.cu
+bool fft_supported(int L, int Ll, int K);
+cudaError_t launch_fft_init(srmra_ctx* c);
+cudaError_t launch_fft_prep(srmra_ctx* c);
+cudaError_t launch_fft_fold(srmra_ctx* c);
+int fft_launches_per_iter(const srmra_ctx* c);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ int imod(int a, int m) {
+    int r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide reductions; `scratch` must hold >= 32 elements of T; all threads get the result.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    T r = lane < nw ? scratch[lane] : T(0);
+    r = warp_sum(r);
+    return r;
+}
+template <typename T>
+__device__ __forceinline__ T block_max(T v, T* scratch, T neg_inf) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    T r = lane < nw ? scratch[lane] : neg_inf;
+    r = warp_max(r);
+    return r;
+}
+
+}  // namespace srmra

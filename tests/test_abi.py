@@ -1,0 +1,56 @@
+"""CPU checks of the C-ABI library: it builds, loads, and exports every symbol include/srmra.h
+declares (no compute calls: there is no GPU here)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "srmra.h")).read()
+    return sorted(set(re.findall(r"SRMRA_API\s+[\w\s\*]*?\b(srmra_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("srmra_init", "srmra_em_iter", "srmra_get_estimate", "srmra_free", "srmra_last_error"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2204_04754_b200._build as b
+    lib_path = b.build()
+    lib = ctypes.CDLL(lib_path)
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    import paper_2204_04754_b200 as m
+    assert sorted(m.ABI_SYMBOLS) == declared_symbols()
+
+
+def test_options_defaults_and_validation_without_gpu():
+    import numpy as np
+    import paper_2204_04754_b200 as m
+    o = m.srmra_default_options()
+    assert (o.path, o.proj_every, o.floor_tau, o.world, o.rank, o.trace_cap) == (0, 1, -1.0, 1, 0, 4096)
+    # argument validation happens before any device call
+    y = np.zeros((3, 4, 4), np.float32)
+    for kw, code in [(dict(K=3), m.SRMRA_ERR_INVALID_ARG), (dict(sigma=-1.0), m.SRMRA_ERR_INVALID_ARG)]:
+        a = dict(y=y, L_high=8, L_low=4, K=2, sigma=0.5, x0=np.zeros((8, 8)), rho1_0=np.ones(8) / 8,
+                 rho2_0=np.ones(8) / 8)
+        a.update(kw)
+        try:
+            m.Context(**a)
+            raise AssertionError("accepted invalid arguments")
+        except m.SrmraError as e:
+            assert e.code == code
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports or links the oracle."""
+    pkg = os.path.join(ROOT, "paper_2204_04754_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "liboracle" not in txt and "srmra_oracle" not in txt, f

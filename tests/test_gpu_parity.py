@@ -1,0 +1,205 @@
+"""GPU parity: libsrmra.so (through the C ABI) vs the float64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star; rho tolerance from DESIGN.md reading R10):
+  x    : max|x_gpu - x_oracle| / max|x_oracle|         <= 1e-4
+  LL   : |LL_gpu - LL_oracle| / |LL_oracle|            <= 1e-6
+  rho  : max|rho_gpu - rho_oracle| / max rho_oracle    <= 1e-4   (per axis)
+"""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+X_TOL, LL_TOL, RHO_TOL = 1e-4, 1e-6, 1e-4
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def srm():
+    import paper_2204_04754_b200 as m
+    return m
+
+
+def gpu_paths(srm, p):
+    """Paths that accept this shape (AUTO is always included)."""
+    out = []
+    for path in ("direct", "fft", "gemm"):
+        try:
+            with srm.Context(p.y[:1], p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path):
+                out.append(path)
+        except srm.SrmraError as e:
+            assert e.code == srm.SRMRA_ERR_UNSUPPORTED, e
+    return out
+
+
+def run_gpu(srm, p, path, iters, proj_every=1):
+    with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path,
+                     proj_every=proj_every) as ctx:
+        ctx.em_iter(iters)
+        x, r1, r2, ll, it = ctx.get_estimate()
+        assert it == iters
+        trace = ctx.loglik_trace()
+        b, cm, m1, m2 = ctx.stats()
+        llo = ctx.obs_loglik()
+        used = ctx.path
+    return dict(x=x, rho1=r1, rho2=r2, ll=ll, trace=trace, b=b, cm=cm, m1=m1, m2=m2, llo=llo, path=used)
+
+
+def assert_close(g, x, r1, r2, trace, tag=""):
+    xe = np.abs(g["x"].astype(np.float64) - x).max() / np.abs(x).max()
+    r1e = np.abs(g["rho1"] - r1).max() / r1.max()
+    r2e = np.abs(g["rho2"] - r2).max() / r2.max()
+    lle = np.max(np.abs(np.asarray(g["trace"]) - np.asarray(trace)) / np.abs(np.asarray(trace)))
+    msg = f"{tag} path={g['path']} x_err={xe:.2e} rho_err={max(r1e, r2e):.2e} ll_err={lle:.2e}"
+    print(msg)
+    assert xe <= X_TOL, msg
+    assert r1e <= RHO_TOL and r2e <= RHO_TOL, msg
+    assert lle <= LL_TOL, msg
+    return xe, max(r1e, r2e), lle
+
+
+TINY = [  # (L_low, K, N, sigma, seed, rho_zeros)
+    (2, 2, 37, 0.7, 0, 0), (4, 2, 41, 0.4, 1, 2), (8, 2, 33, 0.3, 2, 0), (2, 4, 29, 0.5, 3, 1),
+    (4, 4, 31, 0.25, 4, 0), (8, 1, 17, 0.5, 5, 0), (16, 1, 9, 0.6, 6, 3), (1, 4, 23, 0.5, 7, 0),
+    (16, 2, 19, 0.2, 8, 0), (32, 2, 11, 0.25, 9, 0), (8, 4, 13, 0.125, 10, 2),
+]
+
+
+@pytest.mark.parametrize("case", TINY, ids=[f"Ll{c[0]}K{c[1]}N{c[2]}" for c in TINY])
+def test_tiny_shapes_all_paths(srm, oracle_mod, case):
+    Ll, K, N, sigma, seed, zeros = case
+    p = synth.make_random(Ll, K, N, sigma, seed, rho_zeros=zeros)
+    paths = gpu_paths(srm, p)
+    assert paths, "no path accepts this shape"
+    ref = oracle_mod.em_iter(p.y, Ll, K, sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    for path in paths:
+        g = run_gpu(srm, p, path, 1)
+        assert_close(g, ref.x, ref.rho1, ref.rho2, [ref.loglik], tag=str(case))
+        # statistics and per-observation terms
+        np.testing.assert_allclose(g["llo"], ref.ll_obs, rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(g["b"], ref.b, rtol=0, atol=X_TOL * np.abs(ref.b).max())
+        cm_ref = np.array([[ref.colsum[r1::K, r2::K].sum() for r2 in range(K)] for r1 in range(K)])
+        np.testing.assert_allclose(g["cm"], cm_ref, rtol=0, atol=RHO_TOL * cm_ref.max())
+        np.testing.assert_allclose(g["m1"], ref.colsum.sum(1), rtol=0, atol=RHO_TOL * ref.colsum.sum(1).max())
+        np.testing.assert_allclose(g["m2"], ref.colsum.sum(0), rtol=0, atol=RHO_TOL * ref.colsum.sum(0).max())
+        # zero prior mass stays exactly zero
+        assert np.all(g["rho1"][p.rho1_0 == 0] == 0) and np.all(g["rho2"][p.rho2_0 == 0] == 0)
+
+
+def test_c0_full(srm, oracle_mod):
+    p = synth.make_config("c0")
+    ref = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    for path in gpu_paths(srm, p):
+        g = run_gpu(srm, p, path, 1)
+        assert_close(g, ref.x, ref.rho1, ref.rho2, [ref.loglik], tag="c0")
+
+
+def test_c0_monotone_no_projection(srm):
+    """EM ascent through the GPU path with projection off."""
+    p = synth.make_config("c0")
+    for path in gpu_paths(srm, p):
+        g = run_gpu(srm, p, path, 15, proj_every=0)
+        tr = g["trace"]
+        assert np.all(np.diff(tr) >= -1e-6 * np.abs(tr[:-1])), tr
+
+
+def test_c1_reduced_three_iters(srm, oracle_mod):
+    p = synth.make_config("c1", N=1000)
+    x, r1, r2, trace = oracle_mod.run(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, iters=3, proj_every=1)
+    for path in gpu_paths(srm, p):
+        g = run_gpu(srm, p, path, 3)
+        assert_close(g, x, r1, r2, trace, tag="c1/N=1000")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_full_config_vs_golden(srm, name):
+    f = os.path.join(GOLDEN, f"{name}_oracle.npz")
+    if not os.path.exists(f):
+        pytest.skip(f"{f} not generated (tests/golden/make_golden.py)")
+    gold = np.load(f)
+    p = synth.make_config(name)
+    for path in gpu_paths(srm, p):
+        g = run_gpu(srm, p, path, int(gold["iters"]))
+        assert_close(g, gold["x"], gold["rho1"], gold["rho2"], gold["trace"], tag=name)
+
+
+def test_invariants_mass_conservation(srm):
+    """sum_p b[p] = sum_{i,n} y_i[n] and sum_r class_mass = N hold for any x."""
+    p = synth.make_config("c1", N=3001)
+    for path in gpu_paths(srm, p):
+        g = run_gpu(srm, p, path, 1)
+        ysum = p.y.astype(np.float64).sum()
+        assert abs(g["b"].sum() - ysum) <= 1e-6 * np.abs(p.y).sum()
+        assert abs(g["cm"].sum() - p.N) <= 1e-9 * p.N
+        assert abs(g["rho1"].sum() - 1) < 1e-12 and abs(g["rho2"].sum() - 1) < 1e-12
+
+
+def test_empty_shard(srm, oracle_mod):
+    """n_local = 0: no statistics; x keeps x0 (coverage 0 <= tau) then is projected; rho unchanged."""
+    p = synth.make_random(4, 2, 5, 0.5, 1)
+    y0 = p.y[:0]
+    with srm.Context(y0, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0) as ctx:
+        ctx.em_iter(1)
+        x, r1, r2, ll, it = ctx.get_estimate()
+    assert ll == 0.0
+    np.testing.assert_allclose(x, oracle_mod.project(p.x0.astype(np.float64)), atol=1e-7)
+    np.testing.assert_allclose(r1, p.rho1_0, rtol=1e-15)
+
+
+def test_shard_statistics_sum(srm):
+    """Loopback sharding: the local statistics of two disjoint shards sum to those of the whole set
+    (the quantity the NCCL all-reduce forms)."""
+    p = synth.make_config("c1", N=777)
+    for path in gpu_paths(srm, p):
+        parts = []
+        for sl in (slice(0, 400), slice(400, None)):
+            with srm.Context(p.y[sl], p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path) as c:
+                parts.append(c.local_stats())
+        with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path) as c:
+            full = c.local_stats()
+        np.testing.assert_allclose(parts[0] + parts[1], full, rtol=1e-6, atol=1e-6 * np.abs(full).max())
+
+
+def test_load_reuses_context(srm):
+    a = synth.make_config("c0")
+    b = synth.make_config("c0", seed_offset=100)
+    with srm.Context(a.y, a.L_high, a.L_low, a.K, a.sigma, a.x0, a.rho1_0, a.rho2_0) as ctx:
+        ctx.em_iter(2)
+        ctx.load(b.y, b.x0, b.rho1_0, b.rho2_0)
+        ctx.em_iter(1)
+        xb, *_ = ctx.get_estimate()
+        assert ctx.loglik_trace().shape == (1,)
+    with srm.Context(b.y, b.L_high, b.L_low, b.K, b.sigma, b.x0, b.rho1_0, b.rho2_0) as ctx:
+        ctx.em_iter(1)
+        xf, *_ = ctx.get_estimate()
+    np.testing.assert_allclose(xb, xf, atol=1e-6)
+
+
+def test_invalid_arguments(srm):
+    p = synth.make_random(4, 2, 5, 0.5, 1)
+    args = dict(y=p.y, L_high=p.L_high, L_low=p.L_low, K=p.K, sigma=p.sigma, x0=p.x0, rho1_0=p.rho1_0,
+                rho2_0=p.rho2_0)
+    bad = [dict(K=3), dict(sigma=0.0), dict(sigma=float("nan")), dict(rho1_0=p.rho1_0 * 2),
+           dict(rho2_0=-p.rho2_0)]
+    for b in bad:
+        a = dict(args, **b)
+        with pytest.raises(srm.SrmraError) as ei:
+            srm.Context(**a)
+        assert ei.value.code == srm.SRMRA_ERR_INVALID_ARG
+    y = p.y.copy(); y[0, 0, 0] = np.inf
+    with pytest.raises(srm.SrmraError):
+        srm.Context(**dict(args, y=y))
+
+
+def test_torch_stream(srm):
+    torch = pytest.importorskip("torch")
+    p = synth.make_config("c0")
+    s = torch.cuda.Stream()
+    with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, stream=s.cuda_stream) as ctx:
+        ctx.em_iter(2)
+        x, *_ = ctx.get_estimate()
+    assert np.all(np.isfinite(x))
