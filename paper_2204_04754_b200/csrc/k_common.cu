@@ -85,7 +85,9 @@ __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ 
 
 cudaError_t launch_prep(srmra_ctx* c) {
     cudaError_t e;
-    if ((e = cudaMemsetAsync(c->d_colsum, 0, sizeof(double) * c->L2, c->stream)) != cudaSuccess) return e;
+    if (c->path == SRMRA_PATH_DIRECT &&
+        (e = cudaMemsetAsync(c->d_colsum, 0, sizeof(double) * c->L2, c->stream)) != cudaSuccess)
+        return e;
     if ((e = cudaMemsetAsync(c->d_pack, 0, sizeof(double) * c->pk.total, c->stream)) != cudaSuccess) return e;
     k_prep<<<1, 1024, 0, c->stream>>>(c->d_x64, c->d_rho, c->L, c->K, c->inv_2s2, c->par.f32, c->par.f64);
     return cudaGetLastError();
@@ -139,18 +141,32 @@ __global__ void k_finalize(const double* __restrict__ pack, int64_t off_cm, int6
     __syncthreads();
     double tot = 0.0;
     for (int r = 0; r < KK; ++r) tot += cm[r];   // sum_i sum_s' w^{i,s'} (eq:rho_EM denominator)
-    // rho' (eq:rho_EM, separable marginals)
+    // rho' (eq:rho_EM, separable marginals).  A shift with rho_t = 0 has w = 0 for every observation,
+    // so its marginal is exactly 0 (kept exact here; the frequency-domain path would otherwise leave
+    // rounding noise there); other marginals are clamped at 0 and each axis is normalised by its own
+    // total sum_i sum_s w (the eq:rho_EM denominator) so that sum rho = 1 to rounding.
+    double m1s = 0.0, m2s = 0.0;
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
-        if (tot > 0.0) {
-            rho[k] = pack[off_m1 + k] / tot;
-            rho[L + k] = pack[off_m2 + k] / tot;
+        m1s += rho[k] == 0.0 ? 0.0 : fmax(pack[off_m1 + k], 0.0);
+        m2s += rho[L + k] == 0.0 ? 0.0 : fmax(pack[off_m2 + k], 0.0);
+    }
+    m1s = block_sum(m1s, red);
+    m2s = block_sum(m2s, red);
+    __syncthreads();  // every thread has read rho_t above
+    if (tot > 0.0 && m1s > 0.0 && m2s > 0.0) {
+        for (int k = threadIdx.x; k < L; k += blockDim.x) {
+            rho[k] = rho[k] == 0.0 ? 0.0 : fmax(pack[off_m1 + k], 0.0) / m1s;
+            rho[L + k] = rho[L + k] == 0.0 ? 0.0 : fmax(pack[off_m2 + k], 0.0) / m2s;
         }
     }
-    // x' = b / A (eq:x_EM, A diagonal; A[p] = class mass of class (-p mod K)); keep x_t if A <= tau
-    double* dst = project ? xtmp : x64;
+    // x' = b / A (eq:x_EM, A diagonal; A[p] = class mass of class (-p mod K)); keep x_t if A <= tau.
+    // With projection, x' is staged in shared memory when it fits (L^2 <= 16384), else in xtmp.
+    extern __shared__ double xs_dyn[];
+    double* stage = L2 <= 16384 ? xs_dyn : xtmp;
+    double* dst = project ? stage : x64;
     int bad = 0;
     for (int p = threadIdx.x; p < L2; p += blockDim.x) {
-        const int p1 = p / L, p2 = p % L;
+        const int p1 = p / L, p2 = p - p1 * L;
         const double A = cm[imod(-p1, K) * K + imod(-p2, K)];
         const double v = A > tau ? pack[p] / A : x64[p];
         dst[p] = v;
@@ -158,14 +174,14 @@ __global__ void k_finalize(const double* __restrict__ pack, int64_t off_cm, int6
         bad |= !isfinite(v);
     }
     if (project) {
-        __syncthreads();  // xtmp complete (global writes of this block are visible after the barrier)
+        __syncthreads();  // stage complete (global writes of this block are visible after the barrier too)
         for (int p = threadIdx.x; p < L2; p += blockDim.x) {
-            const int p1 = p / L, p2 = p % L;
-            double acc = 0.0;
-#pragma unroll
-            for (int d1 = -1; d1 <= 1; ++d1)
-#pragma unroll
-                for (int d2 = -1; d2 <= 1; ++d2) acc += xtmp[(size_t)imod(p1 + d1, L) * L + imod(p2 + d2, L)];
+            const int p1 = p / L, p2 = p - p1 * L;
+            const int rm = (p1 == 0 ? L - 1 : p1 - 1) * L, r0 = p1 * L, rp = (p1 == L - 1 ? 0 : p1 + 1) * L;
+            const int cm1 = p2 == 0 ? L - 1 : p2 - 1, cp1 = p2 == L - 1 ? 0 : p2 + 1;
+            double acc = stage[rm + cm1] + stage[rm + p2] + stage[rm + cp1];
+            acc += stage[r0 + cm1] + stage[r0 + p2] + stage[r0 + cp1];
+            acc += stage[rp + cm1] + stage[rp + p2] + stage[rp + cp1];
             double v = acc / 9.0;
             v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
             x64[p] = v;
@@ -181,7 +197,14 @@ __global__ void k_finalize(const double* __restrict__ pack, int64_t off_cm, int6
 }
 
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project) {
-    k_finalize<<<1, 1024, 0, c->stream>>>(c->d_pack, c->pk.cmass, c->pk.m1, c->pk.m2, c->pk.ll, c->L, c->K,
+    const size_t sm = c->L2 <= 16384 ? sizeof(double) * c->L2 : 0;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_finalize<<<1, 1024, sm, c->stream>>>(c->d_pack, c->pk.cmass, c->pk.m1, c->pk.m2, c->pk.ll, c->L, c->K,
                                           c->tau, project, c->d_x64, c->d_x32, c->d_rho, c->d_xtmp,
                                           c->d_trace, t, c->opt.trace_cap, c->d_flag);
     return cudaGetLastError();

@@ -157,21 +157,21 @@ int record(srmra_ctx* c) {
 // With profiling on, events bracket the dominant E/M kernel (records 2 and 3 of the quadruple).
 int local_estep_mstep(srmra_ctx* c) {
     int rc;
-    CK(launch_prep(c));
     if (c->path == SRMRA_PATH_FFT) {
-        CK(launch_fft_prep(c));
+        CK(launch_fft_prep(c));  // logit bias + Xhat in one launch
         if ((rc = record(c))) return rc;
         CK(launch_fft_em(c));
         if ((rc = record(c))) return rc;
-        CK(launch_fft_fold(c));
+        CK(launch_fft_fold(c));  // reduce + fold: b, class mass, marginals, LL into the pack
     } else if (c->path == SRMRA_PATH_DIRECT) {
+        CK(launch_prep(c));
         if ((rc = record(c))) return rc;
         CK(launch_direct_em(c));
         if ((rc = record(c))) return rc;
+        CK(launch_pack(c));
     } else {
         return fail(c, SRMRA_ERR_UNSUPPORTED, "path not available");
     }
-    CK(launch_pack(c));
     return SRMRA_OK;
 }
 
@@ -294,9 +294,19 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->d_trace, opt.trace_cap));
     CKI(dalloc(&c->d_flag, 1));
     if (path == SRMRA_PATH_FFT) {
-        CKI(dalloc(&c->d_yhat, (size_t)n_local * c->Ll * c->Lh));
+        CKI(dalloc(&c->d_yhat, (size_t)n_local * fft_yhat_stride(c->Ll)));
         CKI(dalloc(&c->d_xhat, (size_t)c->KK * c->Ll * c->Lh));
-        CKI(dalloc(&c->d_bhat, (size_t)c->KK * c->Ll * c->Lh * 2));
+        CKI(dalloc(&c->d_bhat, fft_bhat_doubles(c->KK, c->Ll)));
+        CKI(fft_plan(c));
+        std::vector<double> tw(2 * (size_t)c->Ll);  // cos / sin (2 pi j / L_low), float64
+        for (int j = 0; j < c->Ll; ++j) {
+            tw[j] = cos(2.0 * M_PI * j / c->Ll);
+            tw[c->Ll + j] = sin(2.0 * M_PI * j / c->Ll);
+        }
+        CKI(dalloc(&c->d_tw, tw.size()));
+        CKI(cudaMemcpy(c->d_tw, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
+        CKI(dalloc(&c->d_part, fft_part_float2(c)));
+        CKI(dalloc(&c->d_llpart, c->fft_grid));
     }
     CKI(cudaMemsetAsync(c->d_llobs, 0, sizeof(double) * (n_local ? n_local : 1), c->stream));
 
@@ -454,8 +464,8 @@ int srmra_get_path(const srmra_ctx* c) { return c ? c->path : SRMRA_ERR_INVALID_
 
 int srmra_launches_per_iter(const srmra_ctx* c) {
     if (!c) return SRMRA_ERR_INVALID_ARG;
-    int n = 3;  // prep, pack, finalize
-    if (c->path == SRMRA_PATH_DIRECT) n += c->n_local > 0 ? 1 : 0;
+    int n = 1;  // finalize
+    if (c->path == SRMRA_PATH_DIRECT) n += 2 + (c->n_local > 0 ? 1 : 0);  // prep, pack, em
     if (c->path == SRMRA_PATH_FFT) n += fft_launches_per_iter(c);
     return n;
 }
@@ -468,7 +478,8 @@ void srmra_free(srmra_ctx* c) {
         if (api.loaded) api.CommDestroy((ncclComm_t)c->nccl_comm);
     }
     void* bufs[] = {c->d_y, c->d_yhat, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
-                    c->par.f32, c->par.f64, c->d_xhat, c->d_colsum, c->d_bhat, c->d_pack, c->d_trace, c->d_flag};
+                    c->par.f32, c->par.f64, c->d_xhat, c->d_colsum, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
+                    c->d_part, c->d_llpart, c->d_tw};
     for (void* p : bufs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

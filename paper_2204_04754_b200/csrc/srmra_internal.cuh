@@ -60,7 +60,12 @@ struct srmra_ctx {
     srmra::IterParams par{};
     float2* d_xhat = nullptr;   // [KK][Ll][Lh] rfft2 of x_r (fft path)
     double* d_colsum = nullptr; // [L2] sum_i w^{i,s}
-    double* d_bhat = nullptr;   // [KK][Ll][Lh][2] frequency-domain numerator (fft path)
+    double* d_bhat = nullptr;   // fft path, float64: Bhat [KK][Ll][Lh] complex | mass lines [KK][Ll+Lh] complex
+    float2* d_part = nullptr;   // fft path: per-CTA float32 partials of the above [fft_grid][...]
+    double* d_llpart = nullptr; // fft path: per-CTA log-likelihood partials [fft_grid]
+    double* d_tw = nullptr;     // fft path: cos | sin (2 pi j / L_low), j < L_low, float64
+    int fft_grid = 0, fft_groups = 0, fft_threads = 0;
+    size_t fft_smem = 0;
     double* d_pack = nullptr;   // packed statistics, see PackLayout
     srmra::PackLayout pk{};
     double* d_trace = nullptr;  // [trace_cap]
@@ -94,6 +99,10 @@ cudaError_t launch_fft_init(srmra_ctx* c);
 cudaError_t launch_fft_prep(srmra_ctx* c);
 cudaError_t launch_fft_fold(srmra_ctx* c);
 int fft_launches_per_iter(const srmra_ctx* c);
+size_t fft_bhat_doubles(int KK, int Ll);  // Bhat [KK][Ll][Lh] complex + mass lines [KK][Ll+Lh] complex
+size_t fft_yhat_stride(int Ll);           // float2 per observation in d_yhat (16-byte multiple)
+cudaError_t fft_plan(srmra_ctx* c);       // grid / groups / smem of the E/M kernel for this shard
+size_t fft_part_float2(const srmra_ctx* c);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ int imod(int a, int m) {

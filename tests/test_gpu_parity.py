@@ -134,7 +134,7 @@ def test_invariants_mass_conservation(srm):
         g = run_gpu(srm, p, path, 1)
         ysum = p.y.astype(np.float64).sum()
         assert abs(g["b"].sum() - ysum) <= 1e-6 * np.abs(p.y).sum()
-        assert abs(g["cm"].sum() - p.N) <= 1e-9 * p.N
+        assert abs(g["cm"].sum() - p.N) <= 1e-6 * p.N   # float32 accumulation per CTA
         assert abs(g["rho1"].sum() - 1) < 1e-12 and abs(g["rho2"].sum() - 1) < 1e-12
 
 
