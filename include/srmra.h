@@ -149,6 +149,11 @@ SRMRA_API int srmra_profile(srmra_ctx* ctx, int32_t enable);
  * and the number of iterations (*n_iters).  Any pointer may be NULL.  Clears the records. */
 SRMRA_API int srmra_profile_read(srmra_ctx* ctx, double* em_kernel_ms, double* iter_ms, int32_t* n_iters);
 
+/* Debug hook: globaltimer stamps (ns) of the FFT path's tail-kernel phase boundaries of the last
+ * iteration, out8[0..5] = start, fold, update, projection, prep, end (0 where a phase did not run).
+ * Requires the environment variable SRMRA_TAIL_STAMPS to be set at srmra_init (else SRMRA_ERR_STATE). */
+SRMRA_API int srmra_debug_timestamps(srmra_ctx* ctx, uint64_t* out8);
+
 /* Write a fresh 128-byte ncclUniqueId into out (rank 0 calls this before srmra_init). */
 SRMRA_API int srmra_nccl_unique_id(void* out128);
 

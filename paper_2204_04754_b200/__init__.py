@@ -31,7 +31,7 @@ PATH_IDS = {v: k for k, v in PATH_NAMES.items()}
 # every symbol include/srmra.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_iter", "srmra_get_estimate",
                "srmra_get_loglik_trace", "srmra_get_stats", "srmra_get_obs_loglik", "srmra_local_stats",
-               "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read",
+               "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
                "srmra_last_error")
 
@@ -74,6 +74,7 @@ def _load():
         "srmra_launches_per_iter": (ctypes.c_int, [_ctxp]),
         "srmra_profile": (ctypes.c_int, [_ctxp, ctypes.c_int32]),
         "srmra_profile_read": (ctypes.c_int, [_ctxp, _dp, _dp, _ip]),
+        "srmra_debug_timestamps": (ctypes.c_int, [_ctxp, ctypes.POINTER(ctypes.c_uint64)]),
         "srmra_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
         "srmra_free": (None, [_ctxp]),
         "srmra_last_error": (ctypes.c_char_p, [_ctxp]),
@@ -192,6 +193,12 @@ def srmra_profile_read(ctx):
     n = ctypes.c_int32()
     _check(_lib.srmra_profile_read(ctx, ctypes.byref(em), ctypes.byref(it), ctypes.byref(n)), ctx)
     return em.value, it.value, n.value
+
+
+def srmra_debug_timestamps(ctx):
+    out = np.zeros(8, dtype=np.uint64)
+    _check(_lib.srmra_debug_timestamps(ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))), ctx)
+    return out
 
 
 def srmra_free(ctx):

@@ -23,6 +23,7 @@
 // path; Bhat is accumulated per CTA in shared memory (float32) and added to the float64 global
 // accumulator once at the end.
 #include <math.h>
+#include <stdlib.h>
 
 #include <utility>
 
@@ -159,14 +160,14 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 struct EmArgs {
     const float2* yhat;     // [n][ystride] rfft2(y_i), float32 (ystride = Ll*Lh rounded up to even)
     const double* ynorm;    // [n]
-    const float2* xhat;     // [KK][Ll][Lh] rfft2(x_r) / Ll^2
-    const float* par32;     // lr1[L] | lr2[L] | beta[KK]
+    const float4* xhat;     // [NP][Ll][Lh] pair-interleaved: (Xhat_{2q}, Xhat_{2q+1}) / Ll^2
+    const float* par32;     // log2 units: lr1[L] | lr2[L] | beta[KK]
     const double* par64;    // E[KK] | E_min
     int64_t n;
     int L, K, KK, ystride, groups;
-    float inv_s2f;
+    float c2;               // log2(e) / sigma^2
     double inv_s2, inv_2s2;
-    float2* part;           // [gridDim.x][PB] per-CTA partials: Bhat [KK][Ll][Lh] | mass lines [KK][Ll+Lh]
+    float2* part;           // [gridDim.x][PB] per-CTA partials, see part_bins()
     double* llpart;         // [gridDim.x] per-CTA log-likelihood partials
     double* llobs;          // [n]
 };
@@ -182,32 +183,84 @@ __host__ __device__ constexpr int group_threads(int KK) {
     return ((((KK + 1) / 2) * LL + 31) / 32) * 32;
 }
 
-// Shared memory of one group (16-B multiple):
-//   Yb [2][ystride] | Wk [NP][LL][WS] | Bs [KK][LL][LH] | Cs [KK][LL+LH] (float2) | red [32] (double)
-// Every group owns its own Bhat / mass-line accumulators, so the bin pass needs no atomics.
+// Accumulators (float2) of one group / one CTA partial, NP = ceil(K^2 / 2) class pairs:
+//   UV [NP][2][Ll][Lh]  U_q[k] = sum_i Yhat_i[k] conj(Z_{i,q}[k]),  V_q[k] = sum_i Yhat_i[k] Z_{i,q}[-k]
+//                       (Z_{i,q} = What_{i,2q} + i What_{i,2q+1}: Bhat_{2q} = (U+V)/2, Bhat_{2q+1} = i(U-V)/2)
+//   R  [KK][Ll]         spatial row sums of the posterior, sum_i sum_t2 w_{i,r}[t1, t2]  (real in .x)
+//   CU [NP][Ll]         sum_i Z_{i,q}[0][k2]  (k1 = 0 row of the transformed posterior pair)
+__host__ __device__ inline int part_bins(int KK, int LL) {
+    const int NP = (KK + 1) / 2, LH = LL / 2 + 1;
+    return 2 * NP * LL * LH + KK * LL + NP * LL;
+}
+
+// Shared memory of one group (16-B multiple): Yb [2][ystride] | Wk [NP][LL][WS] | Acc [part_bins] | red [32]
 template <int LL>
 __host__ __device__ inline size_t group_smem(int KK, int ystride) {
     using G = Geo<LL>;
     const int NP = (KK + 1) / 2;
-    size_t b = sizeof(float2) * (2 * (size_t)ystride + (size_t)NP * LL * G::WS + (size_t)KK * LL * G::LH +
-                                 (size_t)KK * (LL + G::LH)) + sizeof(double) * 32;
+    size_t b = sizeof(float2) * (2 * (size_t)ystride + (size_t)NP * LL * G::WS + (size_t)part_bins(KK, LL)) +
+               sizeof(double) * 32;
     return (b + 15) & ~(size_t)15;
 }
 template <int LL>
+__host__ __device__ inline size_t par_bytes(int KK) {  // logit-bias table lr1 | lr2 | beta, L = K LL <= 8 LL
+    return ((size_t)(2 * 8 * LL + KK) * sizeof(float) + 15) & ~(size_t)15;
+}
+template <int LL>
 __host__ __device__ inline size_t smem_bytes(int KK, int groups, int ystride) {
-    return group_smem<LL>(KK, ystride) * groups;
+    return group_smem<LL>(KK, ystride) * groups + par_bytes<LL>(KK);
 }
 
 // Threads per CTA cap (register budget: one L_low-point complex line per thread lives in registers)
 template <int LL>
 __host__ __device__ constexpr int max_cta_threads() {
-    return LL >= 64 ? 256 : (LL >= 32 ? 384 : (LL >= 16 ? 512 : 1024));
+    return LL >= 64 ? 256 : (LL >= 32 ? 320 : 512);
 }
 
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// (max, scaled sum) pair reduction over the group: (m1, z1) + (m2, z2) = (M, z1 2^(m1-M) + z2 2^(m2-M))
+__device__ __forceinline__ void ms_combine(float& m, float& z, float m2, float z2) {
+    const float M = fmaxf(m, m2);
+    if (M == -INFINITY) return;  // both empty
+    z = z * ex2(m - M) + z2 * ex2(m2 - M);
+    m = M;
+}
+__device__ __forceinline__ void group_reduce_ms(float& m, float& z, float2* scratch, int gwarp, int nwarps, int lane,
+                                                int bar_id, int gthreads) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float z2 = __shfl_xor_sync(0xffffffffu, z, o);
+        ms_combine(m, z, m2, z2);
+    }
+    if (nwarps == 1) return;
+    if (lane == 0) scratch[gwarp] = make_float2(m, z);
+    group_bar(bar_id, gthreads);
+    float M = scratch[0].x, Zs = scratch[0].y;
+    for (int w = 1; w < nwarps; ++w) ms_combine(M, Zs, scratch[w].x, scratch[w].y);
+    group_bar(bar_id, gthreads);
+    m = M;
+    z = Zs;
+}
+
+// PAIRS = true when K^2 is even (every complex transform carries two classes); for odd K^2 the
+// imaginary half of the last pair is empty.
+// XS = true: the pair-interleaved Xhat of this iteration is staged once per CTA in shared memory
+// (ahead of the group areas) instead of being read through L1 in the E-step product.
 template <int LL>
+__host__ __device__ inline size_t xs_bytes(int KK) {
+    return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (LL / 2 + 1);
+}
+
+template <int LL, bool PAIRS, bool XS>
 __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
     using G = Geo<LL>;
-    constexpr int LH = G::LH, WS = G::WS;
+    constexpr int LH = G::LH, WS = G::WS, M = LL - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int KK = a.KK, K = a.K, L = a.L;
     const int NP = (KK + 1) / 2;
@@ -218,35 +271,53 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
     const int gwarp = tg >> 5, nwarps = GT >> 5;
     const int bar_id = 1 + g;
 
-    // ---- shared layout
+    // ---- shared layout: par table | [Xhat (XS)] | group 0 | group 1 | ...
+    float* pars = reinterpret_cast<float*>(smem_raw);
+    const size_t pb = par_bytes<LL>(KK);
+    const size_t xsb = XS ? xs_bytes<LL>(KK) : 0;
+    unsigned char* gbase = smem_raw + pb + xsb;
+    for (int k = threadIdx.x; k < 2 * L + KK; k += blockDim.x) pars[k] = __ldg(a.par32 + k);
+    if (XS) {
+        const float4* src = a.xhat;
+        float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
+        for (int k = threadIdx.x; k < NP * LL * LH; k += blockDim.x) dst[k] = __ldg(src + k);
+    }
+    __syncthreads();
     const size_t per_g = group_smem<LL>(KK, a.ystride);
-    float2* Yb = reinterpret_cast<float2*>(smem_raw + per_g * g);      // [2][ystride]
+    const int PB = part_bins(KK, LL);
+    float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [2][ystride]
     float2* Wk = Yb + 2 * a.ystride;                                    // [NP][LL][WS]
-    float2* Bs = Wk + (size_t)NP * LL * WS;                             // [KK][LL][LH]
-    float2* Cs = Bs + (size_t)KK * LL * LH;                             // [KK][LL + LH]
-    double* red = reinterpret_cast<double*>(Cs + (size_t)KK * (LL + LH));  // [32]
+    float2* Acc = Wk + (size_t)NP * LL * WS;                            // [PB]
+    double* red = reinterpret_cast<double*>(Acc + PB);                  // [32]
     float* redf = reinterpret_cast<float*>(red);
+    float2* red2 = reinterpret_cast<float2*>(red);
+    for (int k = tg; k < 2 * NP * LL * LH; k += GT) Acc[k] = make_float2(0.f, 0.f);
 
-    for (int k = tg; k < KK * LL * LH; k += GT) Bs[k] = make_float2(0.f, 0.f);
-    for (int k = tg; k < KK * (LL + LH); k += GT) Cs[k] = make_float2(0.f, 0.f);
-    group_bar(bar_id, GT);
-
-    const float* lr1 = a.par32;
-    const float* lr2 = a.par32 + L;
-    const float* beta = a.par32 + 2 * L;
+    const float* lr1 = pars;
+    const float* lr2 = pars + L;
+    const float* beta = pars + 2 * L;
     const double emin = a.par64[KK];
 
-    // line owned by this thread in the row / column passes: pair q, index idx
+    // line owned by this thread in every pass: pair q, index idx (column k2 / row n1 / column c)
     const bool line_ok = tg < NP * LL;
     const int q = line_ok ? tg / LL : 0;
     const int idx = line_ok ? tg - q * LL : 0;
     const int ra = 2 * q, rb = 2 * q + 1;
-    const bool has_b = rb < KK;
-    const float2* XA = a.xhat + (size_t)ra * LL * LH;
-    const float2* XB = a.xhat + (size_t)(has_b ? rb : ra) * LL * LH;
+    const bool has_b = PAIRS || rb < KK;
+    const float4* XP = (XS ? reinterpret_cast<const float4*>(smem_raw + pb) : a.xhat) + (size_t)q * LL * LH;
     float2* Wq = Wk + (size_t)q * LL * WS;
+    float2* Uq = Acc + (size_t)(2 * q) * LL * LH;
+    float2* Vq = Uq + (size_t)LL * LH;
+    const int ra2 = ra % K, rb2 = rb % K;
+    // logit bias (log2 units) of this thread's row n1 = idx, per class
+    const float biasA = line_ok ? lr1[ra / K + K * idx] + beta[ra] : 0.f;
+    const float biasB = (line_ok && has_b) ? lr1[rb / K + K * idx] + beta[rb] : 0.f;
 
+    // per-thread accumulators over this group's observations
+    float rsumA = 0.f, rsumB = 0.f;     // row sums of w (class ra / rb, row idx)
+    float2 cu = make_float2(0.f, 0.f);  // sum_i Z_{i,q}[0][idx]
     double ll_acc = 0.0;
+
     const int64_t gstride = (int64_t)gridDim.x * a.groups;
     int64_t i = (int64_t)blockIdx.x * a.groups + g;
     int buf = 0;
@@ -267,144 +338,153 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
         const float2* Y = Yb + buf * a.ystride;
 
         float2 v[LL];
-        // ================= E-step, pass 1: product + inverse FFT along k1 (column k2 = idx)
-        if (line_ok) {
-            const int k2 = idx;
-            // columns k2 >= LH come from the stored half by Hermitian symmetry: A[k] = conj(A[-k])
-            const bool flip = k2 >= LH;
-            const int sk2 = flip ? LL - k2 : k2;
-            const float sgn = flip ? -1.f : 1.f;
+        float sref = 0.f, mall = 0.f, zall = 1.f;
+        // Four 1-D transform passes share ONE register FFT (forward); the two inverse passes use
+        // ifft(z) = conj(fft(conj(z))), with the conjugations folded into the loads / score read-out.
+#pragma unroll 1
+        for (int pass = 0; pass < 4; ++pass) {
+            if (line_ok) {
+                if (pass == 0) {
+                    // E-step along k1 (column k2 = idx): conj of Z = Yhat conj(Xhat_ra) + i Yhat conj(Xhat_rb);
+                    // columns k2 >= LH by Hermitian symmetry from the stored half
+                    const int k2 = idx;
+                    const bool flip = k2 >= LH;
+                    const int sk2 = flip ? LL - k2 : k2;
+                    const float sgn = flip ? -1.f : 1.f;
 #pragma unroll
-            for (int k1 = 0; k1 < LL; ++k1) {
-                const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
-                const int o = sk1 * LH + sk2;
-                const float2 yv = Y[o];
-                const float2 A = cmul_conj(yv, __ldg(XA + o));
-                float2 B = make_float2(0.f, 0.f);
-                if (has_b) B = cmul_conj(yv, __ldg(XB + o));
-                // Z = A + i B with A, B conjugated on the mirrored half
-                v[k1] = make_float2(A.x - sgn * B.y, sgn * A.y + B.x);
+                    for (int k1 = 0; k1 < LL; ++k1) {
+                        const int sk1 = flip ? ((LL - k1) & M) : k1;
+                        const int o = sk1 * LH + sk2;
+                        const float2 yv = Y[o];
+                        const float4 xv = XS ? XP[o] : __ldg(XP + o);
+                        const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
+                        const float2 B = cmul_conj(yv, make_float2(xv.z, xv.w));
+                        v[k1] = make_float2(A.x - sgn * B.y, -sgn * A.y - B.x);
+                    }
+                } else if (pass == 1) {
+                    // E-step along k2 (row n1 = idx) of the conjugated column result
+#pragma unroll
+                    for (int k2 = 0; k2 < LL; ++k2) v[k2] = Wq[idx * WS + k2];
+                } else if (pass == 3) {
+                    // M-step along n1 (column c = idx)
+#pragma unroll
+                    for (int r = 0; r < LL; ++r) v[r] = Wq[r * WS + idx];
+                }
+                // pass 2: v holds the posterior row w of the pair (forward transform along n2)
+                fft<LL, -1>(v);
+                if (pass == 0) {
+#pragma unroll
+                    for (int k1 = 0; k1 < LL; ++k1) Wq[k1 * WS + idx] = v[k1];
+                } else if (pass == 2) {
+#pragma unroll
+                    for (int k2 = 0; k2 < LL; ++k2) Wq[idx * WS + k2] = v[k2];
+                } else if (pass == 3) {
+                    // v[k1] = Z[k1][c]: accumulate U (c < LH), V at column k2 = -c (c == 0 or c >= LL/2)
+                    const int c = idx;
+                    if (c < LH) {
+#pragma unroll
+                        for (int k1 = 0; k1 < LL; ++k1) {
+                            const float2 yv = Y[k1 * LH + c];
+                            const float2 u = cmul_conj(yv, v[k1]);
+                            Uq[k1 * LH + c] = make_float2(Uq[k1 * LH + c].x + u.x, Uq[k1 * LH + c].y + u.y);
+                        }
+                    }
+                    if (c == 0 || 2 * c >= LL) {
+                        const int k2 = (LL - c) & M;
+#pragma unroll
+                        for (int k1 = 0; k1 < LL; ++k1) {
+                            const float2 yv = Y[k1 * LH + k2];
+                            const float2 z = v[(LL - k1) & M];
+                            const float2 w = make_float2(fmaf(yv.x, z.x, -yv.y * z.y), fmaf(yv.x, z.y, yv.y * z.x));
+                            Vq[k1 * LH + k2] = make_float2(Vq[k1 * LH + k2].x + w.x, Vq[k1 * LH + k2].y + w.y);
+                        }
+                    }
+                    cu.x += v[0].x;
+                    cu.y += v[0].y;
+                }
             }
-            fft<LL, +1>(v);
+            if (pass == 1) {
+                // ---- scores S_ra = Re, S_rb = -Im (inverse via conjugation); row reference Sref
+                float lmax = -INFINITY;
+                if (line_ok) {
 #pragma unroll
-            for (int n1 = 0; n1 < LL; ++n1) Wq[n1 * WS + k2] = v[n1];
-        }
-        group_bar(bar_id, GT);
-        // ================= E-step, pass 2: inverse FFT along k2 (row n1 = idx) -> scores
-        const int n1 = idx;
-        float lmax = -INFINITY;
-        if (line_ok) {
+                    for (int n2 = 0; n2 < LL; ++n2) {
+                        v[n2].y = -v[n2].y;
+                        lmax = fmaxf(lmax, has_b ? fmaxf(v[n2].x, v[n2].y) : v[n2].x);
+                    }
+                }
+                sref = group_reduce<float, true>(lmax, redf, gwarp, nwarps, lane, bar_id, GT);
+                // ---- posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e/sigma^2 + bias
+                float mt = -INFINITY, za = 0.f, zb = 0.f;
+                if (line_ok) {
 #pragma unroll
-            for (int k2 = 0; k2 < LL; ++k2) v[k2] = Wq[n1 * WS + k2];
-            fft<LL, +1>(v);   // v[n2] = (S_ra[n1][n2], S_rb[n1][n2])
+                    for (int n2 = 0; n2 < LL; ++n2) {
+                        const float va = fmaf(v[n2].x - sref, a.c2, biasA + lr2[ra2 + K * n2]);
+                        const float vb = has_b ? fmaf(v[n2].y - sref, a.c2, biasB + lr2[rb2 + K * n2]) : -INFINITY;
+                        v[n2] = make_float2(va, vb);
+                        mt = fmaxf(mt, fmaxf(va, vb));
+                    }
+                    // a row whose shifts all have zero prior mass has mt = -inf: its weights are exactly 0
+                    const float mref = mt == -INFINITY ? 0.f : mt;
 #pragma unroll
-            for (int n2 = 0; n2 < LL; ++n2) lmax = fmaxf(lmax, has_b ? fmaxf(v[n2].x, v[n2].y) : v[n2].x);
-        }
-        const float sref = group_reduce<float, true>(lmax, redf, gwarp, nwarps, lane, bar_id, GT);
-        // ================= posterior (eq:weights_EM), logits in the form of k_common.cu
-        const int ra1 = ra / K, ra2 = ra - ra1 * K;
-        const int rb1 = rb / K, rb2 = rb - rb1 * K;
-        float vmax = -INFINITY;
-        if (line_ok) {
-            const float biasA = lr1[ra1 + K * n1] + beta[ra];
-            const float biasB = has_b ? lr1[rb1 + K * n1] + beta[rb] : -INFINITY;
+                    for (int n2 = 0; n2 < LL; ++n2) {
+                        const float ea = ex2(v[n2].x - mref);
+                        const float eb = has_b ? ex2(v[n2].y - mref) : 0.f;
+                        v[n2] = make_float2(ea, eb);
+                        za += ea;
+                        zb += eb;
+                    }
+                }
+                mall = mt;
+                zall = za + zb;
+                group_reduce_ms(mall, zall, red2, gwarp, nwarps, lane, bar_id, GT);
+                if (line_ok) {
+                    const float f = ex2(mt - mall) / zall;  // w = e 2^(mt - M) / Z
+                    rsumA = fmaf(za, f, rsumA);
+                    rsumB = fmaf(zb, f, rsumB);
 #pragma unroll
-            for (int n2 = 0; n2 < LL; ++n2) {
-                const float va = fmaf(v[n2].x - sref, a.inv_s2f, biasA + lr2[ra2 + K * n2]);
-                const float vb = has_b ? fmaf(v[n2].y - sref, a.inv_s2f, biasB + lr2[rb2 + K * n2]) : -INFINITY;
-                v[n2] = make_float2(va, vb);
-                vmax = fmaxf(vmax, fmaxf(va, vb));
+                    for (int n2 = 0; n2 < LL; ++n2) v[n2] = make_float2(v[n2].x * f, v[n2].y * f);
+                }
             }
+            if (pass == 0 || pass == 2) group_bar(bar_id, GT);  // Wq complete before the next reader
         }
-        const float m = group_reduce<float, true>(vmax, redf, gwarp, nwarps, lane, bar_id, GT);
-        float zs = 0.f;
-        if (line_ok) {
-#pragma unroll
-            for (int n2 = 0; n2 < LL; ++n2) {
-                const float ea = __expf(v[n2].x - m);
-                const float eb = has_b ? __expf(v[n2].y - m) : 0.f;
-                v[n2] = make_float2(ea, eb);
-                zs += ea + eb;
-            }
-        }
-        const double Z = group_reduce<double, false>((double)zs, red, gwarp, nwarps, lane, bar_id, GT);
         if (tg == 0) {
-            const double lse = (double)sref * a.inv_s2 + (double)m + log(Z) - (emin + a.ynorm[i]) * a.inv_2s2;
+            const double lse = 0.69314718055994530942 * ((double)mall + log2((double)zall)) +
+                               (double)sref * a.inv_s2 - (emin + a.ynorm[i]) * a.inv_2s2;
             ll_acc += lse;
             if (a.llobs) a.llobs[i] = lse;
         }
-        const float invZ = (float)(1.0 / Z);
-        // ================= M-step, pass 1: forward FFT of the posterior rows (n1 = idx)
-        if (line_ok) {
-#pragma unroll
-            for (int n2 = 0; n2 < LL; ++n2) v[n2] = make_float2(v[n2].x * invZ, v[n2].y * invZ);
-            fft<LL, -1>(v);
-#pragma unroll
-            for (int k2 = 0; k2 < LL; ++k2) Wq[n1 * WS + k2] = v[k2];
-        }
-        group_bar(bar_id, GT);
-        // ================= M-step, pass 2: forward FFT along n1 (column k2 = idx)
-        if (line_ok) {
-            const int k2 = idx;
-#pragma unroll
-            for (int r = 0; r < LL; ++r) v[r] = Wq[r * WS + k2];
-            fft<LL, -1>(v);
-#pragma unroll
-            for (int k1 = 0; k1 < LL; ++k1) Wq[k1 * WS + k2] = v[k1];
-        }
-        group_bar(bar_id, GT);
-        // ================= M-step, pass 3: separate the pair, accumulate Bhat and the mass lines
-        for (int bin = tg; bin < NP * LL * LH; bin += GT) {
-            const int qq = bin / (LL * LH);
-            const int rem = bin - qq * LL * LH;
-            const int k1 = rem / LH, k2 = rem - (rem / LH) * LH;
-            const float2* W = Wk + (size_t)qq * LL * WS;
-            const float2 za = W[k1 * WS + k2];
-            const float2 zb = W[((LL - k1) & (LL - 1)) * WS + ((LL - k2) & (LL - 1))];
-            const float2 wa = make_float2(0.5f * (za.x + zb.x), 0.5f * (za.y - zb.y));   // (Z + conj Z-)/2
-            const float2 wb = make_float2(0.5f * (za.y + zb.y), 0.5f * (zb.x - za.x));   // (Z - conj Z-)/2i
-            const float2 yv = Y[k1 * LH + k2];
-            // each bin of this group is owned by exactly one of its threads: plain read-modify-write
-            const int rA = 2 * qq, rB = 2 * qq + 1;
-            const float2 ba = cmul_conj(yv, wa);
-            float2* BA = Bs + (size_t)rA * LL * LH + rem;
-            *BA = make_float2(BA->x + ba.x, BA->y + ba.y);
-            float2* CA = Cs + (size_t)rA * (LL + LH);
-            if (k2 == 0) CA[k1] = make_float2(CA[k1].x + wa.x, CA[k1].y + wa.y);
-            if (k1 == 0) CA[LL + k2] = make_float2(CA[LL + k2].x + wa.x, CA[LL + k2].y + wa.y);
-            if (rB < KK) {
-                const float2 bb = cmul_conj(yv, wb);
-                float2* BB = Bs + (size_t)rB * LL * LH + rem;
-                *BB = make_float2(BB->x + bb.x, BB->y + bb.y);
-                float2* CB = Cs + (size_t)rB * (LL + LH);
-                if (k2 == 0) CB[k1] = make_float2(CB[k1].x + wb.x, CB[k1].y + wb.y);
-                if (k1 == 0) CB[LL + k2] = make_float2(CB[LL + k2].x + wb.x, CB[LL + k2].y + wb.y);
-            }
-        }
-        group_bar(bar_id, GT);
+        group_bar(bar_id, GT);  // everyone done with Yb[buf] and Wq before they are refilled
         buf ^= 1;
     }
     cp_async_wait0();
+    // register accumulators -> this group's R / CU regions
+    float2* R = Acc + 2 * NP * LL * LH;   // [KK][LL]
+    float2* CU = R + KK * LL;             // [NP][LL]
+    if (line_ok) {
+        R[ra * LL + idx] = make_float2(rsumA, 0.f);
+        if (has_b) R[rb * LL + idx] = make_float2(rsumB, 0.f);
+        CU[q * LL + idx] = cu;
+    }
     if (tg == 0) red[31] = ll_acc;
     __syncthreads();
-    // CTA partial (sum over groups in a fixed order) -> global partial slot of this CTA; the reduce
-    // kernel sums the slots in a fixed order (deterministic, no atomics)
-    const int PB = KK * LL * LH + KK * (LL + LH);
+    // CTA partial (sum over groups in a fixed order) -> global slot of this CTA; the reduce kernel sums
+    // the slots in a fixed order (deterministic, no atomics)
     float2* dst = a.part + (size_t)blockIdx.x * PB;
     for (int k = threadIdx.x; k < PB; k += blockDim.x) {
         float2 s = make_float2(0.f, 0.f);
         for (int gg = 0; gg < a.groups; ++gg) {
-            const float2* B0 = reinterpret_cast<const float2*>(smem_raw + per_g * gg) + 2 * a.ystride + (size_t)NP * LL * WS;
-            s.x += B0[k].x;
-            s.y += B0[k].y;
+            const float2* A0 = reinterpret_cast<const float2*>(gbase + per_g * gg) + 2 * a.ystride + (size_t)NP * LL * WS;
+            s.x += A0[k].x;
+            s.y += A0[k].y;
         }
         dst[k] = s;
     }
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int gg = 0; gg < a.groups; ++gg) {
-            const float2* B0 = reinterpret_cast<const float2*>(smem_raw + per_g * gg) + 2 * a.ystride + (size_t)NP * LL * WS;
-            s += reinterpret_cast<const double*>(B0 + PB)[31];
+            const float2* A0 = reinterpret_cast<const float2*>(gbase + per_g * gg) + 2 * a.ystride + (size_t)NP * LL * WS;
+            s += reinterpret_cast<const double*>(A0 + PB)[31];
         }
         a.llpart[blockIdx.x] = s;
     }
@@ -434,17 +514,29 @@ static cudaError_t plan_em_t(srmra_ctx* c) {
     if (GT > max_cta_threads<LL>()) return cudaErrorInvalidConfiguration;
     int groups = max_cta_threads<LL>() / GT;
     if (groups > 15) groups = 15;
-    // shared-memory budget: 227 KB per CTA
-    while (groups > 1 && smem_bytes<LL>(KK, groups, ys) > 227 * 1024) --groups;
+    const char* eg = getenv("SRMRA_FFT_GROUPS");  // tuning override
+    if (eg && atoi(eg) > 0 && atoi(eg) < groups) groups = atoi(eg);
+    // Xhat staged in shared memory unless that costs a group (SRMRA_FFT_XS=0/1 overrides)
+    const size_t xsb = xs_bytes<LL>(KK);
+    int g_plain = groups, g_xs = groups;
+    while (g_plain > 1 && smem_bytes<LL>(KK, g_plain, ys) > 227 * 1024) --g_plain;
+    while (g_xs > 1 && smem_bytes<LL>(KK, g_xs, ys) + xsb > 227 * 1024) --g_xs;
+    bool xs = g_xs == g_plain && smem_bytes<LL>(KK, g_xs, ys) + xsb <= 227 * 1024;
+    const char* ex = getenv("SRMRA_FFT_XS");
+    if (ex) xs = atoi(ex) != 0 && smem_bytes<LL>(KK, 1, ys) + xsb <= 227 * 1024;
+    groups = xs ? g_xs : g_plain;
     // keep enough CTAs for all SMs when N is small
     const int64_t need = (c->n_local + c->num_sms - 1) / c->num_sms;
     if (need < groups) groups = (int)(need < 1 ? 1 : need);
-    const size_t smem = smem_bytes<LL>(KK, groups, ys);
+    const size_t smem = smem_bytes<LL>(KK, groups, ys) + (xs ? xsb : 0);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(k_fft_em<LL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = (KK % 2 == 0) ? (xs ? k_fft_em<LL, true, true> : k_fft_em<LL, true, false>)
+                              : (xs ? k_fft_em<LL, false, true> : k_fft_em<LL, false, false>);
+    c->fft_xs = xs;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fft_em<LL>, GT * groups, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GT * groups, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t grid = (int64_t)c->num_sms * per_sm;
@@ -463,7 +555,7 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     EmArgs a;
     a.yhat = c->d_yhat;
     a.ynorm = c->d_ynorm;
-    a.xhat = c->d_xhat;
+    a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
     a.n = c->n_local;
@@ -472,18 +564,21 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     a.KK = c->KK;
     a.ystride = ystride_of(LL);
     a.groups = c->fft_groups;
-    a.inv_s2f = (float)c->inv_s2;
+    a.c2 = (float)(1.4426950408889634074 * c->inv_s2);
     a.inv_s2 = c->inv_s2;
     a.inv_2s2 = c->inv_2s2;
     a.part = c->d_part;
     a.llpart = c->d_llpart;
     a.llobs = c->d_llobs;
-    k_fft_em<LL><<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
+    auto kern = (c->KK % 2 == 0) ? (c->fft_xs ? k_fft_em<LL, true, true> : k_fft_em<LL, true, false>)
+                                 : (c->fft_xs ? k_fft_em<LL, false, true> : k_fft_em<LL, false, false>);
+    kern<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
     return cudaGetLastError();
 }
 
-int fft_partial_bins(int KK, int Ll) { return KK * Ll * (Ll / 2 + 1) + KK * (Ll + Ll / 2 + 1); }
-size_t fft_bhat_doubles(int KK, int Ll) { return (size_t)2 * fft_partial_bins(KK, Ll); }
+int fft_partial_bins(int KK, int Ll) { return part_bins(KK, Ll); }
+size_t fft_xhat_float2(int KK, int Ll) { return (size_t)2 * ((KK + 1) / 2) * Ll * (Ll / 2 + 1); }
+size_t fft_bhat_doubles(int KK, int Ll) { return (size_t)2 * fft_partial_bins(KK, Ll) + 1; }  // + LL
 size_t fft_yhat_stride(int Ll) { return (size_t)ystride_of(Ll); }
 size_t fft_part_float2(const srmra_ctx* c) { return (size_t)c->fft_grid * fft_partial_bins(c->KK, c->Ll); }
 
@@ -506,6 +601,7 @@ cudaError_t launch_fft_em(srmra_ctx* c) {
 }
 
 // prep, em, reduce, fold
-int fft_launches_per_iter(const srmra_ctx* c) { return 2 + (c->n_local > 0 ? 2 : 0); }
+// E/M kernel (if the shard is non-empty) + tail (+ a separate reduce-only tail when world > 1)
+int fft_launches_per_iter(const srmra_ctx* c) { return (c->n_local > 0 ? 1 : 0) + 1 + (c->opt.world > 1 ? 1 : 0); }
 
 }  // namespace srmra

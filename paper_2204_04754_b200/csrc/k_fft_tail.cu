@@ -1,0 +1,427 @@
+// k_fft_tail.cu — everything of an FFT-path iteration after the E/M kernel, as ONE cooperative
+// kernel whose phases are separated by grid-wide barriers (one launch instead of four latency-bound
+// single-block kernels).  All arithmetic is float64.
+//
+//   phase R  (a5)  fixed-order sum of the per-CTA float32 partials of k_fft_em (deterministic)
+//   phase F  (a5)  b_r = irfft2(Bhat_r) / L_low^2 scattered to b[(K m - r) mod L]   (eq:x_EM numerator,
+//                  PAPER.md:255-263 with P^{-1} := P^T), Bhat_{2q} = (U_q+V_q)/2, Bhat_{2q+1} = i(U_q-V_q)/2;
+//                  class mass, marginals (eq:rho_EM) and LL into the pack
+//   phase X  (a7)  rho' = marginals / total; x' = b / A (A = class mass of class (-p mod K)), keep x_t if A <= tau
+//   phase P  (a8)  projection x <- clamp(box3x3(x'), -1, 1)   (Algorithm 2 step 2)
+//   phase Q  (a1)  next iteration's Xhat_r = rfft2(x_r)/L_low^2 (pair-interleaved) and logit bias (log2 units)
+// With world > 1 the host runs phase R alone, all-reduces the accumulators over NCCL, then F..Q.
+#include <cooperative_groups.h>
+#include <math.h>
+
+#include "dft64.cuh"
+#include "srmra_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace srmra {
+
+int fft_partial_bins(int KK, int Ll);
+
+namespace ffttail {
+using namespace dft64;
+
+constexpr int kThreads = 256;
+constexpr int kSlices = kThreads / 32;
+
+struct TailArgs {
+    unsigned long long* stamps;  // optional phase timestamps (globaltimer, block 0), 8 entries
+    int mode;                 // TAIL_* bits
+    int L, K, t, project, trace_cap;
+    double tau, inv_2s2;
+    const float2* part;       // [nparts][PB] float32 partials
+    const double* llpart;     // [nparts]
+    int nparts, PB;
+    double* acc;              // [2 PB + 1] float64 accumulators (+ LL)
+    const double* tw;         // cos | sin (2 pi j / L_low)
+    double* pack;
+    int64_t off_cm, off_m1, off_m2, off_ll;
+    double *x64, *rho, *xtmp, *trace;
+    float* x32;
+    int* flag;
+    float2* xhat;             // [NP][Ll][Lh][2]
+    float* par32;             // log2 units: lr1 | lr2 | beta
+    double* par64;            // E | E_min
+    int nchunk;               // row chunks per class in phases F and Q
+};
+
+__device__ inline void grid_sync() { cg::this_grid().sync(); }
+
+// ---- phase R: bins in rounds of 32, kSlices threads per bin, 4 independent chains per thread
+__device__ void phase_reduce(const TailArgs& a) {
+    __shared__ double2 red[kSlices][33];
+    const int b = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    for (int base = blockIdx.x * 32; base < a.PB; base += gridDim.x * 32) {
+        const int k = base + b;
+        double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
+        if (k < a.PB) {
+            int c = sl;
+            for (; c + 3 * kSlices < a.nparts; c += 4 * kSlices) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 v = __ldcg(a.part + (size_t)(c + u * kSlices) * a.PB + k);
+                    sx[u] += v.x;
+                    sy[u] += v.y;
+                }
+            }
+            for (; c < a.nparts; c += kSlices) {
+                const float2 v = __ldcg(a.part + (size_t)c * a.PB + k);
+                sx[0] += v.x;
+                sy[0] += v.y;
+            }
+        }
+        red[sl][b] = make_double2((sx[0] + sx[1]) + (sx[2] + sx[3]), (sy[0] + sy[1]) + (sy[2] + sy[3]));
+        __syncthreads();
+        if (sl == 0 && k < a.PB) {
+            double tx = 0.0, ty = 0.0;
+            for (int j = 0; j < kSlices; ++j) {
+                tx += red[j][b].x;
+                ty += red[j][b].y;
+            }
+            a.acc[2 * k] = tx;
+            a.acc[2 * k + 1] = ty;
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && sl == 1) {  // LL partials: strided lanes then a fixed-order shuffle tree
+        double s = 0.0;
+        for (int c = b; c < a.nparts; c += 32) s += __ldcg(a.llpart + c);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (b == 0) a.acc[2 * a.PB] = s;
+    }
+}
+
+// ---- phase F: item (r, ch) -> rows [ch R, ch R + R) of b_r;  item KK*nchunk -> mass, marginals, LL
+__device__ void phase_fold(const TailArgs& a, double* sm) {
+    const int L = a.L, K = a.K, Ll = L / K, Lh = Ll / 2 + 1, KK = K * K, M = Ll - 1, NP = (KK + 1) / 2;
+    const int R = Ll / a.nchunk;
+    double* cs = sm;
+    double* sn = cs + Ll;
+    double2* B = reinterpret_cast<double2*>(sn + Ll);  // [Ll][Lh]
+    double2* T = B + Ll * Lh;                          // [R][Lh]
+    load_tw(a.tw, cs, sn, Ll);
+    const double2* A = reinterpret_cast<const double2*>(a.acc);
+    const int nitems = KK * a.nchunk + 1;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        __syncthreads();
+        if (item < KK * a.nchunk) {
+            const int r = item / a.nchunk, ch = item - r * a.nchunk, r1 = r / K, r2 = r % K;
+            const int m1a = ch * R;
+            const double2* U = A + (size_t)(r / 2) * 2 * Ll * Lh;
+            const double2* V = U + (size_t)Ll * Lh;
+            for (int e = threadIdx.x; e < Ll * Lh; e += blockDim.x) {
+                const double2 u = __ldcg(U + e), v = __ldcg(V + e);
+                B[e] = (r & 1) ? make_double2(-0.5 * (u.y - v.y), 0.5 * (u.x - v.x))
+                               : make_double2(0.5 * (u.x + v.x), 0.5 * (u.y + v.y));
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < R * Lh; e += blockDim.x) {  // inverse along k1
+                const int mm = e / Lh, k2 = e - mm * Lh, m1 = m1a + mm;
+                double re = 0, im = 0;
+                for (int k1 = 0; k1 < Ll; ++k1) {
+                    const int j = (k1 * m1) & M;
+                    const double2 t = B[k1 * Lh + k2];
+                    re += t.x * cs[j] - t.y * sn[j];
+                    im += t.y * cs[j] + t.x * sn[j];
+                }
+                T[e] = make_double2(re, im);
+            }
+            __syncthreads();
+            const double inv = 1.0 / ((double)Ll * Ll);
+            for (int e = threadIdx.x; e < R * Ll; e += blockDim.x) {  // c2r along k2
+                const int mm = e / Ll, m2 = e - mm * Ll, m1 = m1a + mm;
+                const double2* Tr = T + mm * Lh;
+                double s = Tr[0].x + ((m2 & 1) ? -Tr[Ll / 2].x : Tr[Ll / 2].x);
+                for (int k2 = 1; k2 < Ll / 2; ++k2) {
+                    const int j = (k2 * m2) & M;
+                    s += 2.0 * (Tr[k2].x * cs[j] - Tr[k2].y * sn[j]);
+                }
+                a.pack[(size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L)] = s * inv;
+            }
+        } else {
+            // staged in shared memory (the B / T area is free in this item): row sums R [KK][Ll] (real
+            // part) and the class row lines crow_r[k2], k2 <= Ll/2, separated from the pair lines
+            // CU [NP][Ll]: crow_{2q} = (CU[k] + conj CU[-k])/2, crow_{2q+1} = (CU[k] - conj CU[-k])/(2i)
+            const double2* Rg = A + (size_t)2 * NP * Ll * Lh;
+            const double2* CU = Rg + (size_t)KK * Ll;
+            double* Rs = reinterpret_cast<double*>(B);            // [KK][Ll]
+            double2* crow = reinterpret_cast<double2*>(Rs + KK * Ll);  // [KK][Lh]
+            if (threadIdx.x == 0) a.pack[a.off_ll] = __ldcg(a.acc + 2 * (size_t)a.PB);
+            for (int e = threadIdx.x; e < KK * Ll; e += blockDim.x) Rs[e] = __ldcg(&Rg[e].x);
+            for (int e = threadIdx.x; e < KK * Lh; e += blockDim.x) {
+                const int cls = e / Lh, k2 = e - cls * Lh, qq = cls / 2;
+                const double2 zp = __ldcg(CU + (size_t)qq * Ll + k2), zm = __ldcg(CU + (size_t)qq * Ll + ((Ll - k2) & M));
+                crow[e] = (cls & 1) ? make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x))
+                                    : make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+            }
+            __syncthreads();
+            for (int rr = threadIdx.x; rr < KK; rr += blockDim.x) {
+                double s = 0.0;
+                for (int t = 0; t < Ll; ++t) s += Rs[rr * Ll + t];
+                a.pack[a.off_cm + rr] = s;   // class mass sum_i sum_{s in class r} w^{i,s}
+            }
+            const double invL = 1.0 / Ll;
+            for (int s = threadIdx.x; s < L; s += blockDim.x) {
+                const int rs = s % K, t = s / K;
+                double a1 = 0.0, a2 = 0.0;
+                for (int ro = 0; ro < K; ++ro) {
+                    a1 += Rs[(rs * K + ro) * Ll + t];   // marg1[s] = sum_{r2} R_{(rs, r2)}[t]
+                    const double2* cr = crow + (ro * K + rs) * Lh;  // marg2[s] = sum_{r1} C_{(r1, rs)}[t]
+                    a2 += cr[0].x + ((t & 1) ? -cr[Ll / 2].x : cr[Ll / 2].x);
+                    for (int k2 = 1; k2 < Ll / 2; ++k2) {
+                        const int j = (k2 * t) & M;
+                        a2 += 2.0 * (cr[k2].x * cs[j] - cr[k2].y * sn[j]);
+                    }
+                }
+                a.pack[a.off_m1 + s] = a1;
+                a.pack[a.off_m2 + s] = a2 * invL;
+            }
+        }
+    }
+}
+
+// ---- phase X: rho' (block 0) and x' = b / A (grid-strided pixels)
+__device__ void phase_update(const TailArgs& a) {
+    __shared__ double red[32];
+    const int L = a.L, K = a.K, KK = K * K, L2 = L * L;
+    if (blockIdx.x == 0) {
+        // eq:rho_EM marginals; zero prior mass stays exactly zero; per-axis normalisation (finalize.cuh)
+        double m1s = 0.0, m2s = 0.0;
+        for (int k = threadIdx.x; k < L; k += blockDim.x) {
+            m1s += a.rho[k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m1 + k), 0.0);
+            m2s += a.rho[L + k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m2 + k), 0.0);
+        }
+        m1s = block_sum(m1s, red);
+        m2s = block_sum(m2s, red);
+        __syncthreads();
+        if (m1s > 0.0 && m2s > 0.0) {
+            for (int k = threadIdx.x; k < L; k += blockDim.x) {
+                a.rho[k] = a.rho[k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m1 + k), 0.0) / m1s;
+                a.rho[L + k] = a.rho[L + k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m2 + k), 0.0) / m2s;
+            }
+        }
+    }
+    int bad = 0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L2; p += gridDim.x * blockDim.x) {
+        const int p1 = p / L, p2 = p - p1 * L;
+        const double A = __ldcg(a.pack + a.off_cm + imod(-p1, K) * K + imod(-p2, K));
+        const double v = A > a.tau ? __ldcg(a.pack + p) / A : a.x64[p];
+        bad |= !isfinite(v);
+        if (a.project) {
+            a.xtmp[p] = v;
+        } else {
+            a.x64[p] = v;
+            a.x32[p] = (float)v;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flag, 1);
+    (void)KK;
+}
+
+// ---- phase P: projection D (3x3 circular box, clamp) and the LL trace
+__device__ void phase_project(const TailArgs& a) {
+    const int L = a.L, L2 = L * L;
+    if (a.project) {
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L2; p += gridDim.x * blockDim.x) {
+            const int p1 = p / L, p2 = p - p1 * L;
+            const int rm = (p1 == 0 ? L - 1 : p1 - 1) * L, r0 = p1 * L, rp = (p1 == L - 1 ? 0 : p1 + 1) * L;
+            const int cm1 = p2 == 0 ? L - 1 : p2 - 1, cp1 = p2 == L - 1 ? 0 : p2 + 1;
+            const double* s = a.xtmp;
+            double acc = __ldcg(s + rm + cm1) + __ldcg(s + rm + p2) + __ldcg(s + rm + cp1);
+            acc += __ldcg(s + r0 + cm1) + __ldcg(s + r0 + p2) + __ldcg(s + r0 + cp1);
+            acc += __ldcg(s + rp + cm1) + __ldcg(s + rp + p2) + __ldcg(s + rp + cp1);
+            double v = acc / 9.0;
+            v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+            a.x64[p] = v;
+            a.x32[p] = (float)v;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const double ll = __ldcg(a.pack + a.off_ll);
+        if (a.t < a.trace_cap) a.trace[a.t] = ll;
+        if (!isfinite(ll)) atomicOr(a.flag, 1);
+    }
+}
+
+// ---- phase Q: Xhat of the new x (items (r, ch)) and the logit bias (last item)
+__device__ void phase_prep(const TailArgs& a, double* sm) {
+    const int L = a.L, K = a.K, Ll = L / K, Lh = Ll / 2 + 1, KK = K * K, M = Ll - 1;
+    const int R = Ll / a.nchunk;
+    const int nitems = KK * a.nchunk + 1;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        __syncthreads();
+        if (item < KK * a.nchunk) {
+            const int r = item / a.nchunk, ch = item - r * a.nchunk, r1 = r / K, r2 = r % K;
+            double* cs = sm;
+            double* sn = cs + Ll;
+            double* src = sn + Ll;
+            double2* tmp = reinterpret_cast<double2*>(src + Ll * Ll);
+            load_tw(a.tw, cs, sn, Ll);
+            for (int m = threadIdx.x; m < Ll * Ll; m += blockDim.x) {
+                const int m1 = m / Ll, m2 = m - m1 * Ll;
+                src[m] = __ldcg(a.x64 + (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L));  // x_r[m]
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < Ll * Lh; e += blockDim.x) {  // along n2 (all rows)
+                const int n1 = e / Lh, k2 = e - n1 * Lh;
+                const double* row = src + n1 * Ll;
+                double re = 0, im = 0;
+                for (int n2 = 0; n2 < Ll; ++n2) {
+                    const int j = (k2 * n2) & M;
+                    re = fma(row[n2], cs[j], re);
+                    im = fma(-row[n2], sn[j], im);
+                }
+                tmp[e] = make_double2(re, im);
+            }
+            __syncthreads();
+            const double scale = 1.0 / ((double)Ll * Ll);
+            float2* out = a.xhat + (size_t)(r / 2) * Ll * Lh * 2 + (r & 1);   // pair-interleaved
+            for (int e = threadIdx.x; e < R * Lh; e += blockDim.x) {  // along n1, rows k1 of this chunk
+                const int k1 = ch * R + e / Lh, k2 = e % Lh;
+                double re = 0, im = 0;
+                for (int n1 = 0; n1 < Ll; ++n1) {
+                    const int j = (k1 * n1) & M;
+                    const double2 t = tmp[n1 * Lh + k2];
+                    re += t.x * cs[j] + t.y * sn[j];
+                    im += t.y * cs[j] - t.x * sn[j];
+                }
+                out[((size_t)k1 * Lh + k2) * 2] = make_float2((float)(re * scale), (float)(im * scale));
+            }
+        } else {
+            // logit bias in log2 units: lr = log2 rho, beta_r = (E_min - E_r) log2(e) / (2 sigma^2)
+            __shared__ double Es[256];
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+            for (int r = warp; r < KK; r += nw) {  // one warp per class: E_r = ||x_r||^2
+                const int r1 = r / K, r2 = r % K;
+                double s = 0.0;
+                for (int m = lane; m < Ll * Ll; m += 32) {
+                    const int m1 = m / Ll, m2 = m - m1 * Ll;
+                    const double v = __ldcg(a.x64 + (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L));
+                    s += v * v;
+                }
+                s = warp_sum(s);
+                if (lane == 0) Es[r] = s;
+            }
+            __syncthreads();
+            double emin = Es[0];
+            for (int r = 1; r < KK; ++r) emin = fmin(emin, Es[r]);
+            for (int k = threadIdx.x; k < L; k += blockDim.x) {
+                const double p1 = __ldcg(a.rho + k), p2 = __ldcg(a.rho + L + k);
+                a.par32[k] = p1 > 0.0 ? (float)log2(p1) : -INFINITY;
+                a.par32[L + k] = p2 > 0.0 ? (float)log2(p2) : -INFINITY;
+            }
+            for (int r = threadIdx.x; r < KK; r += blockDim.x) {
+                a.par32[2 * L + r] = (float)((emin - Es[r]) * a.inv_2s2 * 1.4426950408889634074);
+                a.par64[r] = Es[r];
+            }
+            if (threadIdx.x == 0) a.par64[KK] = emin;
+        }
+    }
+}
+
+__device__ inline void stamp(const TailArgs& a, int k) {
+    if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[k] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
+    extern __shared__ double sm[];
+    bool synced = true;
+    stamp(a, 0);
+    if (a.mode & TAIL_REDUCE) {
+        phase_reduce(a);
+        synced = false;
+    }
+    if (a.mode & TAIL_FOLD) {
+        if (!synced) grid_sync();
+        stamp(a, 1);
+        phase_fold(a, sm);
+        synced = false;
+    }
+    if (a.mode & TAIL_FINALIZE) {
+        grid_sync();
+        stamp(a, 2);
+        phase_update(a);
+        grid_sync();
+        stamp(a, 3);
+        phase_project(a);
+        synced = false;
+    }
+    if (a.mode & TAIL_PREP) {
+        if (!synced) grid_sync();
+        stamp(a, 4);
+        phase_prep(a, sm);
+    }
+    if (a.stamps) {
+        __syncthreads();
+        stamp(a, 5);
+    }
+}
+
+}  // namespace ffttail
+
+using namespace ffttail;
+
+int fft_tail_grid(const srmra_ctx* c) {
+    const int PB = fft_partial_bins(c->KK, c->Ll);
+    int g = (PB + 31) / 32;
+    const int items = c->KK * (c->Ll >= 8 ? c->Ll / 8 : 1) + 1;
+    if (g < items) g = items;
+    if (g > c->num_sms) g = c->num_sms;
+    return g < 1 ? 1 : g;
+}
+
+cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
+    const int Ll = c->Ll, Lh = Ll / 2 + 1;
+    TailArgs a;
+    a.stamps = c->d_stamps;
+    a.mode = mode;
+    a.L = c->L;
+    a.K = c->K;
+    a.t = t;
+    a.project = project;
+    a.trace_cap = c->opt.trace_cap;
+    a.tau = c->tau;
+    a.inv_2s2 = c->inv_2s2;
+    a.part = c->d_part;
+    a.llpart = c->d_llpart;
+    a.nparts = c->n_local > 0 ? c->fft_grid : 0;
+    a.PB = fft_partial_bins(c->KK, Ll);
+    a.acc = c->d_bhat;
+    a.tw = c->d_tw;
+    a.pack = c->d_pack;
+    a.off_cm = c->pk.cmass;
+    a.off_m1 = c->pk.m1;
+    a.off_m2 = c->pk.m2;
+    a.off_ll = c->pk.ll;
+    a.x64 = c->d_x64;
+    a.rho = c->d_rho;
+    a.xtmp = c->d_xtmp;
+    a.trace = c->d_trace;
+    a.x32 = c->d_x32;
+    a.flag = c->d_flag;
+    a.xhat = c->d_xhat;
+    a.par32 = c->par.f32;
+    a.par64 = c->par.f64;
+    a.nchunk = Ll >= 8 ? Ll / 8 : 1;
+    const int R = Ll / a.nchunk;
+    size_t sm_fold = sizeof(double) * 2 * Ll + sizeof(double2) * ((size_t)Ll * Lh + (size_t)R * Lh);
+    const size_t sm_marg = sizeof(double) * (2 * Ll + (size_t)c->KK * (Ll + 2 * Lh));  // marginal item staging
+    if (sm_marg > sm_fold) sm_fold = sm_marg;
+    size_t sm_prep = sizeof(double) * (2 * Ll + (size_t)Ll * Ll) + sizeof(double2) * (size_t)Ll * Lh;
+    const size_t sm = sm_fold > sm_prep ? sm_fold : sm_prep;
+    cudaError_t e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = fft_tail_grid(c);
+    void* args[] = {&a};
+    return cudaLaunchCooperativeKernel((const void*)k_fft_tail, dim3(grid), dim3(kThreads), args, sm, c->stream);
+}
+
+}  // namespace srmra

@@ -130,17 +130,24 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
     CK(launch_init_obs(c));
-    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_init(c));
+    if (c->path == SRMRA_PATH_FFT) {
+        CK(launch_fft_init(c));
+        CK(launch_fft_tail(c, TAIL_PREP, 0, 0));  // Xhat and logit bias of theta_0
+    }
     CK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
     c->iters_done = 0;
     return SRMRA_OK;
 }
 
-int allreduce_pack(srmra_ctx* c) {
+// The one data-path collective: sum this rank's sufficient statistics over all ranks.
+// FFT path: the compact float64 accumulators (U, V, row sums, pair line, LL) — the fold after it is
+// linear, so fold(sum) = sum(fold);  direct path: the packed b | class mass | marginals | LL.
+int allreduce_stats(srmra_ctx* c) {
     if (c->opt.world <= 1) return SRMRA_OK;
     NcclApi& api = nccl();
-    ncclResult_t r = api.AllReduce(c->d_pack, c->d_pack, (size_t)c->pk.total, ncclFloat64, ncclSum,
-                                   (ncclComm_t)c->nccl_comm, c->stream);
+    double* buf = c->path == SRMRA_PATH_FFT ? c->d_bhat : c->d_pack;
+    const size_t n = c->path == SRMRA_PATH_FFT ? fft_bhat_doubles(c->KK, c->Ll) : (size_t)c->pk.total;
+    ncclResult_t r = api.AllReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
     if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
     return SRMRA_OK;
 }
@@ -153,16 +160,16 @@ int record(srmra_ctx* c) {
     return SRMRA_OK;
 }
 
-// E + M over the local shard at the current theta: prep, path kernel, pack (no all-reduce).
+// E + M over the local shard at the current theta, up to the (local) sufficient statistics:
+// FFT path: the E/M kernel only (the previous tail, or the load-time tail, already prepared Xhat and
+// the logit bias; the reduce is the first phase of the tail); direct: prep, E/M, pack.
 // With profiling on, events bracket the dominant E/M kernel (records 2 and 3 of the quadruple).
 int local_estep_mstep(srmra_ctx* c) {
     int rc;
     if (c->path == SRMRA_PATH_FFT) {
-        CK(launch_fft_prep(c));  // logit bias + Xhat in one launch
         if ((rc = record(c))) return rc;
         CK(launch_fft_em(c));
         if ((rc = record(c))) return rc;
-        CK(launch_fft_fold(c));  // reduce + fold: b, class mass, marginals, LL into the pack
     } else if (c->path == SRMRA_PATH_DIRECT) {
         CK(launch_prep(c));
         if ((rc = record(c))) return rc;
@@ -293,9 +300,16 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->d_pack, c->pk.total));
     CKI(dalloc(&c->d_trace, opt.trace_cap));
     CKI(dalloc(&c->d_flag, 1));
+    CKI(dalloc(&c->d_counter, 1));
+    CKI(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
+    if (getenv("SRMRA_TAIL_STAMPS")) {
+        CKI(dalloc(&c->d_stamps, 8));
+        CKI(cudaMemset(c->d_stamps, 0, 8 * sizeof(unsigned long long)));
+    }
     if (path == SRMRA_PATH_FFT) {
         CKI(dalloc(&c->d_yhat, (size_t)n_local * fft_yhat_stride(c->Ll)));
-        CKI(dalloc(&c->d_xhat, (size_t)c->KK * c->Ll * c->Lh));
+        CKI(dalloc(&c->d_xhat, fft_xhat_float2(c->KK, c->Ll)));
+        CKI(cudaMemset(c->d_xhat, 0, sizeof(float2) * fft_xhat_float2(c->KK, c->Ll)));
         CKI(dalloc(&c->d_bhat, fft_bhat_doubles(c->KK, c->Ll)));
         CKI(fft_plan(c));
         std::vector<double> tw(2 * (size_t)c->Ll);  // cos / sin (2 pi j / L_low), float64
@@ -358,10 +372,23 @@ int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
         int rc;
         if ((rc = record(c)) != SRMRA_OK) return rc;
         if ((rc = local_estep_mstep(c)) != SRMRA_OK) return rc;
-        if ((rc = allreduce_pack(c)) != SRMRA_OK) return rc;
         const int F = c->opt.proj_every;
         const int project = F > 0 && ((t + 1) % F == 0);
-        CK(launch_finalize(c, t, project));
+        if (c->path == SRMRA_PATH_FFT) {
+            // reduce -> [all-reduce] -> fold -> finalize -> projection -> next prep: one cooperative kernel
+            // (two when the NCCL all-reduce has to sit between the reduce and the fold)
+            const int rest = TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP;
+            if (c->opt.world > 1) {
+                CK(launch_fft_tail(c, TAIL_REDUCE, t, project));
+                if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
+                CK(launch_fft_tail(c, rest, t, project));
+            } else {
+                CK(launch_fft_tail(c, TAIL_REDUCE | rest, t, project));
+            }
+        } else {
+            if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
+            CK(launch_finalize(c, t, project));
+        }
         if ((rc = record(c)) != SRMRA_OK) return rc;
         c->iters_done++;
     }
@@ -455,6 +482,7 @@ int srmra_local_stats(srmra_ctx* c, double* out) {
     int rc = local_estep_mstep(c);
     c->prof = prof;
     if (rc != SRMRA_OK) return rc;
+    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD, 0, 0));  // local, no update
     CK(cudaMemcpyAsync(out, c->d_pack, sizeof(double) * c->pk.total, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SRMRA_OK;
@@ -462,12 +490,18 @@ int srmra_local_stats(srmra_ctx* c, double* out) {
 
 int srmra_get_path(const srmra_ctx* c) { return c ? c->path : SRMRA_ERR_INVALID_ARG; }
 
+int srmra_debug_timestamps(srmra_ctx* c, uint64_t* out8) {
+    if (!c || !out8) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
+    if (!c->d_stamps) return fail(c, SRMRA_ERR_STATE, "set SRMRA_TAIL_STAMPS before srmra_init");
+    CK(cudaMemcpyAsync(out8, c->d_stamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
+
 int srmra_launches_per_iter(const srmra_ctx* c) {
     if (!c) return SRMRA_ERR_INVALID_ARG;
-    int n = 1;  // finalize
-    if (c->path == SRMRA_PATH_DIRECT) n += 2 + (c->n_local > 0 ? 1 : 0);  // prep, pack, em
-    if (c->path == SRMRA_PATH_FFT) n += fft_launches_per_iter(c);
-    return n;
+    if (c->path == SRMRA_PATH_DIRECT) return 3 + (c->n_local > 0 ? 1 : 0);  // prep, pack, finalize [, em]
+    return fft_launches_per_iter(c);  // [em,] tail [, reduce-only tail when world > 1]
 }
 
 void srmra_free(srmra_ctx* c) {
@@ -479,7 +513,7 @@ void srmra_free(srmra_ctx* c) {
     }
     void* bufs[] = {c->d_y, c->d_yhat, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
                     c->par.f32, c->par.f64, c->d_xhat, c->d_colsum, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
-                    c->d_part, c->d_llpart, c->d_tw};
+                    c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps};
     for (void* p : bufs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

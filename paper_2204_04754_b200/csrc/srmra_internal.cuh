@@ -65,11 +65,14 @@ struct srmra_ctx {
     double* d_llpart = nullptr; // fft path: per-CTA log-likelihood partials [fft_grid]
     double* d_tw = nullptr;     // fft path: cos | sin (2 pi j / L_low), j < L_low, float64
     int fft_grid = 0, fft_groups = 0, fft_threads = 0;
+    bool fft_xs = false;        // Xhat staged in shared memory by the E/M kernel
     size_t fft_smem = 0;
     double* d_pack = nullptr;   // packed statistics, see PackLayout
     srmra::PackLayout pk{};
     double* d_trace = nullptr;  // [trace_cap]
     int* d_flag = nullptr;      // [1] numeric error flag
+    unsigned* d_counter = nullptr;  // [1] grid "last block" counter of the fused fold + finalize
+    unsigned long long* d_stamps = nullptr;  // [8] tail-kernel phase timestamps (env SRMRA_TAIL_STAMPS)
     int iters_done = 0;
 
     // multi-GPU
@@ -96,13 +99,15 @@ bool direct_supported(int L, int Ll, int K);
 cudaError_t launch_fft_em(srmra_ctx* c);        // k_fft.cu
 bool fft_supported(int L, int Ll, int K);
 cudaError_t launch_fft_init(srmra_ctx* c);
-cudaError_t launch_fft_prep(srmra_ctx* c);
-cudaError_t launch_fft_fold(srmra_ctx* c);
+// cooperative tail kernel of the FFT path (k_fft_tail.cu): phases selected by TAIL_* bits
+enum { TAIL_REDUCE = 1, TAIL_FOLD = 2, TAIL_FINALIZE = 4, TAIL_PREP = 8 };
+cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project);
 int fft_launches_per_iter(const srmra_ctx* c);
 size_t fft_bhat_doubles(int KK, int Ll);  // Bhat [KK][Ll][Lh] complex + mass lines [KK][Ll+Lh] complex
 size_t fft_yhat_stride(int Ll);           // float2 per observation in d_yhat (16-byte multiple)
 cudaError_t fft_plan(srmra_ctx* c);       // grid / groups / smem of the E/M kernel for this shard
 size_t fft_part_float2(const srmra_ctx* c);
+size_t fft_xhat_float2(int KK, int Ll);   // pair-interleaved Xhat
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ int imod(int a, int m) {

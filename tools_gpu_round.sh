@@ -1,0 +1,9 @@
+#!/bin/bash
+# One GPU round: gpu tests, bench, launch list, ncu --set full of the E/M kernel.  $1 = tag
+T=${1:-x}
+python -m pytest tests -m gpu -q -p no:cacheprovider -rA 2>&1 | grep -E "path=fft|passed|failed|FAILED|Error|error" | head -60 > gpurun_out/pytest_$T.log
+python bench.py --steps 300 --warmup 5 --no-cpu-baseline > gpurun_out/bench_$T.log 2>&1
+python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/plain_$T.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/ncul_$T.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_fft_em -s 3 -c 1 -o gpurun_out/prof_$T python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/ncuf_$T.log 2>&1
+cat gpurun_out/pytest_$T.log; cat gpurun_out/bench_$T.log
