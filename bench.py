@@ -42,6 +42,25 @@ def flop_per_unit(path: str, L_low: int) -> float:
     return 4.0 * L_low * L_low  # direct / gemm: 2 L_low^2 (E-step dot) + 2 L_low^2 (M-step)
 
 
+def roof_kernel(path: str) -> str:
+    return {"fft": "k_fft_em", "direct": "k_direct_em", "gemm": "k_gemm_em"}.get(path, path)
+
+
+def ncu_traffic(kernel: str, cfg: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the latest committed `ncu --set full`
+    capture (profiles/rNN_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        try:
+            v = json.load(open(f)).get(kernel, {}).get(cfg)
+        except (OSError, ValueError):
+            continue
+        if v is not None:
+            return v, os.path.relpath(f, ROOT)
+    return None, None
+
+
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -207,10 +226,12 @@ def run_ours(args):
 
     # roofline of the dominant kernel (measured live: events around it inside the library, same stream)
     fpu = flop_per_unit(path, p.L_low)
+    traffic, traffic_src = ncu_traffic(roof_kernel(path), p.name)
     em_avg_s = em_ms / 1e3 / max(n_prof, 1)
     achieved = fpu * p.N * p.L_high ** 2 / em_avg_s / 1e12
     roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+            "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": int(p.N * p.L_low * (p.L_low // 2 + 1) * 8),
             "kernel": {"fft": "k_fft_em", "direct": "k_direct_em", "gemm": "k_gemm_em"}.get(path, path),
             "flop_per_unit": fpu, "kernel_ms_avg": em_avg_s * 1e3,
             "kernel_share_of_step": em_ms / max(iter_ms, 1e-12),

@@ -521,7 +521,9 @@ static cudaError_t plan_em_t(srmra_ctx* c) {
     int g_plain = groups, g_xs = groups;
     while (g_plain > 1 && smem_bytes<LL>(KK, g_plain, ys) > 227 * 1024) --g_plain;
     while (g_xs > 1 && smem_bytes<LL>(KK, g_xs, ys) + xsb > 227 * 1024) --g_xs;
-    bool xs = g_xs == g_plain && smem_bytes<LL>(KK, g_xs, ys) + xsb <= 227 * 1024;
+    // measured on B200 (tools/em_sweep.py, c1 / c3): Xhat in shared memory with one group fewer beats
+    // Xhat through L1 with the extra group (164 vs 177 us at c1), so stage it whenever it fits
+    bool xs = smem_bytes<LL>(KK, g_xs, ys) + xsb <= 227 * 1024;
     const char* ex = getenv("SRMRA_FFT_XS");
     if (ex) xs = atoi(ex) != 0 && smem_bytes<LL>(KK, 1, ys) + xsb <= 227 * 1024;
     groups = xs ? g_xs : g_plain;
