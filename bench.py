@@ -175,10 +175,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     nccl_id = None
     if world > 1:
+        from paper_2204_04754_b200.shard import broadcast_nccl_id
         dist.init_process_group("nccl", device_id=dev)
-        obj = [srm.srmra_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = broadcast_nccl_id(srm.srmra_nccl_unique_id)
 
     p = synth.make_config(args.config, seed_offset=1000 * rank if world > 1 else 0)
     stream = torch.cuda.Stream(device=dev)
