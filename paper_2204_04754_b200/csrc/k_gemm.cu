@@ -1,0 +1,483 @@
+// k_gemm.cu — the tcgen05 tensor-core E/M path (SRMRA_PATH_GEMM), fp32-accurate 3xTF32.
+//
+//   GEMM1 (E-step)  S = Y T(x)^T : S[i,s] = <y_i, P R_s x> = sum_n y_i[n] x[(n1K - s1) mod L, (n2K - s2) mod L]
+//                   (PAPER.md:37-38 and the residual expansion of eq:likelihood_EM).
+//                   T(x) (L^2 x L_low^2) is never materialised: its rows are windows of the polyphase
+//                   component x_r (s = r + K t: T[s][n] = x_r[n - t]); every 16-byte k-chunk of a row is a
+//                   16-byte-aligned window of one of 4 pre-rotated, periodically extended copies of x_r
+//                   (built by k_gemm_prep, L2-resident), copied into the canonical smem layout by cp.async.
+//   softmax         per observation: posterior w^{i,s} (eq:weights_EM, logits as in k_common.cu), LL_i;
+//                   writes W^T split into tf32 hi / lo, transposed ([L^2][N]) for GEMM2.
+//   GEMM2 (M-step)  Z = W^T Y : Z[s][n] = sum_i w^{i,s} y_i[n]; an all-ones column appended to Y gives
+//                   colsum[s] = sum_i w^{i,s} (eq:rho_EM numerator) in the same GEMM.
+//   fold            b[p] = sum_n Z[(nK - p) mod L][n]  (eq:x_EM numerator with P^{-1} := P^T).
+// The GEMM mainloop: 128x128 output tile per CTA in TMEM (128 columns), K in steps of 32 with a
+// 3-stage cp.async ring; one elected thread issues 3 x 4 tcgen05.mma.kind::tf32 (hi*hi, hi*lo, lo*hi)
+// per step and commits them to the stage's mbarrier, which the loads of the stage's next use wait on.
+#include <math.h>
+
+#include "srmra_internal.cuh"
+#include "tcgen05.cuh"
+
+namespace srmra {
+namespace gemmk {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, THREADS = 128;
+// split-K: the K range is cut into KSPLIT contiguous parts accumulated in separate TMEM blocks and
+// summed in float64 in the epilogue (fp32 tensor-core accumulation error shrinks ~KSPLIT-fold)
+constexpr int KSPLIT = 4;
+constexpr int TILE_BYTES = BM * BK * 4;               // one operand tile (16 KB)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;           // A_hi | A_lo | B_hi | B_lo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
+constexpr uint32_t IDESC = tc::idesc_tf32<BM, BN>();
+
+struct GemmArgs {
+    // A: rows [M][lda] fp32 hi / lo (K-major)
+    const float* a_hi;
+    const float* a_lo;
+    int64_t lda;
+    int M;
+    int K;             // contraction length (multiple of 4)
+    // B dense: rows [N][ldb] hi / lo
+    const float* b_hi;
+    const float* b_lo;
+    int64_t ldb;
+    int N;
+    // B implicit T(x) (GEMM1): xe[hi|lo][KK][4 rot][Ll][2 Ll]
+    const float* xe;
+    int L, Ll, K_ds;
+    // C: [M][ldc] fp32
+    float* c;
+    int64_t ldc;
+};
+
+// rotated, periodically extended polyphase copies: xe[h][r][rot][row][c] = x_r[row][(c + rot) mod Ll]
+__device__ __forceinline__ size_t xe_index(int h, int r, int rot, int row, int c, int KK, int Ll) {
+    return ((((size_t)h * KK + r) * 4 + rot) * Ll + row) * (2 * Ll) + c;
+}
+
+template <bool IMPLICIT_B>
+__global__ void __launch_bounds__(THREADS, 1) k_gemm3(GemmArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte aligned operand area
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t mbar[STAGES];
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+    if (warp == 0) tc::tmem_alloc<BN * KSPLIT>(&tmem_slot);
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) tc::mbar_init(tc::smem_u32(&mbar[s]), 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t taddr = tmem_slot;
+
+    // ---- per-thread load plan: thread tid copies row tid of the A tile and row tid of the B tile
+    const int arow = m0 + tid;
+    const bool a_ok = arow < g.M;
+    const float* a_hi_row = g.a_hi + (size_t)(a_ok ? arow : 0) * g.lda;
+    const float* a_lo_row = g.a_lo + (size_t)(a_ok ? arow : 0) * g.lda;
+    const int brow = n0 + tid;
+    const bool b_ok = brow < g.N;
+    const float* b_hi_row = nullptr;
+    const float* b_lo_row = nullptr;
+    // implicit T: row s = brow -> class r = (s1 mod K, s2 mod K), low-res shift t = (s1 div K, s2 div K);
+    // T[s][n1 Ll + n2] = x_r[(n1 - t1) mod Ll][(n2 - t2) mod Ll]; the window of a chunk starting at n2
+    // starts at st = (n2 - t2) mod Ll = (st0 + n2) mod Ll with st0 = (-t2) mod Ll; n2 advances by 4 so the
+    // rotation rot = st0 & 3 is fixed per row and the extended column is c0 = (st0 & ~3) + n2.
+    int t1 = 0, rot = 0, c0base = 0, rcls = 0;
+    if (IMPLICIT_B) {
+        const int s = b_ok ? brow : 0;
+        const int s1 = s / g.L, s2 = s - s1 * g.L;
+        rcls = (s1 % g.K_ds) * g.K_ds + (s2 % g.K_ds);
+        t1 = s1 / g.K_ds;
+        const int t2 = s2 / g.K_ds;
+        const int st0 = (g.Ll - t2) % g.Ll;
+        rot = st0 & 3;
+        c0base = st0 - rot;
+    } else {
+        b_hi_row = g.b_hi + (size_t)(b_ok ? brow : 0) * g.ldb;
+        b_lo_row = g.b_lo + (size_t)(b_ok ? brow : 0) * g.ldb;
+    }
+    const int KKc = g.K_ds * g.K_ds;
+
+    auto load_tile = [&](int kt, int st) {
+        unsigned char* sb = base + st * STAGE_BYTES;
+        const uint32_t sa_hi = tc::smem_u32(sb), sa_lo = sa_hi + TILE_BYTES;
+        const uint32_t sb_hi = sa_lo + TILE_BYTES, sb_lo = sb_hi + TILE_BYTES;
+#pragma unroll
+        for (int j = 0; j < BK / 4; ++j) {
+            const int k = kt * BK + 4 * j;
+            const bool kv = k < g.K;
+            const uint32_t off = tc::kmajor_off<BK>(tid, 4 * j);
+            tc::cp_async16_zfill(sa_hi + off, a_hi_row + (kv ? k : 0), a_ok && kv);
+            tc::cp_async16_zfill(sa_lo + off, a_lo_row + (kv ? k : 0), a_ok && kv);
+            if (IMPLICIT_B) {
+                const int n1 = k / g.Ll, n2 = k - n1 * g.Ll;
+                const int row = (n1 - t1 + g.Ll) % g.Ll;
+                const size_t ih = xe_index(0, rcls, rot, row, c0base + n2, KKc, g.Ll);
+                const size_t il = xe_index(1, rcls, rot, row, c0base + n2, KKc, g.Ll);
+                tc::cp_async16_zfill(sb_hi + off, g.xe + (kv ? ih : 0), b_ok && kv);
+                tc::cp_async16_zfill(sb_lo + off, g.xe + (kv ? il : 0), b_ok && kv);
+            } else {
+                tc::cp_async16_zfill(sb_hi + off, b_hi_row + (kv ? k : 0), b_ok && kv);
+                tc::cp_async16_zfill(sb_lo + off, b_lo_row + (kv ? k : 0), b_ok && kv);
+            }
+        }
+        tc::cp_async_commit();
+    };
+
+    const int nk = (g.K + BK - 1) / BK;
+    const int kper = (nk + KSPLIT - 1) / KSPLIT;  // K tiles per split part
+    load_tile(0, 0);
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % STAGES;
+        if (kt + 1 < nk) {
+            const int st1 = (kt + 1) % STAGES;
+            if (kt + 1 >= STAGES) tc::mbar_wait(tc::smem_u32(&mbar[st1]), ((kt + 1) / STAGES - 1) & 1);
+            load_tile(kt + 1, st1);
+            tc::cp_async_wait<1>();
+        } else {
+            tc::cp_async_wait<0>();
+        }
+        tc::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t sa = tc::smem_u32(base + st * STAGE_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint32_t o = kk * 256;  // two 16-byte k-chunks per MMA
+                const uint64_t ah = tc::kmajor_desc<BK>(sa + o), al = tc::kmajor_desc<BK>(sa + TILE_BYTES + o);
+                const uint64_t bh = tc::kmajor_desc<BK>(sa + 2 * TILE_BYTES + o);
+                const uint64_t bl = tc::kmajor_desc<BK>(sa + 3 * TILE_BYTES + o);
+                const int part = kt / kper;
+                const uint32_t td = taddr + (uint32_t)(part * BN);
+                tc::mma_tf32(td, ah, bh, IDESC, ((kt - part * kper) | kk) != 0);
+                tc::mma_tf32(td, ah, bl, IDESC, 1u);
+                tc::mma_tf32(td, al, bh, IDESC, 1u);
+            }
+            tc::commit(tc::smem_u32(&mbar[st]));
+        }
+    }
+    tc::mbar_wait(tc::smem_u32(&mbar[(nk - 1) % STAGES]), ((nk - 1) / STAGES) & 1);
+    tc::fence_after();
+
+    // ---- epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows; 16 columns per load
+    const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+    for (int cc = 0; cc < BN; cc += 16) {
+        float v[16];
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+        const int nparts = (nk + kper - 1) / kper;
+        for (int part = 0; part < nparts; ++part) {
+            tc::tmem_ld16(taddr + ((uint32_t)(warp * 32) << 16) + part * BN + cc, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] += (double)v[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = (float)acc[j];
+        if (row < g.M) {
+            float* dst = g.c + (size_t)row * g.ldc + n0 + cc;
+            if (n0 + cc + 16 <= g.N) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+                for (int j = 0; j < 16; ++j)
+                    if (n0 + cc + j < g.N) dst[j] = v[j];
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<BN * KSPLIT>(taddr);
+}
+
+// ---------------------------------------------------------------- init: tf32 splits of Y and Y^T
+// yhl: [2][n][Ll2] (hi | lo);  ythl: [2][Ll2 + 16][ldw] (hi | lo), row Ll2 = ones (colsum), rows beyond 0
+__global__ void k_gemm_init(const float* __restrict__ y, int64_t n, int Ll2, int64_t ldw, float* __restrict__ yhl,
+                            float* __restrict__ ythl) {
+    __shared__ float tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int k0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const size_t plane_y = (size_t)n * Ll2, plane_t = (size_t)(Ll2 + 16) * ldw;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = i0 + r;
+        const int k = k0 + tx;
+        float v = 0.f;
+        if (i < n && k < Ll2) {
+            v = y[i * Ll2 + k];
+            float hi, lo;
+            tc::split_tf32(v, hi, lo);
+            yhl[i * Ll2 + k] = hi;
+            yhl[plane_y + i * Ll2 + k] = lo;
+        }
+        tile[r][tx] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int k = k0 + r;
+        const int64_t i = i0 + tx;
+        if (k < Ll2 && i < ldw) {
+            float hi, lo;
+            tc::split_tf32(i < n ? tile[tx][r] : 0.f, hi, lo);
+            ythl[(size_t)k * ldw + i] = hi;
+            ythl[plane_t + (size_t)k * ldw + i] = lo;
+        }
+    }
+}
+__global__ void k_gemm_init_ones(int64_t n, int Ll2, int64_t ldw, float* __restrict__ ythl) {
+    const size_t plane_t = (size_t)(Ll2 + 16) * ldw;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < 16 * ldw; e += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e / ldw);
+        const int64_t i = e - (int64_t)r * ldw;
+        ythl[(size_t)(Ll2 + r) * ldw + i] = (r == 0 && i < n) ? 1.f : 0.f;
+        ythl[plane_t + (size_t)(Ll2 + r) * ldw + i] = 0.f;
+    }
+}
+
+// ---------------------------------------------------------------- prep: rotated extended polyphase copies
+__global__ void k_gemm_prep(const float* __restrict__ x32, int L, int K, float* __restrict__ xe) {
+    const int Ll = L / K, KK = K * K;
+    const int total = KK * 4 * Ll * 2 * Ll;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int c = e % (2 * Ll);
+        const int row = (e / (2 * Ll)) % Ll;
+        const int rot = (e / (2 * Ll * Ll)) % 4;
+        const int r = e / (2 * Ll * Ll * 4);
+        const int r1 = r / K, r2 = r % K;
+        const int m2 = (c + rot) % Ll;
+        const float v = x32[(size_t)imod(K * row - r1, L) * L + imod(K * m2 - r2, L)];  // x_r[row][m2]
+        float hi, lo;
+        tc::split_tf32(v, hi, lo);
+        xe[xe_index(0, r, rot, row, c, KK, Ll)] = hi;
+        xe[xe_index(1, r, rot, row, c, KK, Ll)] = lo;
+    }
+}
+
+// ---------------------------------------------------------------- softmax (posterior), transposed W^T
+// Block: 32 observations.  Phase 1 (warp per row): Sref, m, Z, LL_i (logits of k_common.cu, natural
+// units).  Phase 2: 32 x 32 tiles, w = exp(v - m) / Z, transposed through shared memory into W^T hi / lo.
+__global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ S, int64_t n, int L, int K,
+                                                      const float* __restrict__ par32, const double* __restrict__ par64,
+                                                      const double* __restrict__ ynorm, float inv_s2f, double inv_s2,
+                                                      double inv_2s2, int64_t ldw, float* __restrict__ wthl,
+                                                      double* __restrict__ llobs, double* __restrict__ ll_out,
+                                                      const float* __restrict__ y, const double* __restrict__ x64,
+                                                      const double* __restrict__ rho) {
+    __shared__ float sref_s[32], m_s[32], iz_s[32];
+    __shared__ float tile[32][33];
+    __shared__ double llsum;
+    const int L2 = L * L, KK = K * K;
+    const float* lr1 = par32;
+    const float* lr2 = par32 + L;
+    const float* beta = par32 + 2 * L;
+    (void)par64;
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) llsum = 0.0;
+    __syncthreads();
+    for (int rr = warp; rr < 32; rr += 8) {
+        const int64_t i = i0 + rr;
+        if (i >= n) continue;
+        const float* Si = S + (size_t)i * L2;
+        float mx = -INFINITY;
+        for (int s = lane; s < L2; s += 32) mx = fmaxf(mx, Si[s]);
+        const float sref = warp_max(mx);
+        float vm = -INFINITY;
+        int am = 0;
+        for (int s = lane; s < L2; s += 32) {
+            const int s1 = s / L, s2 = s - s1 * L;
+            const float v = fmaf(Si[s] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
+            if (v > vm) { vm = v; am = s; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // argmax (ties: smaller shift index)
+            const float v2 = __shfl_xor_sync(0xffffffffu, vm, o);
+            const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+            if (v2 > vm || (v2 == vm && a2 < am)) { vm = v2; am = a2; }
+        }
+        const float m = vm;
+        float z = 0.f;
+        for (int s = lane; s < L2; s += 32) {
+            const int s1 = s / L, s2 = s - s1 * L;
+            const float v = fmaf(Si[s] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
+            z += expf(v - m);
+        }
+        const double Z = warp_sum((double)z);
+        // log-sum-exp anchored at the argmax shift s*: lse = ell[s*] + log sum_s exp(v_s - v_s*), with
+        // ell[s*] = log rho1 + log rho2 - ||y_i - P R_s* x||^2 / (2 sigma^2) from an exact float64 residual,
+        // so the fp32 score error only enters through the (small) log-sum term (eq:likelihood_EM)
+        const int a1 = am / L, a2 = am - a1 * L, Ll = L / K;
+        double d = 0.0;
+        for (int nn = lane; nn < Ll * Ll; nn += 32) {
+            const int n1 = nn / Ll, n2 = nn - n1 * Ll;
+            const double e = (double)y[(size_t)i * Ll * Ll + nn] - x64[(size_t)imod(n1 * K - a1, L) * L + imod(n2 * K - a2, L)];
+            d += e * e;
+        }
+        d = warp_sum(d);
+        if (lane == 0) {
+            sref_s[rr] = sref;
+            m_s[rr] = m;
+            iz_s[rr] = (float)(1.0 / Z);
+            const double lse = log(rho[a1]) + log(rho[L + a2]) - d * inv_2s2 + log(Z);
+            if (llobs) llobs[i] = lse;
+            atomicAdd(&llsum, lse);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(ll_out, llsum);
+    const size_t plane = (size_t)L2 * ldw;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int s0 = 0; s0 < L2; s0 += 32) {
+        __syncthreads();
+        for (int rr = ty; rr < 32; rr += 8) {  // rows = observations, coalesced along shifts
+            const int64_t i = i0 + rr;
+            const int s = s0 + tx;
+            float w = 0.f;
+            if (i < n && s < L2) {
+                const int s1 = s / L, s2 = s - s1 * L;
+                const float v = fmaf(S[(size_t)i * L2 + s] - sref_s[rr], inv_s2f,
+                                     lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
+                w = expf(v - m_s[rr]) * iz_s[rr];
+            }
+            tile[rr][tx] = w;
+        }
+        __syncthreads();
+        for (int rr = ty; rr < 32; rr += 8) {  // rows = shifts, coalesced along observations
+            const int s = s0 + rr;
+            const int64_t i = i0 + tx;
+            if (s < L2 && i < ldw) {
+                float hi, lo;
+                tc::split_tf32(tile[tx][rr], hi, lo);
+                wthl[(size_t)s * ldw + i] = hi;
+                wthl[plane + (size_t)s * ldw + i] = lo;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- fold: b[p] = sum_n Z[(nK - p) mod L][n]
+__global__ void k_gemm_fold(const float* __restrict__ Z, int64_t ldz, int L, int K, double* __restrict__ b,
+                            double* __restrict__ colsum) {
+    const int Ll = L / K, Ll2 = Ll * Ll, L2 = L * L;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int p = warp; p < L2; p += nw) {
+        const int p1 = p / L, p2 = p - p1 * L;
+        double acc = 0.0;
+        for (int nn = lane; nn < Ll2; nn += 32) {
+            const int n1 = nn / Ll, n2 = nn - n1 * Ll;
+            const int s = imod(n1 * K - p1, L) * L + imod(n2 * K - p2, L);
+            acc += (double)Z[(size_t)s * ldz + nn];
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            b[p] = acc;
+            colsum[p] = (double)Z[(size_t)p * ldz + Ll2];  // column Ll2 = W^T . ones
+        }
+    }
+}
+
+}  // namespace gemmk
+
+// ==================================================================== host side
+using namespace gemmk;
+
+bool gemm_supported(int L, int Ll, int K) { return Ll >= 4 && (Ll % 4) == 0 && L <= 4096 && K * K <= 256; }
+
+static int64_t ldw_of(int64_t n) { return ((n + 3) / 4) * 4 > 0 ? ((n + 3) / 4) * 4 : 4; }
+
+size_t gemm_bytes(const srmra_ctx* c) {
+    const int64_t n = c->n_local, ldw = ldw_of(n);
+    size_t b = 0;
+    b += sizeof(float) * 2 * (size_t)n * c->Ll2;                 // Y hi/lo
+    b += sizeof(float) * 2 * (size_t)(c->Ll2 + 16) * ldw;        // Y^T hi/lo (+ ones row)
+    b += sizeof(float) * (size_t)n * c->L2;                      // S
+    b += sizeof(float) * 2 * (size_t)c->L2 * ldw;                // W^T hi/lo
+    b += sizeof(float) * (size_t)c->L2 * (c->Ll2 + 16);          // Z
+    b += sizeof(float) * 2 * (size_t)c->KK * 4 * c->Ll * 2 * c->Ll;  // rotated x copies
+    return b;
+}
+
+cudaError_t gemm_alloc(srmra_ctx* c) {
+    const int64_t n = c->n_local, ldw = ldw_of(n);
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->g_yhl, sizeof(float) * (2 * (size_t)n * c->Ll2 + 4))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->g_ythl, sizeof(float) * 2 * (size_t)(c->Ll2 + 16) * ldw)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->g_s, sizeof(float) * ((size_t)n * c->L2 + 4))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->g_wthl, sizeof(float) * 2 * (size_t)c->L2 * ldw)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->g_z, sizeof(float) * (size_t)c->L2 * (c->Ll2 + 16))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->g_xe, sizeof(float) * 2 * (size_t)c->KK * 4 * c->Ll * 2 * c->Ll)) != cudaSuccess) return e;
+    c->g_ldw = ldw;
+    return cudaFuncSetAttribute(k_gemm3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess
+               ? cudaGetLastError()
+               : cudaFuncSetAttribute(k_gemm3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+}
+
+void gemm_free(srmra_ctx* c) {
+    void* bufs[] = {c->g_yhl, c->g_ythl, c->g_s, c->g_wthl, c->g_z, c->g_xe};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
+}
+
+cudaError_t launch_gemm_init(srmra_ctx* c) {
+    const int64_t n = c->n_local;
+    if (n == 0) return cudaSuccess;
+    dim3 grid((unsigned)((c->g_ldw + 31) / 32), (unsigned)((c->Ll2 + 31) / 32));
+    k_gemm_init<<<grid, 256, 0, c->stream>>>(c->d_y, n, c->Ll2, c->g_ldw, c->g_yhl, c->g_ythl);
+    k_gemm_init_ones<<<64, 256, 0, c->stream>>>(n, c->Ll2, c->g_ldw, c->g_ythl);
+    return cudaGetLastError();
+}
+
+// prep (k_prep of k_common.cu runs first) -> GEMM1 -> softmax -> GEMM2 -> fold; the pack kernel follows
+cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1) {
+    const int64_t n = c->n_local;
+    const int total = c->KK * 4 * c->Ll * 2 * c->Ll;
+    k_gemm_prep<<<(total + 255) / 256, 256, 0, c->stream>>>(c->d_x32, c->L, c->K, c->g_xe);
+    if (n == 0) return cudaGetLastError();
+    if (ev_em0) cudaEventRecord(ev_em0, c->stream);
+    GemmArgs g1{};
+    g1.a_hi = c->g_yhl;
+    g1.a_lo = c->g_yhl + (size_t)n * c->Ll2;
+    g1.lda = c->Ll2;
+    g1.M = (int)n;
+    g1.K = c->Ll2;
+    g1.N = c->L2;
+    g1.xe = c->g_xe;
+    g1.L = c->L;
+    g1.Ll = c->Ll;
+    g1.K_ds = c->K;
+    g1.c = c->g_s;
+    g1.ldc = c->L2;
+    k_gemm3<true><<<dim3((c->L2 + BN - 1) / BN, (unsigned)((n + BM - 1) / BM)), THREADS, SMEM_BYTES, c->stream>>>(g1);
+    k_gemm_softmax<<<(unsigned)((n + 31) / 32), 256, 0, c->stream>>>(
+        c->g_s, n, c->L, c->K, c->par.f32, c->par.f64, c->d_ynorm, (float)c->inv_s2, c->inv_s2, c->inv_2s2, c->g_ldw,
+        c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho);
+    GemmArgs g2{};
+    g2.a_hi = c->g_wthl;
+    g2.a_lo = c->g_wthl + (size_t)c->L2 * c->g_ldw;
+    g2.lda = c->g_ldw;
+    g2.M = c->L2;
+    g2.K = (int)c->g_ldw;
+    g2.b_hi = c->g_ythl;
+    g2.b_lo = c->g_ythl + (size_t)(c->Ll2 + 16) * c->g_ldw;
+    g2.ldb = c->g_ldw;
+    g2.N = c->Ll2 + 16;
+    g2.c = c->g_z;
+    g2.ldc = c->Ll2 + 16;
+    k_gemm3<false><<<dim3((g2.N + BN - 1) / BN, (c->L2 + BM - 1) / BM), THREADS, SMEM_BYTES, c->stream>>>(g2);
+    if (ev_em1) cudaEventRecord(ev_em1, c->stream);
+    k_gemm_fold<<<(c->L2 * 32 + 255) / 256, 256, 0, c->stream>>>(c->g_z, c->Ll2 + 16, c->L, c->K,
+                                                                  c->d_pack + c->pk.b, c->d_colsum);
+    return cudaGetLastError();
+}
+
+}  // namespace srmra

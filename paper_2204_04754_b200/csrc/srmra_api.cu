@@ -109,10 +109,11 @@ int check_rho(const double* r, int L, std::vector<double>& out) {
 int choose_path(int requested, int L, int Ll, int K) {
     if (requested == SRMRA_PATH_DIRECT) return direct_supported(L, Ll, K) ? SRMRA_PATH_DIRECT : -1;
     if (requested == SRMRA_PATH_FFT) return fft_supported(L, Ll, K) ? SRMRA_PATH_FFT : -1;
-    if (requested == SRMRA_PATH_GEMM) return -1;  // not built yet
-    // AUTO: measured choice ("Path choice")
+    if (requested == SRMRA_PATH_GEMM) return gemm_supported(L, Ll, K) ? SRMRA_PATH_GEMM : -1;
+    // AUTO: measured choice ("Path choice"): FFT < direct < GEMM in time wherever compiled
     if (fft_supported(L, Ll, K)) return SRMRA_PATH_FFT;
     if (direct_supported(L, Ll, K)) return SRMRA_PATH_DIRECT;
+    if (gemm_supported(L, Ll, K)) return SRMRA_PATH_GEMM;
     return -1;
 }
 
@@ -130,6 +131,7 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
     CK(launch_init_obs(c));
+    if (c->path == SRMRA_PATH_GEMM) CK(launch_gemm_init(c));
     if (c->path == SRMRA_PATH_FFT) {
         CK(launch_fft_init(c));
         CK(launch_fft_tail(c, TAIL_PREP, 0, 0));  // Xhat and logit bias of theta_0
@@ -170,6 +172,12 @@ int local_estep_mstep(srmra_ctx* c) {
         if ((rc = record(c))) return rc;
         CK(launch_fft_em(c));
         if ((rc = record(c))) return rc;
+    } else if (c->path == SRMRA_PATH_GEMM) {
+        CK(launch_prep(c));
+        if ((rc = record(c))) return rc;
+        CK(launch_gemm_em(c, nullptr, nullptr));  // x copies, GEMM1, softmax, GEMM2, fold
+        if ((rc = record(c))) return rc;
+        CK(launch_pack(c));
     } else if (c->path == SRMRA_PATH_DIRECT) {
         CK(launch_prep(c));
         if ((rc = record(c))) return rc;
@@ -321,6 +329,13 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
         CKI(cudaMemcpy(c->d_tw, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
         CKI(dalloc(&c->d_part, fft_part_float2(c)));
         CKI(dalloc(&c->d_llpart, c->fft_grid));
+    }
+    if (path == SRMRA_PATH_GEMM) {
+        size_t fr = 0, tot = 0;
+        CKI(cudaMemGetInfo(&fr, &tot));
+        if (gemm_bytes(c) + (size_t)(1u << 30) > fr)
+            return bail(fail(c, SRMRA_ERR_OOM, "gemm path: scores / posterior buffers exceed free device memory"));
+        CKI(gemm_alloc(c));
     }
     CKI(cudaMemsetAsync(c->d_llobs, 0, sizeof(double) * (n_local ? n_local : 1), c->stream));
 
@@ -501,6 +516,8 @@ int srmra_debug_timestamps(srmra_ctx* c, uint64_t* out8) {
 int srmra_launches_per_iter(const srmra_ctx* c) {
     if (!c) return SRMRA_ERR_INVALID_ARG;
     if (c->path == SRMRA_PATH_DIRECT) return 3 + (c->n_local > 0 ? 1 : 0);  // prep, pack, finalize [, em]
+    // prep, x copies, pack, finalize [, GEMM1, softmax, GEMM2, fold]
+    if (c->path == SRMRA_PATH_GEMM) return 4 + (c->n_local > 0 ? 4 : 0);
     return fft_launches_per_iter(c);  // [em,] tail [, reduce-only tail when world > 1]
 }
 
@@ -516,6 +533,7 @@ void srmra_free(srmra_ctx* c) {
                     c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps};
     for (void* p : bufs)
         if (p) cudaFree(p);
+    gemm_free(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;

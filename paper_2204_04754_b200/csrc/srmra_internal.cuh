@@ -75,6 +75,15 @@ struct srmra_ctx {
     unsigned long long* d_stamps = nullptr;  // [8] tail-kernel phase timestamps (env SRMRA_TAIL_STAMPS)
     int iters_done = 0;
 
+    // gemm path (k_gemm.cu): tf32 hi|lo splits, scores, transposed posterior, Z = W^T Y, rotated x copies
+    float* g_yhl = nullptr;   // [2][n][Ll2]
+    float* g_ythl = nullptr;  // [2][Ll2 + 16][ldw]  (row Ll2 = ones)
+    float* g_s = nullptr;     // [n][L2]
+    float* g_wthl = nullptr;  // [2][L2][ldw]
+    float* g_z = nullptr;     // [L2][Ll2 + 16]
+    float* g_xe = nullptr;    // [2][KK][4][Ll][2 Ll]
+    int64_t g_ldw = 0;        // n rounded up to a multiple of 4
+
     // multi-GPU
     void* nccl_comm = nullptr;
 
@@ -99,6 +108,13 @@ bool direct_supported(int L, int Ll, int K);
 cudaError_t launch_fft_em(srmra_ctx* c);        // k_fft.cu
 bool fft_supported(int L, int Ll, int K);
 cudaError_t launch_fft_init(srmra_ctx* c);
+// tcgen05 3xTF32 GEMM path (k_gemm.cu)
+bool gemm_supported(int L, int Ll, int K);
+size_t gemm_bytes(const srmra_ctx* c);
+cudaError_t gemm_alloc(srmra_ctx* c);
+void gemm_free(srmra_ctx* c);
+cudaError_t launch_gemm_init(srmra_ctx* c);
+cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1);
 // cooperative tail kernel of the FFT path (k_fft_tail.cu): phases selected by TAIL_* bits
 enum { TAIL_REDUCE = 1, TAIL_FOLD = 2, TAIL_FINALIZE = 4, TAIL_PREP = 8 };
 cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project);

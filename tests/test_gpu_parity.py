@@ -127,6 +127,32 @@ def test_full_config_vs_golden(srm, name):
         assert_close(g, gold["x"], gold["rho1"], gold["rho2"], gold["trace"], tag=name)
 
 
+@pytest.mark.slow
+def test_c4_full_size_sampled(srm, oracle_mod):
+    """configs[4] at full size (N = 10^5, L_high = 256, L_low = 128) in the launch configuration of the
+    path AUTO picks: the oracle cannot run the whole iteration in seconds, so it checks a sample of
+    per-observation log-likelihood terms one by one, plus size-independent invariants (mass
+    conservation sum_p b = sum y, class mass = N, sum rho = 1) and the finiteness of x."""
+    p = synth.make_config("c4")
+    with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0) as ctx:
+        ctx.em_iter(1)
+        x, r1, r2, ll, it = ctx.get_estimate()
+        b, cm, m1, m2 = ctx.stats()
+        llo = ctx.obs_loglik()
+        path = ctx.path
+    idx = np.array([0, 1, 12345, 54321, 77777, p.N - 1])
+    ref = oracle_mod.loglik_obs(p.y, idx, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0)
+    err = np.abs(llo[idx] - ref) / np.abs(ref)
+    print(f"c4 path={path} sampled LL_i rel err max {err.max():.2e}")
+    assert err.max() <= LL_TOL
+    assert abs(llo.sum() - ll) <= 1e-9 * abs(ll)
+    ysum = p.y.astype(np.float64).sum()
+    assert abs(b.sum() - ysum) <= 1e-6 * np.abs(p.y).sum()
+    assert abs(cm.sum() - p.N) <= 1e-6 * p.N
+    assert abs(r1.sum() - 1) < 1e-12 and abs(r2.sum() - 1) < 1e-12
+    assert np.all(np.isfinite(x)) and np.abs(x).max() <= 1.0
+
+
 def test_invariants_mass_conservation(srm):
     """sum_p b[p] = sum_{i,n} y_i[n] and sum_r class_mass = N hold for any x."""
     p = synth.make_config("c1", N=3001)
