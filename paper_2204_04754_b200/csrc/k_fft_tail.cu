@@ -47,6 +47,8 @@ struct TailArgs {
     float* par32;             // log2 units: lr1 | lr2 | beta
     double* par64;            // E | E_min
     int nchunk;               // row chunks per class in phases F and Q
+    int* iter;                // device iteration counter (t is read here, +1 after finalize) or NULL
+    int proj_every;           // F of Algorithm 2 (project after t when (t+1) % F == 0; 0 = never)
 };
 
 __device__ inline void grid_sync() { cg::this_grid().sync(); }
@@ -333,6 +335,10 @@ __device__ inline void stamp(const TailArgs& a, int k) {
 
 __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     extern __shared__ double sm[];
+    if (a.iter) {  // graph-replayable: the iteration index and the projection flag come from the device
+        a.t = *reinterpret_cast<volatile int*>(a.iter);
+        a.project = a.proj_every > 0 && ((a.t + 1) % a.proj_every == 0);
+    }
     bool synced = true;
     stamp(a, 0);
     if (a.mode & TAIL_REDUCE) {
@@ -363,6 +369,8 @@ __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
         __syncthreads();
         stamp(a, 5);
     }
+    // every block read the counter before its first grid barrier; block 0 passed at least two since
+    if (a.iter && (a.mode & TAIL_FINALIZE) && blockIdx.x == 0 && threadIdx.x == 0) *a.iter = a.t + 1;
 }
 
 }  // namespace ffttail
@@ -387,6 +395,8 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     a.K = c->K;
     a.t = t;
     a.project = project;
+    a.iter = c->d_iter;
+    a.proj_every = c->opt.proj_every;
     a.trace_cap = c->opt.trace_cap;
     a.tau = c->tau;
     a.inv_2s2 = c->inv_2s2;
@@ -420,8 +430,17 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     cudaError_t e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int grid = fft_tail_grid(c);
-    void* args[] = {&a};
-    return cudaLaunchCooperativeKernel((const void*)k_fft_tail, dim3(grid), dim3(kThreads), args, sm, c->stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers; capturable in a CUDA graph
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_fft_tail, a);
 }
 
 }  // namespace srmra

@@ -130,6 +130,7 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemcpyAsync(c->d_x32, x0, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
     CK(launch_init_obs(c));
     if (c->path == SRMRA_PATH_GEMM) CK(launch_gemm_init(c));
     if (c->path == SRMRA_PATH_FFT) {
@@ -310,6 +311,7 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->d_flag, 1));
     CKI(dalloc(&c->d_counter, 1));
     CKI(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
+    CKI(dalloc(&c->d_iter, 1));
     if (getenv("SRMRA_TAIL_STAMPS")) {
         CKI(dalloc(&c->d_stamps, 8));
         CKI(cudaMemset(c->d_stamps, 0, 8 * sizeof(unsigned long long)));
@@ -382,6 +384,73 @@ int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
+    // FFT path on one rank: replay a captured CUDA graph of one iteration (E/M kernel + cooperative
+    // tail); the tail takes t and the projection flag from the device counter.  With profiling on, the
+    // graph variant carries 4 event-record nodes that are re-pointed to fresh pool events per replay.
+    if (c->path == SRMRA_PATH_FFT && c->opt.world == 1 && !c->graph_failed && n_iters > 0) {
+        cudaGraphExec_t* exec = c->prof ? &c->graph_prof : &c->graph;
+        if (!*exec) {
+            cudaGraph_t g = nullptr;
+            cudaEvent_t ph[4] = {nullptr, nullptr, nullptr, nullptr};
+            bool ok = true;
+            if (c->prof)
+                for (int k = 0; k < 4 && ok; ++k) ok = cudaEventCreate(&ph[k]) == cudaSuccess;
+            ok = ok && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                bool l = true;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[0], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[1], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                l = l && launch_fft_em(c) == cudaSuccess;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[2], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                l = l && launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP, 0, 0) == cudaSuccess;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[3], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && l;
+            }
+            if (ok && c->prof) {  // find the event-record nodes by their placeholder events
+                size_t nn = 0;
+                ok = cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess;
+                std::vector<cudaGraphNode_t> nodes(nn);
+                ok = ok && cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess;
+                for (size_t k = 0; ok && k < nn; ++k) {
+                    cudaGraphNodeType ty;
+                    if (cudaGraphNodeGetType(nodes[k], &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord) continue;
+                    cudaEvent_t ev;
+                    if (cudaGraphEventRecordNodeGetEvent(nodes[k], &ev) != cudaSuccess) continue;
+                    for (int j = 0; j < 4; ++j)
+                        if (ev == ph[j]) c->prof_nodes[j] = nodes[k];
+                }
+                for (int j = 0; j < 4; ++j) ok = ok && c->prof_nodes[j] != nullptr;
+            }
+            if (ok) ok = cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
+            // the profiling variant keeps its graph: exec-node updates refer to the graph's node handles
+            if (g && ok && c->prof) c->graph_prof_src = g;
+            else if (g) cudaGraphDestroy(g);
+            if (!ok) {
+                cudaGetLastError();  // clear the capture error; stream launches are used instead
+                *exec = nullptr;
+                c->graph_failed = true;
+            }
+            // placeholders must outlive the exec (destroying them invalidates its event-record nodes)
+            for (int k = 0; k < 4; ++k) {
+                if (ok && c->prof) c->prof_ph[k] = ph[k];
+                else if (ph[k]) cudaEventDestroy(ph[k]);
+            }
+        }
+        if (*exec) {
+            for (int it = 0; it < n_iters; ++it) {
+                if (c->prof) {
+                    for (int j = 0; j < 4; ++j) {
+                        cudaEvent_t e = c->prof_event();
+                        if (!e) return fail(c, SRMRA_ERR_CUDA, "cudaEventCreate failed");
+                        CK(cudaGraphExecEventRecordNodeSetEvent(*exec, c->prof_nodes[j], e));
+                    }
+                }
+                CK(cudaGraphLaunch(*exec, c->stream));
+                c->iters_done++;
+            }
+            return SRMRA_OK;
+        }
+    }
     for (int it = 0; it < n_iters; ++it) {
         const int t = c->iters_done;
         int rc;
@@ -534,6 +603,12 @@ void srmra_free(srmra_ctx* c) {
     for (void* p : bufs)
         if (p) cudaFree(p);
     gemm_free(c);
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->graph_prof) cudaGraphExecDestroy(c->graph_prof);
+    if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
+    for (int k = 0; k < 4; ++k)
+        if (c->prof_ph[k]) cudaEventDestroy(c->prof_ph[k]);
+    if (c->d_iter) cudaFree(c->d_iter);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;

@@ -72,6 +72,13 @@ struct srmra_ctx {
     double* d_trace = nullptr;  // [trace_cap]
     int* d_flag = nullptr;      // [1] numeric error flag
     unsigned* d_counter = nullptr;  // [1] grid "last block" counter of the fused fold + finalize
+    int* d_iter = nullptr;          // [1] device iteration counter (FFT tail reads t from it)
+    cudaGraphExec_t graph = nullptr;  // captured FFT iteration (E/M kernel + tail), world == 1
+    cudaGraphExec_t graph_prof = nullptr;  // same with 4 event-record nodes (profiling quadruple)
+    cudaGraphNode_t prof_nodes[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaGraph_t graph_prof_src = nullptr;     // kept alive with graph_prof (exec-node updates need it)
+    cudaEvent_t prof_ph[4] = {nullptr, nullptr, nullptr, nullptr};  // capture placeholders, same
+    bool graph_failed = false;
     unsigned long long* d_stamps = nullptr;  // [8] tail-kernel phase timestamps (env SRMRA_TAIL_STAMPS)
     int iters_done = 0;
 
