@@ -19,7 +19,11 @@ def test_header_declares_the_boundary():
 
 
 def test_library_exports_every_declared_symbol():
-    import paper_2204_04754_b200._build as b
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_srmra_build", os.path.join(ROOT, "paper_2204_04754_b200",
+                                                                                 "_build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)        # by path: the package import itself needs the built library
     lib_path = b.build()
     lib = ctypes.CDLL(lib_path)
     for s in declared_symbols():
