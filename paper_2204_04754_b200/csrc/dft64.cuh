@@ -8,17 +8,20 @@ namespace dft64 {
 
 // forward real 2-D DFT of the Ll x Ll image `src` (smem, float64) -> half spectrum `out` (float32),
 // scaled; `tmp` holds Ll x Lh complex; cs/sn: cos/sin(2 pi j / Ll), j < Ll.
-__device__ inline void dft2_real_fwd(const double* src, double2* tmp, const double* cs, const double* sn, int Ll,
-                              double scale, float2* out, int ostride = 1) {
+// out row stride `orow` (>= Lh) float2; src may be float (exact for float32 data) or double.
+template <typename T>
+__device__ inline void dft2_real_fwd(const T* src, double2* tmp, const double* cs, const double* sn, int Ll,
+                                     double scale, float2* out, int orow) {
     const int Lh = Ll / 2 + 1, M = Ll - 1;
     for (int e = threadIdx.x; e < Ll * Lh; e += blockDim.x) {  // along n2: tmp[n1][k2]
         const int n1 = e / Lh, k2 = e - n1 * Lh;
-        const double* row = src + n1 * Ll;
+        const T* row = src + n1 * Ll;
         double re = 0, im = 0;
         for (int n2 = 0; n2 < Ll; ++n2) {
             const int j = (k2 * n2) & M;
-            re = fma(row[n2], cs[j], re);
-            im = fma(-row[n2], sn[j], im);
+            const double xv = (double)row[n2];
+            re = fma(xv, cs[j], re);
+            im = fma(-xv, sn[j], im);
         }
         tmp[e] = make_double2(re, im);
     }
@@ -32,7 +35,7 @@ __device__ inline void dft2_real_fwd(const double* src, double2* tmp, const doub
             re += t.x * cs[j] + t.y * sn[j];  // t * exp(-i theta)
             im += t.y * cs[j] - t.x * sn[j];
         }
-        out[(size_t)e * ostride] = make_float2((float)(re * scale), (float)(im * scale));
+        out[(size_t)k1 * orow + k2] = make_float2((float)(re * scale), (float)(im * scale));
     }
 }
 

@@ -27,101 +27,12 @@
 
 #include <utility>
 
+#include "regfft.cuh"
 #include "srmra_internal.cuh"
 
 namespace srmra {
 namespace fftk {
-
-// ------------------------------------------------------------------ compile-time twiddles
-constexpr double kPi = 3.14159265358979323846264338327950288;
-
-constexpr double sin_series(double x) {
-    double t = x, s = x;
-    for (int n = 1; n < 20; ++n) {
-        t *= -x * x / ((2.0 * n) * (2.0 * n + 1.0));
-        s += t;
-    }
-    return s;
-}
-constexpr double cos_series(double x) {
-    double t = 1.0, s = 1.0;
-    for (int n = 1; n < 20; ++n) {
-        t *= -x * x / ((2.0 * n - 1.0) * (2.0 * n));
-        s += t;
-    }
-    return s;
-}
-// cos(2 pi k / n) and sin(2 pi k / n), exact at multiples of pi/2
-constexpr double cos2pi(int k, int n) {
-    k %= n;
-    if (k < 0) k += n;
-    if (k == 0) return 1.0;
-    if (2 * k == n) return -1.0;
-    if (4 * k == n || 4 * k == 3 * n) return 0.0;
-    return cos_series(2.0 * kPi * k / n);
-}
-constexpr double sin2pi(int k, int n) {
-    k %= n;
-    if (k < 0) k += n;
-    if (k == 0 || 2 * k == n) return 0.0;
-    if (4 * k == n) return 1.0;
-    if (4 * k == 3 * n) return -1.0;
-    return sin_series(2.0 * kPi * k / n);
-}
-constexpr int bitrev(int i, int n) {
-    int r = 0;
-    for (int b = 1; b < n; b <<= 1) {
-        r = (r << 1) | (i & 1);
-        i >>= 1;
-    }
-    return r;
-}
-
-// ------------------------------------------------------------------ register FFT (radix 2)
-// In place, natural order in and out, unnormalised; SIGN = -1 forward, +1 inverse.
-template <int N, int SIGN, int LEN, int I, int J>
-__device__ __forceinline__ void bfly(float2* t) {
-    constexpr int TK = J * (N / LEN);
-    const float2 a = t[I + J], b = t[I + J + LEN / 2];
-    float2 bw;
-    if constexpr (TK == 0) {
-        bw = b;
-    } else if constexpr (4 * TK == N) {
-        if constexpr (SIGN > 0) bw = make_float2(-b.y, b.x);   // b * (+i)
-        else bw = make_float2(b.y, -b.x);                      // b * (-i)
-    } else {
-        constexpr float c = (float)cos2pi(TK, N);
-        constexpr float s = (float)(SIGN * sin2pi(TK, N));
-        bw = make_float2(fmaf(b.x, c, -b.y * s), fmaf(b.x, s, b.y * c));
-    }
-    t[I + J] = make_float2(a.x + bw.x, a.y + bw.y);
-    t[I + J + LEN / 2] = make_float2(a.x - bw.x, a.y - bw.y);
-}
-template <int N, int SIGN, int LEN, int I, int... Js>
-__device__ __forceinline__ void bfly_block(float2* t, std::integer_sequence<int, Js...>) {
-    (bfly<N, SIGN, LEN, I, Js>(t), ...);
-}
-template <int N, int SIGN, int LEN, int... Bs>
-__device__ __forceinline__ void fft_stage(float2* t, std::integer_sequence<int, Bs...>) {
-    (bfly_block<N, SIGN, LEN, Bs * LEN>(t, std::make_integer_sequence<int, LEN / 2>{}), ...);
-}
-template <int N, int SIGN, int... Ls>
-__device__ __forceinline__ void fft_stages(float2* t, std::integer_sequence<int, Ls...>) {
-    (fft_stage<N, SIGN, (2 << Ls)>(t, std::make_integer_sequence<int, N / (2 << Ls)>{}), ...);
-}
-constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
-template <int N, int... Is>
-__device__ __forceinline__ void bitrev_copy(float2* t, const float2* v, std::integer_sequence<int, Is...>) {
-    ((t[Is] = v[bitrev(Is, N)]), ...);
-}
-template <int N, int SIGN>
-__device__ __forceinline__ void fft(float2 (&v)[N]) {
-    float2 t[N];
-    bitrev_copy<N>(t, v, std::make_integer_sequence<int, N>{});
-    fft_stages<N, SIGN>(t, std::make_integer_sequence<int, ilog2(N)>{});
-#pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = t[i];
-}
+using namespace regfft;
 
 // ------------------------------------------------------------------ group sync / reductions
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
@@ -495,12 +406,21 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
 // ==================================================================== host side
 using namespace fftk;
 
+// Yhat row stride (float2): the stored half spectrum Lh = Ll/2 + 1; at Ll = 128 the rows are padded to
+// 72 so that the staged copy is bank-conflict-free for the thread-pair access of k_fft128.cu
+int yrow_of(int Ll) { return Ll == 128 ? 72 : Ll / 2 + 1; }
+
 int ystride_of(int Ll) {
-    const int n = Ll * (Ll / 2 + 1);
-    return (n + 1) & ~1;  // even number of float2 -> 16-byte rows for cp.async
+    const int n = Ll * yrow_of(Ll);
+    return (n + 1) & ~1;  // even number of float2 -> 16-byte rows for cp.async / bulk copies
 }
 
+bool fft128_supported(int K);
+cudaError_t fft128_plan(srmra_ctx* c);
+cudaError_t launch_fft_em128(srmra_ctx* c);
+
 bool fft_supported(int L, int Ll, int K) {
+    if (Ll == 128) return fft128_supported(K);  // k_fft128.cu: class pairs on a CTA cluster
     if (Ll < 2 || Ll > 64 || (Ll & (Ll - 1))) return false;
     if (K * K > 64) return false;
     return true;
@@ -595,10 +515,14 @@ size_t fft_part_float2(const srmra_ctx* c) { return (size_t)c->fft_grid * fft_pa
         default: return cudaErrorInvalidValue;   \
     }
 
-cudaError_t fft_plan(srmra_ctx* c) { SRMRA_LL_DISPATCH(plan_em_t, c) }
+cudaError_t fft_plan(srmra_ctx* c) {
+    if (c->Ll == 128) return fft128_plan(c);
+    SRMRA_LL_DISPATCH(plan_em_t, c)
+}
 
 cudaError_t launch_fft_em(srmra_ctx* c) {
     if (c->n_local == 0) return cudaSuccess;
+    if (c->Ll == 128) return launch_fft_em128(c);
     SRMRA_LL_DISPATCH(launch_em_t, c)
 }
 

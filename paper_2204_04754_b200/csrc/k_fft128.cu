@@ -1,0 +1,545 @@
+// k_fft128.cu — FFT-path E-step + M-step for L_low = 128 (configs[4]: L_high = 256, K = 2).
+//
+// Same mathematics as k_fft.cu (sub-image form of the likelihood; eq:weights_EM,
+// eq:x_EM with P^{-1} := P^T, eq:rho_EM): for observation i and class pair q = (2q, 2q+1)
+//     S_{i,2q} + i S_{i,2q+1} = ifft2( Yhat_i conj(Xhat_2q) + i Yhat_i conj(Xhat_2q+1) )   (E-step scores)
+//     U_q += Yhat_i conj(Z_{i,q}),  V_q += Yhat_i Z_{i,q}(-k),  Z_{i,q} = fft2(w_{i,2q} + i w_{i,2q+1})
+// but at L_low = 128 one pair's 128 x 128 complex working transform (128 KB) and its M-step
+// accumulators (133 KB) no longer fit next to each other in one SM, so the layout changes:
+//
+//  * one CTA per class pair; the K^2/2 pairs of an observation run on the CTAs of ONE thread-block
+//    cluster, which exchange their softmax partials (max reference, max, scaled sum) through
+//    distributed shared memory once per observation (the log-sum-exp over all L_high^2 shifts);
+//  * 256 threads, a thread PAIR per 128-point line: each thread does a 64-point register FFT and
+//    the radix-2 stage across the pair goes through warp shuffles (DIT for the inverse passes:
+//    parity-split input, half-split output; DIF for the forward passes: half-split input,
+//    parity-split output — so the E-row output feeds the M-row input in registers, and the M-col
+//    output keeps k1 and -k1 in the same thread);
+//  * the transpose buffer is an XOR-swizzled 128 x 128 float2 array (conflict-free for all four
+//    access patterns, no padding);
+//  * Yhat_i (row stride 72 float2) is brought into shared memory by ONE bulk copy per observation
+//    (cp.async.bulk + mbarrier), issued as soon as the previous observation's E-column pass is done;
+//  * the M-step accumulators U_q / V_q live in TENSOR MEMORY (256 KB per SM): each thread owns one
+//    TMEM lane segment of 128 columns for its accumulator line and 128 columns for the Yhat values
+//    it read in the E-column pass (exactly the ones its M-column pass needs), tcgen05.ld/st move
+//    them; the two columns (0 and 64) that need both U and V add V through a small shared stage.
+#include <math.h>
+#include <stdlib.h>
+
+#include "regfft.cuh"
+#include "srmra_internal.cuh"
+#include "tcgen05.cuh"
+
+namespace srmra {
+
+int ystride_of(int Ll);
+int fft_partial_bins(int KK, int Ll);
+
+namespace fft128 {
+using namespace regfft;
+
+constexpr int LL = 128, LH = 65, YR = 72, NT = 256, MAXNP = 8;
+constexpr uint32_t YBYTES = LL * YR * 8;  // one observation's staged spectrum, 73,728 B
+
+// dynamic shared memory layout (bytes)
+constexpr int OFF_W = 0;                      // float2 [128][128] swizzled transpose buffer
+constexpr int OFF_Y = OFF_W + LL * LL * 8;    // float2 [128][72]  Yhat_i
+constexpr int OFF_PAR = OFF_Y + (int)YBYTES;  // float [2L + KK] logit bias (log2 units), L <= 512
+constexpr int OFF_ZC = OFF_PAR + 4224;        // float2 [2][128]  Z columns 0 and 64 (V extra)
+constexpr int OFF_YC = OFF_ZC + 2048;         // float2 [2][128]  Yhat columns 0 and 64
+constexpr int OFF_RED = OFF_YC + 2048;        // float2 [16]      block reductions
+constexpr int OFF_XCH = OFF_RED + 128;        // float4 [2][MAXNP] cluster softmax exchange
+constexpr int OFF_MBAR = OFF_XCH + 32 * MAXNP;
+constexpr int OFF_TSLOT = OFF_MBAR + 8;
+constexpr int SMEM = OFF_TSLOT + 8;
+
+// element (r, c) of the transpose buffer: rows 32 apart and the two parities of a column land in
+// different 8-byte bank groups for both row-wise and column-wise thread-pair access
+__device__ __forceinline__ int swz(int r, int c) { return r * LL + (c ^ (((r << 1) & 14) ^ (((r >> 5) & 1) << 3))); }
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float2 cmul_conj(float2 a, float2 b) {  // a * conj(b)
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 shfl_pair(float2 v) {
+    return make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1), __shfl_xor_sync(0xffffffffu, v.y, 1));
+}
+
+// ---------------------------------------------------------------- cluster / bulk copy / TMEM
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_f4(uint32_t local, uint32_t rank, float4 v) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// two 16-column loads and the wait in ONE asm statement (no use of the outputs can be scheduled
+// before the wait)
+__device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float (&va)[16], uint32_t tb, float (&vb)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=f"(va[0]), "=f"(va[1]), "=f"(va[2]), "=f"(va[3]), "=f"(va[4]), "=f"(va[5]), "=f"(va[6]), "=f"(va[7]),
+          "=f"(va[8]), "=f"(va[9]), "=f"(va[10]), "=f"(va[11]), "=f"(va[12]), "=f"(va[13]), "=f"(va[14]),
+          "=f"(va[15]), "=f"(vb[0]), "=f"(vb[1]), "=f"(vb[2]), "=f"(vb[3]), "=f"(vb[4]), "=f"(vb[5]), "=f"(vb[6]),
+          "=f"(vb[7]), "=f"(vb[8]), "=f"(vb[9]), "=f"(vb[10]), "=f"(vb[11]), "=f"(vb[12]), "=f"(vb[13]),
+          "=f"(vb[14]), "=f"(vb[15])
+        : "r"(ta), "r"(tb)
+        : "memory");
+}
+
+// ---------------------------------------------------------------- 128-point FFT over a thread pair
+// w = exp(SIGN 2 pi i / 128).  DIT: in v[m] = x[2m + h]; 64-point FFT F_h; G_1[k] = w^k F_1[k];
+// X[k] = G_0[k] + G_1[k], X[k + 64] = G_0[k] - G_1[k].  Thread h keeps k in [32h, 32h + 32).
+// out v[j] = X[32h + j], v[32 + j] = X[64 + 32h + j].
+template <int SIGN, int J>
+__device__ __forceinline__ void dit_x1(float2 (&v)[64], bool hb, float sh) {
+    constexpr float c0 = (float)cos2pi(J, 128), s0 = (float)(SIGN * sin2pi(J, 128));
+    constexpr float c1 = (float)cos2pi(J + 32, 128), s1 = (float)(SIGN * sin2pi(J + 32, 128));
+    float2 a = v[J], b = v[J + 32];
+    if (hb) {
+        a = make_float2(fmaf(a.x, c0, -a.y * s0), fmaf(a.x, s0, a.y * c0));
+        b = make_float2(fmaf(b.x, c1, -b.y * s1), fmaf(b.x, s1, b.y * c1));
+    }
+    const float2 own = hb ? b : a, snd = hb ? a : b;
+    const float2 rcv = shfl_pair(snd);
+    v[J] = make_float2(own.x + rcv.x, own.y + rcv.y);
+    v[J + 32] = make_float2(sh * (own.x - rcv.x), sh * (own.y - rcv.y));
+}
+template <int SIGN, int... Js>
+__device__ __forceinline__ void dit_xall(float2 (&v)[64], bool hb, float sh, std::integer_sequence<int, Js...>) {
+    (dit_x1<SIGN, Js>(v, hb, sh), ...);
+}
+template <int SIGN>
+__device__ __forceinline__ void dit_pair(float2 (&v)[64], int h) {
+    fft<64, SIGN>(v);
+    dit_xall<SIGN>(v, h != 0, h ? -1.f : 1.f, std::make_integer_sequence<int, 32>{});
+}
+
+// DIF: in v[j] = x[32h + j], v[32 + j] = x[64 + 32h + j]; a[n] = x[n] + x[n+64],
+// b[n] = (x[n] - x[n+64]) w^n; thread 0 transforms a (X[2k]), thread 1 transforms b (X[2k+1]).
+// out v[k] = X[2k + h].
+template <int SIGN, int J>
+__device__ __forceinline__ void dif_x1(float2 (&v)[64], bool hb) {
+    constexpr float c = (float)cos2pi(J, 128), s = (float)(SIGN * sin2pi(J, 128));
+    const float2 x0 = v[J], x1 = v[J + 32];
+    const float2 a = make_float2(x0.x + x1.x, x0.y + x1.y);
+    const float2 d = make_float2(x0.x - x1.x, x0.y - x1.y);
+    float2 b = make_float2(fmaf(d.x, c, -d.y * s), fmaf(d.x, s, d.y * c));
+    if (hb) b = SIGN > 0 ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);  // w^32 = SIGN i
+    const float2 own = hb ? b : a, snd = hb ? a : b;
+    const float2 rcv = shfl_pair(snd);
+    v[J] = hb ? rcv : own;
+    v[J + 32] = hb ? own : rcv;
+}
+template <int SIGN, int... Js>
+__device__ __forceinline__ void dif_xall(float2 (&v)[64], bool hb, std::integer_sequence<int, Js...>) {
+    (dif_x1<SIGN, Js>(v, hb), ...);
+}
+template <int SIGN>
+__device__ __forceinline__ void dif_pair(float2 (&v)[64], int h) {
+    dif_xall<SIGN>(v, h != 0, std::make_integer_sequence<int, 32>{});
+    fft<64, SIGN>(v);
+}
+
+// ---------------------------------------------------------------- block reductions (8 warps)
+__device__ __forceinline__ float cta_max(float v, float2* red, int lane, int warp) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[warp].x = v;
+    __syncthreads();
+    float r = red[0].x;
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) r = fmaxf(r, red[w].x);
+    return r;
+}
+__device__ __forceinline__ void ms_combine(float& m, float& z, float m2, float z2) {
+    const float M = fmaxf(m, m2);
+    if (M == -INFINITY) return;
+    z = z * ex2(m - M) + z2 * ex2(m2 - M);
+    m = M;
+}
+__device__ __forceinline__ void cta_ms(float& m, float& z, float2* red, int lane, int warp) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), z2 = __shfl_xor_sync(0xffffffffu, z, o);
+        ms_combine(m, z, m2, z2);
+    }
+    if (lane == 0) red[8 + warp] = make_float2(m, z);
+    __syncthreads();
+    float M = red[8].x, Z = red[8].y;
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) ms_combine(M, Z, red[8 + w].x, red[8 + w].y);
+    m = M;
+    z = Z;
+}
+
+struct Em128Args {
+    const float2* yhat;   // [n][128][72] rfft2(y_i), float32
+    const double* ynorm;  // [n]
+    const float4* xhat;   // [NP][128][65] pair-interleaved (Xhat_2q, Xhat_2q+1) / L_low^2
+    const float* par32;   // log2 units: lr1[L] | lr2[L] | beta[KK]
+    const double* par64;  // E[KK] | E_min
+    int64_t n;
+    int L, K, KK, NP, PB;
+    float c2;             // log2(e) / sigma^2
+    double c2d, inv_2s2;
+    float2* part;         // [clusters][PB] per-cluster partials (layout of k_fft.cu part_bins)
+    double* llpart;       // [clusters]
+    double* llobs;        // [n]
+};
+
+template <bool PAIRS>
+__global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    float2* W = reinterpret_cast<float2*>(sm + OFF_W);
+    float2* Ys = reinterpret_cast<float2*>(sm + OFF_Y);
+    float* pars = reinterpret_cast<float*>(sm + OFF_PAR);
+    float2* zc = reinterpret_cast<float2*>(sm + OFF_ZC);
+    float2* yc = reinterpret_cast<float2*>(sm + OFF_YC);
+    float2* red = reinterpret_cast<float2*>(sm + OFF_RED);
+    float4* xch = reinterpret_cast<float4*>(sm + OFF_XCH);
+    const uint32_t mbar = tc::smem_u32(sm + OFF_MBAR);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + OFF_TSLOT);
+
+    const int t = threadIdx.x, h = t & 1, l = t >> 1, lane = t & 31, warp = t >> 5;
+    const int NP = a.NP, K = a.K, L = a.L, KK = a.KK;
+    const int q = NP > 1 ? (int)cluster_rank() : 0;
+    const int64_t cl = blockIdx.x / NP, ncl = gridDim.x / NP;
+    const int ra = 2 * q, rb = 2 * q + 1;
+    const bool has_b = PAIRS || rb < KK;
+
+    for (int k = t; k < 2 * L + KK; k += NT) pars[k] = __ldg(a.par32 + k);
+    if (t == 0) {
+        tc::mbar_init(mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(tslot);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    // TMEM: lane = t & 127 (warp w reaches lanes 32 (w & 3) ..); columns [256 (t >> 7), +128) hold the
+    // Yhat values of this thread's line, the next 128 its accumulator line (U or V)
+    const uint32_t trow = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t ty = trow + (uint32_t)((t >> 7) * 256), tacc = ty + 128;
+    {
+        float z[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) tmem_st16(tacc + 16 * ch, z);
+        tmem_wait_st();
+    }
+    int64_t i = cl;
+    if (t == 0 && i < a.n) {
+        mbar_expect_tx(mbar, YBYTES);
+        bulk_g2s(tc::smem_u32(Ys), a.yhat + i * (int64_t)(LL * YR), YBYTES, mbar);
+    }
+
+    // this thread's line: column l (passes 0, 3) / row l (passes 1, 2), half / parity h
+    const bool flip = l >= LH;             // column beyond the stored half spectrum (Hermitian mirror)
+    const bool role_u = l < LH;            // accumulates U_q[., l]; otherwise V_q[., 128 - l]
+    const bool both = (l == 0 || l == LL / 2);  // columns that also need V (added via zc / yc)
+    const float su = role_u ? -1.f : 1.f;  // U: Yhat conj(Z); V: Yhat Z
+    const int sk2 = flip ? LL - l : l;
+    const float sg = flip ? -1.f : 1.f;
+    const float4* XP = a.xhat + (size_t)q * LL * LH;
+    const float* lr1 = pars;
+    const float* lr2 = pars + L;
+    const float* beta = pars + 2 * L;
+    const int ra2 = ra % K, rb2 = rb % K;
+    const float biasA = lr1[ra / K + K * l] + beta[ra];
+    const float biasB = has_b ? lr1[rb / K + K * l] + beta[rb] : 0.f;
+    const double emin = a.par64[KK];
+
+    float rsumA = 0.f, rsumB = 0.f;        // row sums of the posterior (row l, this half), classes ra / rb
+    float2 cu = make_float2(0.f, 0.f);     // sum_i Z_{i,q}[0][l]
+    float2 vex = make_float2(0.f, 0.f);    // V_q[t & 127][64 (t >> 7)] (columns 0 / 64)
+    double ll_acc = 0.0;
+    uint32_t phase = 0;
+    int it = 0;
+    auto vex_update = [&]() {
+        const int col = t >> 7, k1 = t & (LL - 1);
+        const float2 yv = yc[col * LL + k1], z = zc[col * LL + ((LL - k1) & (LL - 1))];
+        vex.x += yv.x * z.x - yv.y * z.y;
+        vex.y += yv.y * z.x + yv.x * z.y;
+    };
+
+    for (; i < a.n; i += ncl, ++it) {
+        tc::mbar_wait(mbar, phase);
+        phase ^= 1;
+        float2 v[64];
+        // ---- pass 0: E-step, inverse along k1 for column k2 = l of Z = Yhat conj(Xa) + i Yhat conj(Xb)
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            float ys[16];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int m = ch * 8 + e;
+                const int k1 = 2 * m + h;
+                const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
+                const float2 yv = Ys[sk1 * YR + sk2];
+                const float4 xv = __ldg(XP + sk1 * LH + sk2);
+                const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
+                const float2 B = has_b ? cmul_conj(yv, make_float2(xv.z, xv.w)) : make_float2(0.f, 0.f);
+                v[m] = make_float2(A.x - sg * B.y, sg * A.y + B.x);
+                ys[2 * e] = yv.x;
+                ys[2 * e + 1] = yv.y;
+            }
+            tmem_st16(ty + 16 * ch, ys);  // the Yhat values this thread's M-column pass needs
+        }
+        dit_pair<1>(v, h);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            W[swz(32 * h + j, l)] = v[j];
+            W[swz(64 + 32 * h + j, l)] = v[32 + j];
+        }
+        __syncthreads();
+        // Yhat_i has been consumed: stream the next observation's spectrum in behind passes 1-3
+        if (t == 0 && i + ncl < a.n) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(mbar, YBYTES);
+            bulk_g2s(tc::smem_u32(Ys), a.yhat + (i + ncl) * (int64_t)(LL * YR), YBYTES, mbar);
+        }
+        if (it > 0) vex_update();  // columns 0 / 64 of the previous observation (zc, yc of its pass 3)
+        // ---- pass 1: E-step, inverse along k2 for row n1 = l -> scores
+#pragma unroll
+        for (int m = 0; m < 64; ++m) v[m] = W[swz(l, 2 * m + h)];
+        dit_pair<1>(v, h);
+        // v[j] = S_a + i S_b at n2 = 32h + j; v[32 + j] at n2 = 64 + 32h + j
+        float lmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
+        const float sref = cta_max(lmax, red, lane, warp);
+        // posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e / sigma^2 + bias
+        float mt = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            const int n2 = 32 * h + j + ((j >> 5) << 5);
+            const float va = fmaf(v[j].x - sref, a.c2, biasA + lr2[ra2 + K * n2]);
+            const float vb = has_b ? fmaf(v[j].y - sref, a.c2, biasB + lr2[rb2 + K * n2]) : -INFINITY;
+            v[j] = make_float2(va, vb);
+            mt = fmaxf(mt, fmaxf(va, vb));
+        }
+        const float mref = mt == -INFINITY ? 0.f : mt;
+        float za = 0.f, zb = 0.f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            const float ea = ex2(v[j].x - mref);
+            const float eb = has_b ? ex2(v[j].y - mref) : 0.f;
+            v[j] = make_float2(ea, eb);
+            za += ea;
+            zb += eb;
+        }
+        float mall = mt, zall = za + zb;
+        cta_ms(mall, zall, red, lane, warp);
+        // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64 offsets)
+        double G, Z;
+        float dq;
+        if (NP > 1) {
+            const int slot = (it & 1) * MAXNP;
+            if (t < NP) st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t, make_float4(sref, mall, zall, 0.f));
+            cluster_sync_all();
+            double gq = -INFINITY;
+            G = -INFINITY;
+            for (int r = 0; r < NP; ++r) {
+                const float4 e = xch[slot + r];
+                const double g = e.y == -INFINITY ? -INFINITY : (double)e.x * a.c2d + (double)e.y;
+                if (r == q) gq = g;
+                G = fmax(G, g);
+            }
+            Z = 0.0;
+            for (int r = 0; r < NP; ++r) {
+                const float4 e = xch[slot + r];
+                if (e.y != -INFINITY) Z += (double)e.z * (double)ex2((float)((double)e.x * a.c2d + (double)e.y - G));
+            }
+            dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
+        } else {
+            G = (double)sref * a.c2d + (double)mall;
+            Z = (double)zall;
+            dq = 0.f;
+        }
+        const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f : ex2(mt - mall + dq) / (float)Z;
+        rsumA = fmaf(za, f, rsumA);
+        rsumB = fmaf(zb, f, rsumB);
+#pragma unroll
+        for (int j = 0; j < 64; ++j) v[j] = make_float2(v[j].x * f, v[j].y * f);
+        if (q == 0 && t == 0) {
+            const double lse = 0.69314718055994530942 * (G + log2(Z)) - (emin + a.ynorm[i]) * a.inv_2s2;
+            ll_acc += lse;
+            if (a.llobs) a.llobs[i] = lse;
+        }
+        // ---- pass 2: M-step, forward along n2 for row l (each thread rewrites the elements it read)
+        dif_pair<-1>(v, h);
+#pragma unroll
+        for (int k = 0; k < 64; ++k) W[swz(l, 2 * k + h)] = v[k];
+        __syncthreads();
+        // ---- pass 3: M-step, forward along n1 for column c = l -> Z_{i,q}[k1 = 2m + h][l]
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            v[j] = W[swz(32 * h + j, l)];
+            v[32 + j] = W[swz(64 + 32 * h + j, l)];
+        }
+        dif_pair<-1>(v, h);
+        if (h == 0) {
+            cu.x += v[0].x;
+            cu.y += v[0].y;
+        }
+        // U_q[2m+h][l] += Yhat conj(Z)  (l < 65);  V_q[-(2m+h)][128-l] += Yhat[-(2m+h)][128-l] Z[2m+h][l]
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            float ys[16], ac[16];
+            tmem_ld16x2(ty + 16 * ch, ys, tacc + 16 * ch, ac);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int m = ch * 8 + e;
+                const float2 z = v[m];
+                const float zy = su * z.y;
+                ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
+                ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
+                if (both) {
+                    zc[(l >> 6) * LL + 2 * m + h] = z;
+                    yc[(l >> 6) * LL + 2 * m + h] = make_float2(ys[2 * e], ys[2 * e + 1]);
+                }
+            }
+            tmem_st16(tacc + 16 * ch, ac);
+        }
+        tmem_wait_st();
+    }
+    __syncthreads();
+    if (it > 0) vex_update();
+
+    // ---- this cluster's partials: U / V of pair q, row sums of classes ra / rb, pair line CU
+    float2* P = a.part + (size_t)cl * a.PB;
+    float2* Uq = P + (size_t)(2 * q) * LL * LH;
+    float2* Vq = Uq + (size_t)LL * LH;
+#pragma unroll
+    for (int ch = 0; ch < 8; ch += 2) {
+        float ac0[16], ac1[16];
+        tmem_ld16x2(tacc + 16 * ch, ac0, tacc + 16 * ch + 16, ac1);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int m = ch * 8 + e;
+            const float2 val = e < 8 ? make_float2(ac0[2 * e], ac0[2 * e + 1]) : make_float2(ac1[2 * e - 16], ac1[2 * e - 15]);
+            if (role_u) Uq[(2 * m + h) * LH + l] = val;
+            else Vq[((LL - 2 * m - h) & (LL - 1)) * LH + (LL - l)] = val;
+        }
+    }
+    Vq[(t & (LL - 1)) * LH + (t >> 7) * (LL / 2)] = vex;
+    float2* R = P + (size_t)2 * NP * LL * LH;  // [KK][LL]
+    float2* CU = R + (size_t)KK * LL;          // [NP][LL]
+    const float rA = rsumA + __shfl_xor_sync(0xffffffffu, rsumA, 1);
+    const float rB = rsumB + __shfl_xor_sync(0xffffffffu, rsumB, 1);
+    if (h == 0) {
+        R[ra * LL + l] = make_float2(rA, 0.f);
+        if (has_b) R[rb * LL + l] = make_float2(rB, 0.f);
+        CU[q * LL + l] = cu;
+    }
+    if (q == 0 && t == 0) a.llpart[cl] = ll_acc;
+    tc::fence_before();
+    __syncthreads();
+    if (NP > 1) cluster_sync_all();  // no peer still writes into this CTA's exchange slots
+    if (warp == 0) tc::tmem_dealloc<512>(*tslot);
+}
+
+}  // namespace fft128
+
+using namespace fft128;
+
+static cudaLaunchConfig_t em128_config(const srmra_ctx* c, cudaLaunchAttribute* attr, int clusters) {
+    const int NP = (c->KK + 1) / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * NP));
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = c->stream;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = NP;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+bool fft128_supported(int K) { return K >= 1 && 2 * MAXNP >= K * K; }
+
+cudaError_t fft128_plan(srmra_ctx* c) {
+    auto kern = (c->KK % 2 == 0) ? k_fft_em128<true> : k_fft_em128<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = em128_config(c, attr, 1);
+    int max_clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+    int64_t clusters = max_clusters;
+    if (clusters > c->n_local) clusters = c->n_local;
+    if (clusters < 1) clusters = 1;
+    c->fft_grid = (int)clusters;  // partial slots (one per cluster)
+    c->fft_groups = (c->KK + 1) / 2;
+    c->fft_threads = NT;
+    c->fft_smem = SMEM;
+    c->fft_xs = false;
+    return cudaSuccess;
+}
+
+cudaError_t launch_fft_em128(srmra_ctx* c) {
+    Em128Args a;
+    a.yhat = c->d_yhat;
+    a.ynorm = c->d_ynorm;
+    a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
+    a.par32 = c->par.f32;
+    a.par64 = c->par.f64;
+    a.n = c->n_local;
+    a.L = c->L;
+    a.K = c->K;
+    a.KK = c->KK;
+    a.NP = (c->KK + 1) / 2;
+    a.PB = fft_partial_bins(c->KK, LL);
+    a.c2 = (float)(1.4426950408889634074 * c->inv_s2);
+    a.c2d = 1.4426950408889634074 * c->inv_s2;
+    a.inv_2s2 = c->inv_2s2;
+    a.part = c->d_part;
+    a.llpart = c->d_llpart;
+    a.llobs = c->d_llobs;
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = em128_config(c, attr, c->fft_grid);
+    if (c->KK % 2 == 0) return cudaLaunchKernelEx(&cfg, k_fft_em128<true>, a);
+    return cudaLaunchKernelEx(&cfg, k_fft_em128<false>, a);
+}
+
+}  // namespace srmra

@@ -9,24 +9,30 @@
 namespace srmra {
 
 int ystride_of(int Ll);
+int yrow_of(int Ll);
 
 namespace fftaux {
 using namespace dft64;
 
-__global__ void k_fft_init(const float* __restrict__ y, int64_t n, int Ll, int ystride, const double* __restrict__ tw,
-                           float2* __restrict__ yhat) {
+__global__ void k_fft_init(const float* __restrict__ y, int64_t n, int Ll, int yrow, int ystride,
+                           const double* __restrict__ tw, float2* __restrict__ yhat) {
     extern __shared__ double sm[];
     const int Lh = Ll / 2 + 1;
     double* cs = sm;
     double* sn = cs + Ll;
-    double* src = sn + Ll;
-    double2* tmp = reinterpret_cast<double2*>(src + Ll * Ll);
+    double2* tmp = reinterpret_cast<double2*>(sn + Ll);                 // [Ll][Lh]
+    float* src = reinterpret_cast<float*>(tmp + (size_t)Ll * Lh);      // [Ll][Ll] (float32 input: exact)
     load_tw(tw, cs, sn, Ll);
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        for (int k = threadIdx.x; k < Ll * Ll; k += blockDim.x) src[k] = (double)y[i * Ll * Ll + k];
+        for (int k = threadIdx.x; k < Ll * Ll; k += blockDim.x) src[k] = y[i * Ll * Ll + k];
         __syncthreads();
-        dft2_real_fwd(src, tmp, cs, sn, Ll, 1.0, yhat + i * ystride);
-        if (threadIdx.x == 0 && ystride > Ll * Lh) yhat[i * ystride + Ll * Lh] = make_float2(0.f, 0.f);
+        float2* out = yhat + i * ystride;
+        dft2_real_fwd(src, tmp, cs, sn, Ll, 1.0, out, yrow);
+        // zero the row padding and the tail pad (never read by the kernels; kept deterministic)
+        for (int k = threadIdx.x; k < ystride; k += blockDim.x) {
+            const int k1 = k / yrow, k2 = k - k1 * yrow;
+            if (k1 >= Ll || k2 >= Lh) out[k] = make_float2(0.f, 0.f);
+        }
         __syncthreads();
     }
 }
@@ -35,7 +41,9 @@ __global__ void k_fft_init(const float* __restrict__ y, int64_t n, int Ll, int y
 
 using namespace fftaux;
 
-static size_t dft_smem(int Ll) { return sizeof(double) * (2 * Ll + Ll * Ll) + sizeof(double2) * Ll * (Ll / 2 + 1); }
+static size_t dft_smem(int Ll) {
+    return sizeof(double) * 2 * Ll + sizeof(double2) * Ll * (Ll / 2 + 1) + sizeof(float) * Ll * Ll;
+}
 
 cudaError_t launch_fft_init(srmra_ctx* c) {
     if (c->n_local == 0) return cudaSuccess;
@@ -43,8 +51,8 @@ cudaError_t launch_fft_init(srmra_ctx* c) {
     cudaError_t e = cudaFuncSetAttribute(k_fft_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int64_t grid = c->n_local < 65536 ? c->n_local : 65536;
-    k_fft_init<<<(unsigned)grid, 256, sm, c->stream>>>(c->d_y, c->n_local, c->Ll, ystride_of(c->Ll), c->d_tw,
-                                                         c->d_yhat);
+    k_fft_init<<<(unsigned)grid, 256, sm, c->stream>>>(c->d_y, c->n_local, c->Ll, yrow_of(c->Ll), ystride_of(c->Ll),
+                                                         c->d_tw, c->d_yhat);
     return cudaGetLastError();
 }
 

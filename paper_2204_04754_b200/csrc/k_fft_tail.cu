@@ -46,7 +46,8 @@ struct TailArgs {
     float2* xhat;             // [NP][Ll][Lh][2]
     float* par32;             // log2 units: lr1 | lr2 | beta
     double* par64;            // E | E_min
-    int nchunk;               // row chunks per class in phases F and Q
+    int nchunk;               // row chunks per class in phase F
+    int nchunk_q, wq;         // phase Q: column chunks per class, columns per chunk
     int* iter;                // device iteration counter (t is read here, +1 after finalize) or NULL
     int proj_every;           // F of Algorithm 2 (project after t when (t+1) % F == 0; 0 = never)
 };
@@ -249,27 +250,30 @@ __device__ void phase_project(const TailArgs& a) {
     }
 }
 
-// ---- phase Q: Xhat of the new x (items (r, ch)) and the logit bias (last item)
+// ---- phase Q: Xhat of the new x (items (r, ch): columns k2 in chunk ch of class r) and the logit bias
+// (last item).  Each item stages x_r (float64), transforms its k2 columns along n2 for every row, then
+// along n1: no work is repeated across items and the shared memory stays below 227 KB at L_low = 128.
 __device__ void phase_prep(const TailArgs& a, double* sm) {
     const int L = a.L, K = a.K, Ll = L / K, Lh = Ll / 2 + 1, KK = K * K, M = Ll - 1;
-    const int R = Ll / a.nchunk;
-    const int nitems = KK * a.nchunk + 1;
+    const int Wq = a.wq, nck = a.nchunk_q;
+    const int nitems = KK * nck + 1;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
         __syncthreads();
-        if (item < KK * a.nchunk) {
-            const int r = item / a.nchunk, ch = item - r * a.nchunk, r1 = r / K, r2 = r % K;
+        if (item < KK * nck) {
+            const int r = item / nck, ch = item - r * nck, r1 = r / K, r2 = r % K;
+            const int k2a = ch * Wq, nw = min(Wq, Lh - k2a);
             double* cs = sm;
             double* sn = cs + Ll;
             double* src = sn + Ll;
-            double2* tmp = reinterpret_cast<double2*>(src + Ll * Ll);
+            double2* tmp = reinterpret_cast<double2*>(src + Ll * Ll);  // [Ll][Wq]
             load_tw(a.tw, cs, sn, Ll);
             for (int m = threadIdx.x; m < Ll * Ll; m += blockDim.x) {
                 const int m1 = m / Ll, m2 = m - m1 * Ll;
                 src[m] = __ldcg(a.x64 + (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L));  // x_r[m]
             }
             __syncthreads();
-            for (int e = threadIdx.x; e < Ll * Lh; e += blockDim.x) {  // along n2 (all rows)
-                const int n1 = e / Lh, k2 = e - n1 * Lh;
+            for (int e = threadIdx.x; e < Ll * nw; e += blockDim.x) {  // along n2: tmp[n1][k2 - k2a]
+                const int n1 = e / nw, kk = e - n1 * nw, k2 = k2a + kk;
                 const double* row = src + n1 * Ll;
                 double re = 0, im = 0;
                 for (int n2 = 0; n2 < Ll; ++n2) {
@@ -277,17 +281,17 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                     re = fma(row[n2], cs[j], re);
                     im = fma(-row[n2], sn[j], im);
                 }
-                tmp[e] = make_double2(re, im);
+                tmp[n1 * Wq + kk] = make_double2(re, im);
             }
             __syncthreads();
             const double scale = 1.0 / ((double)Ll * Ll);
             float2* out = a.xhat + (size_t)(r / 2) * Ll * Lh * 2 + (r & 1);   // pair-interleaved
-            for (int e = threadIdx.x; e < R * Lh; e += blockDim.x) {  // along n1, rows k1 of this chunk
-                const int k1 = ch * R + e / Lh, k2 = e % Lh;
+            for (int e = threadIdx.x; e < Ll * nw; e += blockDim.x) {  // along n1: rows k1, columns of the chunk
+                const int k1 = e / nw, kk = e - k1 * nw, k2 = k2a + kk;
                 double re = 0, im = 0;
                 for (int n1 = 0; n1 < Ll; ++n1) {
                     const int j = (k1 * n1) & M;
-                    const double2 t = tmp[n1 * Lh + k2];
+                    const double2 t = tmp[n1 * Wq + kk];
                     re += t.x * cs[j] + t.y * sn[j];
                     im += t.y * cs[j] - t.x * sn[j];
                 }
@@ -421,11 +425,13 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
     a.nchunk = Ll >= 8 ? Ll / 8 : 1;
+    a.wq = (Lh + a.nchunk - 1) / a.nchunk;
+    a.nchunk_q = (Lh + a.wq - 1) / a.wq;
     const int R = Ll / a.nchunk;
     size_t sm_fold = sizeof(double) * 2 * Ll + sizeof(double2) * ((size_t)Ll * Lh + (size_t)R * Lh);
     const size_t sm_marg = sizeof(double) * (2 * Ll + (size_t)c->KK * (Ll + 2 * Lh));  // marginal item staging
     if (sm_marg > sm_fold) sm_fold = sm_marg;
-    size_t sm_prep = sizeof(double) * (2 * Ll + (size_t)Ll * Ll) + sizeof(double2) * (size_t)Ll * Lh;
+    size_t sm_prep = sizeof(double) * (2 * Ll + (size_t)Ll * Ll) + sizeof(double2) * (size_t)Ll * a.wq;
     const size_t sm = sm_fold > sm_prep ? sm_fold : sm_prep;
     cudaError_t e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

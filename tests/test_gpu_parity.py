@@ -66,6 +66,9 @@ TINY = [  # (L_low, K, N, sigma, seed, rho_zeros)
     (2, 2, 37, 0.7, 0, 0), (4, 2, 41, 0.4, 1, 2), (8, 2, 33, 0.3, 2, 0), (2, 4, 29, 0.5, 3, 1),
     (4, 4, 31, 0.25, 4, 0), (8, 1, 17, 0.5, 5, 0), (16, 1, 9, 0.6, 6, 3), (1, 4, 23, 0.5, 7, 0),
     (16, 2, 19, 0.2, 8, 0), (32, 2, 11, 0.25, 9, 0), (8, 4, 13, 0.125, 10, 2),
+    # L_low = 128 (k_fft128.cu: thread-pair lines, class pairs on a CTA cluster): K = 1 (no cluster,
+    # odd K^2), K = 2 (configs[4] geometry, 2-CTA clusters) with zeros in rho
+    (128, 1, 5, 0.5, 11, 0), (128, 2, 6, 0.35, 12, 2),
 ]
 
 
@@ -105,6 +108,19 @@ def test_c0_monotone_no_projection(srm):
         g = run_gpu(srm, p, path, 15, proj_every=0)
         tr = g["trace"]
         assert np.all(np.diff(tr) >= -1e-6 * np.abs(tr[:-1])), tr
+
+
+def test_c4_geometry_reduced(srm, oracle_mod):
+    """configs[4]'s geometry and recipe (L_high = 256, L_low = 128, K = 2, sigma = 0.5) at N = 24: every
+    path against the oracle element by element, two iterations (the second runs on the first's
+    projected estimate and prepared spectra)."""
+    p = synth.make_config("c4", N=24)
+    x, r1, r2, trace = oracle_mod.run(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, iters=2, proj_every=1)
+    paths = gpu_paths(srm, p)
+    assert "fft" in paths
+    for path in paths:
+        g = run_gpu(srm, p, path, 2)
+        assert_close(g, x, r1, r2, trace, tag="c4/N=24")
 
 
 def test_c1_reduced_three_iters(srm, oracle_mod):
