@@ -499,7 +499,8 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
 }
 
 int fft_partial_bins(int KK, int Ll) { return part_bins(KK, Ll); }
-size_t fft_xhat_float2(int KK, int Ll) { return (size_t)2 * ((KK + 1) / 2) * Ll * (Ll / 2 + 1); }
+// hi plane | lo plane (x_hat = hi + lo, both float32; the lo plane is read by k_fft128.cu)
+size_t fft_xhat_float2(int KK, int Ll) { return (size_t)4 * ((KK + 1) / 2) * Ll * (Ll / 2 + 1); }
 size_t fft_bhat_doubles(int KK, int Ll) { return (size_t)2 * fft_partial_bins(KK, Ll) + 1; }  // + LL
 size_t fft_yhat_stride(int Ll) { return (size_t)ystride_of(Ll); }
 size_t fft_part_float2(const srmra_ctx* c) { return (size_t)c->fft_grid * fft_partial_bins(c->KK, c->Ll); }

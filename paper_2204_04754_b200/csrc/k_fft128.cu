@@ -65,6 +65,11 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ float2 cmul_conj(float2 a, float2 b) {  // a * conj(b)
     return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
+// a * conj(bh + bl) with the small product first (one rounding at the size of the result)
+__device__ __forceinline__ float2 cmul_conj_acc(float2 a, float2 bh, float2 bl) {
+    const float lx = fmaf(a.x, bl.x, a.y * bl.y), ly = fmaf(a.y, bl.x, -a.x * bl.y);
+    return make_float2(fmaf(a.x, bh.x, fmaf(a.y, bh.y, lx)), fmaf(a.y, bh.x, fmaf(-a.x, bh.y, ly)));
+}
 __device__ __forceinline__ float2 shfl_pair(float2 v) {
     return make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1), __shfl_xor_sync(0xffffffffu, v.y, 1));
 }
@@ -209,9 +214,10 @@ __device__ __forceinline__ void cta_ms(float& m, float& z, float2* red, int lane
 struct Em128Args {
     const float2* yhat;   // [n][128][72] rfft2(y_i), float32
     const double* ynorm;  // [n]
-    const float4* xhat;   // [NP][128][65] pair-interleaved (Xhat_2q, Xhat_2q+1) / L_low^2
+    const double* ysum;   // [n] sum_n y_i[n] (the DC bin Yhat_i[0][0], float64)
+    const float4* xhat;   // [2 (hi | lo)][NP][128][65] pair-interleaved (Xhat_2q, Xhat_2q+1) / L_low^2
     const float* par32;   // log2 units: lr1[L] | lr2[L] | beta[KK]
-    const double* par64;  // E[KK] | E_min
+    const double* par64;  // E[KK] | E_min | xm[KK] (mean of x_r)
     int64_t n;
     int L, K, KK, NP, PB;
     float c2;             // log2(e) / sigma^2
@@ -276,6 +282,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const int sk2 = flip ? LL - l : l;
     const float sg = flip ? -1.f : 1.f;
     const float4* XP = a.xhat + (size_t)q * LL * LH;
+    const float4* XPL = XP + (size_t)NP * LL * LH;  // lo plane
     const float* lr1 = pars;
     const float* lr2 = pars + L;
     const float* beta = pars + 2 * L;
@@ -283,6 +290,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const float biasA = lr1[ra / K + K * l] + beta[ra];
     const float biasB = has_b ? lr1[rb / K + K * l] + beta[rb] : 0.f;
     const double emin = a.par64[KK];
+    const double xmA = a.par64[KK + 1 + ra], xmB = has_b ? a.par64[KK + 1 + rb] : 0.0;  // means of x_ra, x_rb
 
     float rsumA = 0.f, rsumB = 0.f;        // row sums of the posterior (row l, this half), classes ra / rb
     float2 cu = make_float2(0.f, 0.f);     // sum_i Z_{i,q}[0][l]
@@ -312,9 +320,15 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
                 const float2 yv = Ys[sk1 * YR + sk2];
                 const float4 xv = __ldg(XP + sk1 * LH + sk2);
-                const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
-                const float2 B = has_b ? cmul_conj(yv, make_float2(xv.z, xv.w)) : make_float2(0.f, 0.f);
+                const float4 xl = __ldg(XPL + sk1 * LH + sk2);
+                // Yhat conj(Xhat_hi + Xhat_lo): the float32 rounding of Xhat is shared by every observation
+                // and would bias the class logits systematically; the lo part removes it
+                const float2 A = cmul_conj_acc(yv, make_float2(xv.x, xv.y), make_float2(xl.x, xl.y));
+                const float2 B = has_b ? cmul_conj_acc(yv, make_float2(xv.z, xv.w), make_float2(xl.z, xl.w))
+                                       : make_float2(0.f, 0.f);
                 v[m] = make_float2(A.x - sg * B.y, sg * A.y + B.x);
+                // the DC bin (constant over the shifts) is added back in float64 after the transform
+                if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
                 ys[2 * e] = yv.x;
                 ys[2 * e + 1] = yv.y;
             }
@@ -338,11 +352,19 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
 #pragma unroll
         for (int m = 0; m < 64; ++m) v[m] = W[swz(l, 2 * m + h)];
         dit_pair<1>(v, h);
-        // v[j] = S_a + i S_b at n2 = 32h + j; v[32 + j] at n2 = 64 + 32h + j
+        // v[j] = S_a + i S_b at n2 = 32h + j; v[32 + j] at n2 = 64 + 32h + j, without the DC terms
+        // D_c = ysum_i mean(x_c) (float64): S_c = v + D_c; scores are kept relative to D_a
+        const double ysi = a.ysum[i];
+        const double Da = ysi * xmA;
+        const float dba = has_b ? (float)(ysi * xmB - Da) : 0.f;
         float lmax = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
+        for (int j = 0; j < 64; ++j) {
+            v[j].y += dba;
+            lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
+        }
         const float sref = cta_max(lmax, red, lane, warp);
+        const double sref_d = Da + (double)sref;  // max score of the pair, float64
         // posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e / sigma^2 + bias
         float mt = -INFINITY;
 #pragma unroll
@@ -368,29 +390,31 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64 offsets)
         double G, Z;
         float dq;
+        // g_q = log2 of this pair's largest unnormalised weight (float64): Sref c2 + m_q
+        const double gq = mall == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)mall;
         if (NP > 1) {
             const int slot = (it & 1) * MAXNP;
-            if (t < NP) st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t, make_float4(sref, mall, zall, 0.f));
+            const unsigned long long gb = (unsigned long long)__double_as_longlong(gq);
+            if (t < NP)
+                st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t,
+                              make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)), zall, 0.f));
             cluster_sync_all();
-            double gq = -INFINITY;
+            double g[MAXNP];
             G = -INFINITY;
             for (int r = 0; r < NP; ++r) {
                 const float4 e = xch[slot + r];
-                const double g = e.y == -INFINITY ? -INFINITY : (double)e.x * a.c2d + (double)e.y;
-                if (r == q) gq = g;
-                G = fmax(G, g);
+                g[r] = __longlong_as_double((long long)(((unsigned long long)__float_as_uint(e.y) << 32) |
+                                                        __float_as_uint(e.x)));
+                G = fmax(G, g[r]);
             }
             Z = 0.0;
-            for (int r = 0; r < NP; ++r) {
-                const float4 e = xch[slot + r];
-                if (e.y != -INFINITY) Z += (double)e.z * (double)ex2((float)((double)e.x * a.c2d + (double)e.y - G));
-            }
-            dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
+            for (int r = 0; r < NP; ++r)
+                if (g[r] != -INFINITY) Z += (double)xch[slot + r].z * (double)ex2((float)(g[r] - G));
         } else {
-            G = (double)sref * a.c2d + (double)mall;
+            G = gq;
             Z = (double)zall;
-            dq = 0.f;
         }
+        dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
         const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f : ex2(mt - mall + dq) / (float)Z;
         rsumA = fmaf(za, f, rsumA);
         rsumB = fmaf(zb, f, rsumB);
@@ -521,6 +545,7 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     Em128Args a;
     a.yhat = c->d_yhat;
     a.ynorm = c->d_ynorm;
+    a.ysum = c->d_ysum;
     a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;

@@ -15,7 +15,8 @@ namespace fftaux {
 using namespace dft64;
 
 __global__ void k_fft_init(const float* __restrict__ y, int64_t n, int Ll, int yrow, int ystride,
-                           const double* __restrict__ tw, float2* __restrict__ yhat) {
+                           const double* __restrict__ tw, float2* __restrict__ yhat, double* __restrict__ ysum) {
+    __shared__ double scratch[32];
     extern __shared__ double sm[];
     const int Lh = Ll / 2 + 1;
     double* cs = sm;
@@ -24,8 +25,14 @@ __global__ void k_fft_init(const float* __restrict__ y, int64_t n, int Ll, int y
     float* src = reinterpret_cast<float*>(tmp + (size_t)Ll * Lh);      // [Ll][Ll] (float32 input: exact)
     load_tw(tw, cs, sn, Ll);
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        for (int k = threadIdx.x; k < Ll * Ll; k += blockDim.x) src[k] = y[i * Ll * Ll + k];
-        __syncthreads();
+        double s = 0.0;
+        for (int k = threadIdx.x; k < Ll * Ll; k += blockDim.x) {
+            const float v = y[i * Ll * Ll + k];
+            src[k] = v;
+            s += (double)v;
+        }
+        s = block_sum(s, scratch);  // (synchronises)
+        if (threadIdx.x == 0) ysum[i] = s;
         float2* out = yhat + i * ystride;
         dft2_real_fwd(src, tmp, cs, sn, Ll, 1.0, out, yrow);
         // zero the row padding and the tail pad (never read by the kernels; kept deterministic)
@@ -52,7 +59,7 @@ cudaError_t launch_fft_init(srmra_ctx* c) {
     if (e != cudaSuccess) return e;
     const int64_t grid = c->n_local < 65536 ? c->n_local : 65536;
     k_fft_init<<<(unsigned)grid, 256, sm, c->stream>>>(c->d_y, c->n_local, c->Ll, yrow_of(c->Ll), ystride_of(c->Ll),
-                                                         c->d_tw, c->d_yhat);
+                                                         c->d_tw, c->d_yhat, c->d_ysum);
     return cudaGetLastError();
 }
 

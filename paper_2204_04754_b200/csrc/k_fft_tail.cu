@@ -43,7 +43,7 @@ struct TailArgs {
     double *x64, *rho, *xtmp, *trace;
     float* x32;
     int* flag;
-    float2* xhat;             // [NP][Ll][Lh][2]
+    float2* xhat;             // [2 (hi | lo)][NP][Ll][Lh][2]
     float* par32;             // log2 units: lr1 | lr2 | beta
     double* par64;            // E | E_min
     int nchunk;               // row chunks per class in phase F
@@ -286,6 +286,7 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
             __syncthreads();
             const double scale = 1.0 / ((double)Ll * Ll);
             float2* out = a.xhat + (size_t)(r / 2) * Ll * Lh * 2 + (r & 1);   // pair-interleaved
+            const size_t lo_plane = (size_t)((KK + 1) / 2) * Ll * Lh * 2;         // x_hat = hi + lo
             for (int e = threadIdx.x; e < Ll * nw; e += blockDim.x) {  // along n1: rows k1, columns of the chunk
                 const int k1 = e / nw, kk = e - k1 * nw, k2 = k2a + kk;
                 double re = 0, im = 0;
@@ -295,22 +296,30 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                     re += t.x * cs[j] + t.y * sn[j];
                     im += t.y * cs[j] - t.x * sn[j];
                 }
-                out[((size_t)k1 * Lh + k2) * 2] = make_float2((float)(re * scale), (float)(im * scale));
+                const double vr = re * scale, vi = im * scale;
+                const float2 hi = make_float2((float)vr, (float)vi);
+                out[((size_t)k1 * Lh + k2) * 2] = hi;
+                out[lo_plane + ((size_t)k1 * Lh + k2) * 2] = make_float2((float)(vr - hi.x), (float)(vi - hi.y));
             }
         } else {
             // logit bias in log2 units: lr = log2 rho, beta_r = (E_min - E_r) log2(e) / (2 sigma^2)
             __shared__ double Es[256];
             const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-            for (int r = warp; r < KK; r += nw) {  // one warp per class: E_r = ||x_r||^2
+            for (int r = warp; r < KK; r += nw) {  // one warp per class: E_r = ||x_r||^2, mean of x_r
                 const int r1 = r / K, r2 = r % K;
-                double s = 0.0;
+                double s = 0.0, sx = 0.0;
                 for (int m = lane; m < Ll * Ll; m += 32) {
                     const int m1 = m / Ll, m2 = m - m1 * Ll;
                     const double v = __ldcg(a.x64 + (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L));
                     s += v * v;
+                    sx += v;
                 }
                 s = warp_sum(s);
-                if (lane == 0) Es[r] = s;
+                sx = warp_sum(sx);
+                if (lane == 0) {
+                    Es[r] = s;
+                    a.par64[KK + 1 + r] = sx / ((double)Ll * Ll);
+                }
             }
             __syncthreads();
             double emin = Es[0];

@@ -391,7 +391,9 @@ __global__ void k_gemm_fold(const float* __restrict__ Z, int64_t ldz, int L, int
 // ==================================================================== host side
 using namespace gemmk;
 
-bool gemm_supported(int L, int Ll, int K) { return Ll >= 4 && (Ll % 4) == 0 && L <= 4096 && K * K <= 256; }
+// L_low <= 64: the fp32 tensor-core accumulation chains (L_low^2 / KSPLIT terms) keep the scores within the
+// parity tolerance; at L_low = 128 the FFT path (k_fft128.cu) is the path.
+bool gemm_supported(int L, int Ll, int K) { return Ll >= 4 && Ll <= 64 && (Ll % 4) == 0 && L <= 4096 && K * K <= 256; }
 
 static int64_t ldw_of(int64_t n) { return ((n + 3) / 4) * 4 > 0 ? ((n + 3) / 4) * 4 : 4; }
 

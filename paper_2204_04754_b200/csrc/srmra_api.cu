@@ -304,7 +304,8 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->d_xtmp, c->L2));
     CKI(dalloc(&c->d_rho, 2 * c->L));
     CKI(dalloc(&c->par.f32, 2 * c->L + c->KK));
-    CKI(dalloc(&c->par.f64, c->KK + 2));
+    CKI(dalloc(&c->par.f64, 2 * c->KK + 2));
+    CKI(cudaMemset(c->par.f64, 0, sizeof(double) * (2 * c->KK + 2)));
     CKI(dalloc(&c->d_colsum, c->L2));
     CKI(dalloc(&c->d_pack, c->pk.total));
     CKI(dalloc(&c->d_trace, opt.trace_cap));
@@ -318,6 +319,7 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     }
     if (path == SRMRA_PATH_FFT) {
         CKI(dalloc(&c->d_yhat, (size_t)n_local * fft_yhat_stride(c->Ll)));
+        CKI(dalloc(&c->d_ysum, n_local));
         CKI(dalloc(&c->d_xhat, fft_xhat_float2(c->KK, c->Ll)));
         CKI(cudaMemset(c->d_xhat, 0, sizeof(float2) * fft_xhat_float2(c->KK, c->Ll)));
         CKI(dalloc(&c->d_bhat, fft_bhat_doubles(c->KK, c->Ll)));
@@ -597,7 +599,7 @@ void srmra_free(srmra_ctx* c) {
         NcclApi& api = nccl();
         if (api.loaded) api.CommDestroy((ncclComm_t)c->nccl_comm);
     }
-    void* bufs[] = {c->d_y, c->d_yhat, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
+    void* bufs[] = {c->d_y, c->d_yhat, c->d_ysum, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
                     c->par.f32, c->par.f64, c->d_xhat, c->d_colsum, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
                     c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps};
     for (void* p : bufs)

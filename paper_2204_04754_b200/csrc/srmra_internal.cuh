@@ -20,7 +20,7 @@ namespace srmra {
 struct IterParams {
     // float32 (device), laid out contiguously: lr1[L] | lr2[L] | beta[K^2]
     float* f32;
-    // float64 (device): E[K^2] | E_min | (unused)
+    // float64 (device): E[K^2] | E_min | xm[K^2] (mean of x_r, fft path)
     double* f64;
 };
 
@@ -48,6 +48,7 @@ struct srmra_ctx {
     float* d_y = nullptr;       // [n][Ll][Ll]             (direct / gemm paths)
     float2* d_yhat = nullptr;   // [n][Ll][Lh]             (fft path: rfft2 of y_i, float32)
     double* d_ynorm = nullptr;  // [n]  ||y_i||^2, float64
+    double* d_ysum = nullptr;   // [n]  sum_n y_i[n], float64 (fft path: the DC term of the scores)
     double* d_llobs = nullptr;  // [n]  per-observation log-likelihood of the last iteration
 
     // theta

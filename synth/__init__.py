@@ -164,14 +164,15 @@ def make_config(name: str, N: int | None = None, seed_offset: int = 0) -> Proble
 
 
 def make_random(L_low: int, K: int, N: int, sigma: float, seed: int,
-                rho_zeros: int = 0, rho_kind: str = "dirichlet") -> Problem:
-    """Randomised small shapes (SURVEY.md §4 'randomised tiny shapes'): blurred-noise image,
+                rho_zeros: int = 0, rho_kind: str = "dirichlet", image: str = "noise") -> Problem:
+    """Randomised small shapes (SURVEY.md §4 'randomised tiny shapes'): blurred-noise image
+    (`image="noise"`) or the blob image of configs[2..4] (`image="blobs"`, 2 L / 8 blobs),
     Dirichlet shift pmfs (optionally with `rho_zeros` exact zeros in the *initial* rho),
     odd N allowed."""
     L = L_low * K
     ss = np.random.SeedSequence([777, L_low, K, N, seed])
     r_img, r_sh, r_noise, r_init = [np.random.Generator(np.random.PCG64(s)) for s in ss.spawn(4)]
-    x = _blurred_noise(r_img, L, max(1.0, L / 16))
+    x = _blobs(r_img, L, max(1, L // 4)) if image == "blobs" else _blurred_noise(r_img, L, max(1.0, L / 16))
     if rho_kind == "dirichlet":
         rho1 = r_sh.dirichlet(np.ones(L))
         rho2 = r_sh.dirichlet(np.ones(L))
