@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsrmra.so")
+# SRMRA_LIB: an alternative in-tree build of the same library (A/B timing of kernel variants, tools/)
+LIB_PATH = os.environ.get("SRMRA_LIB") or os.path.join(_HERE, "libsrmra.so")
 
 SRMRA_OK = 0
 SRMRA_ERR_INVALID_ARG = -1

@@ -51,7 +51,6 @@ __device__ __forceinline__ T group_reduce(T v, T* scratch, int gwarp, int nwarps
     group_bar(bar_id, gthreads);
     T r = scratch[0];
     for (int w = 1; w < nwarps; ++w) r = MAX ? (scratch[w] > r ? scratch[w] : r) : r + scratch[w];
-    group_bar(bar_id, gthreads);  // scratch reusable
     return r;
 }
 
@@ -154,7 +153,6 @@ __device__ __forceinline__ void group_reduce_ms(float& m, float& z, float2* scra
     group_bar(bar_id, gthreads);
     float M = scratch[0].x, Zs = scratch[0].y;
     for (int w = 1; w < nwarps; ++w) ms_combine(M, Zs, scratch[w].x, scratch[w].y);
-    group_bar(bar_id, gthreads);
     m = M;
     z = Zs;
 }
@@ -241,11 +239,9 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
         cp_async_commit();
     };
     prefetch(i, 0);
-
+    cp_async_wait0();
+    group_bar(bar_id, GT);
     for (; i < a.n; i += gstride) {
-        prefetch(i + gstride, buf ^ 1);
-        cp_async_wait1();
-        group_bar(bar_id, GT);
         const float2* Y = Yb + buf * a.ystride;
 
         float2 v[LL];
@@ -348,7 +344,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
                 }
                 mall = mt;
                 zall = za + zb;
-                group_reduce_ms(mall, zall, red2, gwarp, nwarps, lane, bar_id, GT);
+                group_reduce_ms(mall, zall, red2 + 8, gwarp, nwarps, lane, bar_id, GT);  // scratch disjoint from the max
                 if (line_ok) {
                     const float f = ex2(mt - mall) / zall;  // w = e 2^(mt - M) / Z
                     rsumA = fmaf(za, f, rsumA);
@@ -357,18 +353,24 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
                     for (int n2 = 0; n2 < LL; ++n2) v[n2] = make_float2(v[n2].x * f, v[n2].y * f);
                 }
             }
-            if (pass == 0 || pass == 2) group_bar(bar_id, GT);  // Wq complete before the next reader
+            if (pass == 0) {
+                group_bar(bar_id, GT);
+                prefetch(i + gstride, buf ^ 1);
+            } else if (pass == 2) {
+                cp_async_wait0();
+                group_bar(bar_id, GT);
+            }
         }
         if (tg == 0) {
-            const double lse = 0.69314718055994530942 * ((double)mall + log2((double)zall)) +
+            const double lse = 0.69314718055994530942 * ((double)mall + (double)log2f(zall)) +
                                (double)sref * a.inv_s2 - (emin + a.ynorm[i]) * a.inv_2s2;
             ll_acc += lse;
             if (a.llobs) a.llobs[i] = lse;
         }
-        group_bar(bar_id, GT);  // everyone done with Yb[buf] and Wq before they are refilled
         buf ^= 1;
     }
     cp_async_wait0();
+    group_bar(bar_id, GT);
     // register accumulators -> this group's R / CU regions
     float2* R = Acc + 2 * NP * LL * LH;   // [KK][LL]
     float2* CU = R + KK * LL;             // [NP][LL]
