@@ -29,6 +29,7 @@
 
 #include "regfft.cuh"
 #include "srmra_internal.cuh"
+#include "tcgen05.cuh"
 
 namespace srmra {
 namespace fftk {
@@ -80,6 +81,7 @@ struct EmArgs {
     float2* part;           // [gridDim.x][PB] per-CTA partials, see part_bins()
     double* llpart;         // [gridDim.x] per-CTA log-likelihood partials
     double* llobs;          // [n]
+    int tmem_cols;          // TACC: tensor-memory columns allocated per CTA (power of two >= 32)
 };
 
 template <int LL>
@@ -121,10 +123,27 @@ __host__ __device__ inline size_t smem_bytes(int KK, int groups, int ystride) {
     return group_smem<LL>(KK, ystride) * groups + par_bytes<LL>(KK);
 }
 
-// Threads per CTA cap (register budget: one L_low-point complex line per thread lives in registers)
+// TACC (L_low >= 32): the M-step accumulators U_q / V_q live in tensor memory instead of the group's
+// shared memory, which leaves room for more groups (warps) per SM.  Group shared memory then holds
+// Yb [2][ystride] | Wk [NP][LL][WS] | zc [NP][2][LL] | yc [NP][2][LL] | red [32]; at the end the group's
+// partial (layout part_bins) is staged over Yb / Wk.
 template <int LL>
+__host__ __device__ inline size_t group_smem_t(int KK, int ystride) {
+    using G = Geo<LL>;
+    const int NP = (KK + 1) / 2;
+    size_t b = sizeof(float2) * (2 * (size_t)ystride + (size_t)NP * LL * G::WS + 4 * (size_t)NP * LL) +
+               sizeof(double) * 32;
+    return (b + 15) & ~(size_t)15;
+}
+template <int LL>
+__host__ __device__ inline bool tacc_fits(int KK, int ystride) {  // the staged partial fits over Yb / Wk
+    return part_bins(KK, LL) <= 2 * ystride + ((KK + 1) / 2) * LL * Geo<LL>::WS;
+}
+
+// Threads per CTA cap (register budget: one L_low-point complex line per thread lives in registers)
+template <int LL, bool TACC = false>
 __host__ __device__ constexpr int max_cta_threads() {
-    return LL >= 64 ? 256 : (LL >= 32 ? 320 : 512);
+    return LL >= 64 ? 256 : (LL >= 32 ? (TACC ? 384 : 320) : 512);
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -166,8 +185,8 @@ __host__ __device__ inline size_t xs_bytes(int KK) {
     return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (LL / 2 + 1);
 }
 
-template <int LL, bool PAIRS, bool XS>
-__global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
+template <int LL, bool PAIRS, bool XS, bool TACC>
+__global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArgs a) {
     using G = Geo<LL>;
     constexpr int LH = G::LH, WS = G::WS, M = LL - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -191,16 +210,36 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
         float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
         for (int k = threadIdx.x; k < NP * LL * LH; k += blockDim.x) dst[k] = __ldg(src + k);
     }
+    __shared__ uint32_t tmem_slot;
+    if (TACC && threadIdx.x < 32) tc::tmem_alloc_n(&tmem_slot, a.tmem_cols);
+    if (TACC) tc::fence_before();
     __syncthreads();
-    const size_t per_g = group_smem<LL>(KK, a.ystride);
+    if (TACC) tc::fence_after();
+    const size_t per_g = TACC ? group_smem_t<LL>(KK, a.ystride) : group_smem<LL>(KK, a.ystride);
     const int PB = part_bins(KK, LL);
     float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [2][ystride]
     float2* Wk = Yb + 2 * a.ystride;                                    // [NP][LL][WS]
-    float2* Acc = Wk + (size_t)NP * LL * WS;                            // [PB]
-    double* red = reinterpret_cast<double*>(Acc + PB);                  // [32]
+    // TACC: zc | yc | red after Wk, the partial staged over Yb (at the end); else Acc [PB] | red
+    float2* Acc = TACC ? Yb : Wk + (size_t)NP * LL * WS;
+    float2* zc = Wk + (size_t)NP * LL * WS;                             // [NP][2][LL] (TACC)
+    float2* yc = zc + 2 * NP * LL;                                      // [NP][2][LL] (TACC)
+    double* red = reinterpret_cast<double*>(TACC ? yc + 2 * NP * LL : Acc + PB);  // [32]
     float* redf = reinterpret_cast<float*>(red);
     float2* red2 = reinterpret_cast<float2*>(red);
-    for (int k = tg; k < 2 * NP * LL * LH; k += GT) Acc[k] = make_float2(0.f, 0.f);
+    if (!TACC)
+        for (int k = tg; k < 2 * NP * LL * LH; k += GT) Acc[k] = make_float2(0.f, 0.f);
+    // TMEM: warp w reaches lanes 32 (w & 3); a thread's accumulator line (2 LL columns) starts at column
+    // 2 LL (w >> 2) of its lane
+    const int warp = threadIdx.x >> 5;
+    const uint32_t tacc = TACC ? tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * LL) : 0u;
+    if (TACC) {
+        float z[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 2 * LL / 16; ++ch) tc::tmem_st16(tacc + 16 * ch, z);
+        tc::tmem_wait_st();
+    }
 
     const float* lr1 = pars;
     const float* lr2 = pars + L;
@@ -226,6 +265,29 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
     float rsumA = 0.f, rsumB = 0.f;     // row sums of w (class ra / rb, row idx)
     float2 cu = make_float2(0.f, 0.f);  // sum_i Z_{i,q}[0][idx]
     double ll_acc = 0.0;
+    // TACC roles in the M-column pass (column c = idx of pair q): c < LH accumulates U_q[., c], c >= LH
+    // accumulates V_q[., LL - c]; the V columns 0 and LL/2 (from c = 0, LL/2) go through zc / yc into
+    // vex0 / vexh, owned by thread (q, k1 = idx)
+    const bool role_u = idx < LH;
+    const float su = role_u ? -1.f : 1.f;
+    const int ycol = role_u ? idx : LL - idx;
+    const bool vsrc = line_ok && (idx == 0 || idx == LL / 2);
+    float2 vex0 = make_float2(0.f, 0.f), vexh = make_float2(0.f, 0.f);
+    auto vex_update = [&]() {
+        if (line_ok) {
+            const float2* zq = zc + 2 * q * LL;
+            const float2* yq = yc + 2 * q * LL;
+            const int mk = (LL - idx) & M;
+            float2 yv = yq[idx], z = zq[mk];
+            vex0.x += yv.x * z.x - yv.y * z.y;
+            vex0.y += yv.y * z.x + yv.x * z.y;
+            yv = yq[LL + idx];
+            z = zq[LL + mk];
+            vexh.x += yv.x * z.x - yv.y * z.y;
+            vexh.y += yv.y * z.x + yv.x * z.y;
+        }
+    };
+    bool vex_pending = false;
 
     const int64_t gstride = (int64_t)gridDim.x * a.groups;
     int64_t i = (int64_t)blockIdx.x * a.groups + g;
@@ -250,7 +312,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
         // ifft(z) = conj(fft(conj(z))), with the conjugations folded into the loads / score read-out.
 #pragma unroll 1
         for (int pass = 0; pass < 4; ++pass) {
-            if (line_ok) {
+            if (line_ok || (TACC && pass == 3)) {  // tcgen05.ld/st are warp-collective
                 if (pass == 0) {
                     // E-step along k1 (column k2 = idx): conj of Z = Yhat conj(Xhat_ra) + i Yhat conj(Xhat_rb);
                     // columns k2 >= LH by Hermitian symmetry from the stored half
@@ -285,6 +347,31 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
                 } else if (pass == 2) {
 #pragma unroll
                     for (int k2 = 0; k2 < LL; ++k2) Wq[idx * WS + k2] = v[k2];
+                } else if (pass == 3 && TACC) {
+                    // U_q[k1][c] += Yhat[k1][c] conj(Z[k1]) (c < LH) | V_q[k1][LL-c] += Yhat[k1][LL-c] Z[-k1]
+#pragma unroll
+                    for (int ch = 0; ch < 2 * LL / 16; ++ch) {
+                        float ac[16];
+                        tc::tmem_ld16(tacc + 16 * ch, ac);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int k1 = 8 * ch + e;
+                            const float2 yv = Y[k1 * LH + ycol];
+                            const float2 zu = v[k1], zv = v[(LL - k1) & M];
+                            const float zx = role_u ? zu.x : zv.x, zy = su * (role_u ? zu.y : zv.y);
+                            ac[2 * e] = fmaf(yv.x, zx, fmaf(-yv.y, zy, ac[2 * e]));
+                            ac[2 * e + 1] = fmaf(yv.y, zx, fmaf(yv.x, zy, ac[2 * e + 1]));
+                            if (vsrc) {
+                                const int col = idx == 0 ? 0 : LL;
+                                zc[2 * q * LL + col + k1] = zu;
+                                yc[2 * q * LL + col + k1] = yv;
+                            }
+                        }
+                        tc::tmem_st16(tacc + 16 * ch, ac);
+                    }
+                    tc::tmem_wait_st();
+                    cu.x += v[0].x;
+                    cu.y += v[0].y;
                 } else if (pass == 3) {
                     // v[k1] = Z[k1][c]: accumulate U (c < LH), V at column k2 = -c (c == 0 or c >= LL/2)
                     const int c = idx;
@@ -355,6 +442,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
             }
             if (pass == 0) {
                 group_bar(bar_id, GT);
+                if (TACC && vex_pending) vex_update();  // zc / yc of the previous observation (its pass 3)
                 prefetch(i + gstride, buf ^ 1);
             } else if (pass == 2) {
                 cp_async_wait0();
@@ -368,9 +456,36 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
             if (a.llobs) a.llobs[i] = lse;
         }
         buf ^= 1;
+        vex_pending = true;
     }
     cp_async_wait0();
     group_bar(bar_id, GT);
+    if (TACC) {
+        if (vex_pending) vex_update();
+        // stage the TMEM accumulator lines and the V columns 0 / LL/2 as this group's partial (over Yb / Wk;
+        // every thread of the group is past its last use of them)
+        group_bar(bar_id, GT);
+        float2* Uq = Acc + (size_t)(2 * q) * LL * LH;
+        float2* Vq = Uq + (size_t)LL * LH;
+#pragma unroll
+        for (int ch = 0; ch < 2 * LL / 16; ++ch) {
+            float ac[16];
+            tc::tmem_ld16(tacc + 16 * ch, ac);
+            if (line_ok) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int k1 = 8 * ch + e;
+                    const float2 val = make_float2(ac[2 * e], ac[2 * e + 1]);
+                    if (role_u) Uq[k1 * LH + idx] = val;
+                    else Vq[k1 * LH + (LL - idx)] = val;
+                }
+            }
+        }
+        if (line_ok) {
+            Vq[idx * LH] = vex0;
+            Vq[idx * LH + LL / 2] = vexh;
+        }
+    }
     // register accumulators -> this group's R / CU regions
     float2* R = Acc + 2 * NP * LL * LH;   // [KK][LL]
     float2* CU = R + KK * LL;             // [NP][LL]
@@ -384,10 +499,13 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
     // CTA partial (sum over groups in a fixed order) -> global slot of this CTA; the reduce kernel sums
     // the slots in a fixed order (deterministic, no atomics)
     float2* dst = a.part + (size_t)blockIdx.x * PB;
+    const size_t acc_off = TACC ? 0 : 2 * (size_t)a.ystride + (size_t)NP * LL * WS;  // float2 within a group
+    const size_t red_off = TACC ? acc_off + 2 * (size_t)a.ystride + (size_t)NP * LL * WS + 4 * (size_t)NP * LL - acc_off
+                                : acc_off + PB;
     for (int k = threadIdx.x; k < PB; k += blockDim.x) {
         float2 s = make_float2(0.f, 0.f);
         for (int gg = 0; gg < a.groups; ++gg) {
-            const float2* A0 = reinterpret_cast<const float2*>(gbase + per_g * gg) + 2 * a.ystride + (size_t)NP * LL * WS;
+            const float2* A0 = reinterpret_cast<const float2*>(gbase + per_g * gg) + acc_off;
             s.x += A0[k].x;
             s.y += A0[k].y;
         }
@@ -396,10 +514,15 @@ __global__ void __launch_bounds__(max_cta_threads<LL>(), 1) k_fft_em(EmArgs a) {
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int gg = 0; gg < a.groups; ++gg) {
-            const float2* A0 = reinterpret_cast<const float2*>(gbase + per_g * gg) + 2 * a.ystride + (size_t)NP * LL * WS;
-            s += reinterpret_cast<const double*>(A0 + PB)[31];
+            const float2* G0 = reinterpret_cast<const float2*>(gbase + per_g * gg);
+            s += reinterpret_cast<const double*>(G0 + red_off)[31];
         }
         a.llpart[blockIdx.x] = s;
+    }
+    if (TACC) {
+        tc::fence_before();
+        __syncthreads();
+        if (threadIdx.x < 32) tc::tmem_dealloc_n(tmem_slot, a.tmem_cols);
     }
 }
 
@@ -428,41 +551,56 @@ bool fft_supported(int L, int Ll, int K) {
     return true;
 }
 
-template <int LL>
-static cudaError_t plan_em_t(srmra_ctx* c) {
+template <int LL, bool TACC>
+static auto em_kernel(int KK, bool xs) {
+    return (KK % 2 == 0) ? (xs ? k_fft_em<LL, true, true, TACC> : k_fft_em<LL, true, false, TACC>)
+                         : (xs ? k_fft_em<LL, false, true, TACC> : k_fft_em<LL, false, false, TACC>);
+}
+
+template <int LL, bool TACC>
+static cudaError_t plan_em_tt(srmra_ctx* c) {
     const int KK = c->KK;
     const int GT = group_threads<LL>(KK);
     const int ys = ystride_of(LL);
-    if (GT > max_cta_threads<LL>()) return cudaErrorInvalidConfiguration;
-    int groups = max_cta_threads<LL>() / GT;
+    constexpr int MAXT = max_cta_threads<LL, TACC>();
+    if (GT > MAXT) return cudaErrorInvalidConfiguration;
+    auto gsm = [&](int g) { return (TACC ? group_smem_t<LL>(KK, ys) : group_smem<LL>(KK, ys)) * g + par_bytes<LL>(KK); };
+    int groups = MAXT / GT;
     if (groups > 15) groups = 15;
     const char* eg = getenv("SRMRA_FFT_GROUPS");  // tuning override
     if (eg && atoi(eg) > 0 && atoi(eg) < groups) groups = atoi(eg);
     // Xhat staged in shared memory unless that costs a group (SRMRA_FFT_XS=0/1 overrides)
     const size_t xsb = xs_bytes<LL>(KK);
     int g_plain = groups, g_xs = groups;
-    while (g_plain > 1 && smem_bytes<LL>(KK, g_plain, ys) > 227 * 1024) --g_plain;
-    while (g_xs > 1 && smem_bytes<LL>(KK, g_xs, ys) + xsb > 227 * 1024) --g_xs;
+    while (g_plain > 1 && gsm(g_plain) > 227 * 1024) --g_plain;
+    while (g_xs > 1 && gsm(g_xs) + xsb > 227 * 1024) --g_xs;
     // measured on B200 (tools/em_sweep.py, c1 / c3): Xhat in shared memory with one group fewer beats
     // Xhat through L1 with the extra group (164 vs 177 us at c1), so stage it whenever it fits
-    bool xs = smem_bytes<LL>(KK, g_xs, ys) + xsb <= 227 * 1024;
+    bool xs = gsm(g_xs) + xsb <= 227 * 1024;
     const char* ex = getenv("SRMRA_FFT_XS");
-    if (ex) xs = atoi(ex) != 0 && smem_bytes<LL>(KK, 1, ys) + xsb <= 227 * 1024;
+    if (ex) xs = atoi(ex) != 0 && gsm(1) + xsb <= 227 * 1024;
     groups = xs ? g_xs : g_plain;
     // keep enough CTAs for all SMs when N is small
     const int64_t need = (c->n_local + c->num_sms - 1) / c->num_sms;
     if (need < groups) groups = (int)(need < 1 ? 1 : need);
-    const size_t smem = smem_bytes<LL>(KK, groups, ys) + (xs ? xsb : 0);
+    const size_t smem = gsm(groups) + (xs ? xsb : 0);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    auto kern = (KK % 2 == 0) ? (xs ? k_fft_em<LL, true, true> : k_fft_em<LL, true, false>)
-                              : (xs ? k_fft_em<LL, false, true> : k_fft_em<LL, false, false>);
+    auto kern = em_kernel<LL, TACC>(KK, xs);
     c->fft_xs = xs;
+    c->fft_tacc = TACC;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GT * groups, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    // TACC: tensor-memory columns per CTA (one 2 LL-column line per thread, 4 warps share the 128 lanes);
+    // the CTAs resident on one SM must fit the 512 columns together
+    int cols = 32;
+    while (cols < ((GT * groups / 32 + 3) / 4) * 2 * LL) cols *= 2;
+    if (TACC && cols > 512) return cudaErrorInvalidConfiguration;
+    if (TACC && per_sm * cols > 512) per_sm = 512 / cols;
+    c->fft_tmem_cols = TACC ? cols : 0;
     int64_t grid = (int64_t)c->num_sms * per_sm;
     const int64_t max_grid = (c->n_local + groups - 1) / groups;
     if (grid > max_grid) grid = max_grid;
@@ -472,6 +610,18 @@ static cudaError_t plan_em_t(srmra_ctx* c) {
     c->fft_threads = GT * groups;
     c->fft_smem = smem;
     return cudaSuccess;
+}
+
+template <int LL>
+static cudaError_t plan_em_t(srmra_ctx* c) {
+    // tensor-memory accumulators where the staged partial fits (L_low >= 32); SRMRA_FFT_TACC=0 disables
+    const char* et = getenv("SRMRA_FFT_TACC");
+    const bool tacc_ok = LL >= 32 && tacc_fits<LL>(c->KK, ystride_of(LL)) && !(et && atoi(et) == 0);
+    if constexpr (LL >= 32) {
+        if (tacc_ok && plan_em_tt<LL, true>(c) == cudaSuccess) return cudaSuccess;
+        cudaGetLastError();
+    }
+    return plan_em_tt<LL, false>(c);
 }
 
 template <int LL>
@@ -494,9 +644,14 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     a.part = c->d_part;
     a.llpart = c->d_llpart;
     a.llobs = c->d_llobs;
-    auto kern = (c->KK % 2 == 0) ? (c->fft_xs ? k_fft_em<LL, true, true> : k_fft_em<LL, true, false>)
-                                 : (c->fft_xs ? k_fft_em<LL, false, true> : k_fft_em<LL, false, false>);
-    kern<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
+    a.tmem_cols = c->fft_tmem_cols;
+    if constexpr (LL >= 32) {
+        if (c->fft_tacc) {
+            em_kernel<LL, true>(c->KK, c->fft_xs)<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
+            return cudaGetLastError();
+        }
+    }
+    em_kernel<LL, false>(c->KK, c->fft_xs)<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -98,15 +98,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  "l"(src), "r"(bytes), "r"(mbar)
                  : "memory");
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16};" ::"r"(taddr),
-        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
-        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // two 16-column loads and the wait in ONE asm statement (no use of the outputs can be scheduled
 // before the wait)
 __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float (&va)[16], uint32_t tb, float (&vb)[16]) {
@@ -265,8 +256,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) z[j] = 0.f;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) tmem_st16(tacc + 16 * ch, z);
-        tmem_wait_st();
+        for (int ch = 0; ch < 8; ++ch) tc::tmem_st16(tacc + 16 * ch, z);
+        tc::tmem_wait_st();
     }
     int64_t i = cl;
     if (t == 0 && i < a.n) {
@@ -332,7 +323,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 ys[2 * e] = yv.x;
                 ys[2 * e + 1] = yv.y;
             }
-            tmem_st16(ty + 16 * ch, ys);  // the Yhat values this thread's M-column pass needs
+            tc::tmem_st16(ty + 16 * ch, ys);  // the Yhat values this thread's M-column pass needs
         }
         dit_pair<1>(v, h);
 #pragma unroll
@@ -458,9 +449,9 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                     yc[(l >> 6) * LL + 2 * m + h] = make_float2(ys[2 * e], ys[2 * e + 1]);
                 }
             }
-            tmem_st16(tacc + 16 * ch, ac);
+            tc::tmem_st16(tacc + 16 * ch, ac);
         }
-        tmem_wait_st();
+        tc::tmem_wait_st();
     }
     __syncthreads();
     if (it > 0) vex_update();

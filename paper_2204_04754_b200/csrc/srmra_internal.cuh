@@ -67,6 +67,8 @@ struct srmra_ctx {
     double* d_tw = nullptr;     // fft path: cos | sin (2 pi j / L_low), j < L_low, float64
     int fft_grid = 0, fft_groups = 0, fft_threads = 0;
     bool fft_xs = false;        // Xhat staged in shared memory by the E/M kernel
+    bool fft_tacc = false;      // E/M kernel keeps the M-step accumulators in tensor memory
+    int fft_tmem_cols = 0;      // tensor-memory columns per CTA (fft_tacc)
     size_t fft_smem = 0;
     double* d_pack = nullptr;   // packed statistics, see PackLayout
     srmra::PackLayout pk{};
