@@ -150,7 +150,9 @@ SRMRA_API int srmra_profile(srmra_ctx* ctx, int32_t enable);
 SRMRA_API int srmra_profile_read(srmra_ctx* ctx, double* em_kernel_ms, double* iter_ms, int32_t* n_iters);
 
 /* Debug hook: globaltimer stamps (ns) of the FFT path's tail-kernel phase boundaries of the last
- * iteration, out8[0..5] = start, fold, update, projection, prep, end (0 where a phase did not run).
+ * iteration, out8[0..5] = start, fold, update, projection, prep, end (0 where a phase did not run),
+ * out8[6] = earliest and out8[7] = latest start / end over all tail blocks since the previous call
+ * (each call re-arms them).
  * Requires the environment variable SRMRA_TAIL_STAMPS to be set at srmra_init (else SRMRA_ERR_STATE). */
 SRMRA_API int srmra_debug_timestamps(srmra_ctx* ctx, uint64_t* out8);
 

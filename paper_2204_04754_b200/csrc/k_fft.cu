@@ -73,7 +73,7 @@ struct EmArgs {
     const double* ynorm;    // [n]
     const float4* xhat;     // [NP][Ll][Lh] pair-interleaved: (Xhat_{2q}, Xhat_{2q+1}) / Ll^2
     const float* par32;     // log2 units: lr1[L] | lr2[L] | beta[KK]
-    const double* par64;    // E[KK] | E_min
+    const double* par64;    // E[KK] | (unused) | xm[KK]
     int64_t n;
     int L, K, KK, ystride, groups;
     float c2;               // log2(e) / sigma^2
@@ -204,7 +204,12 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     const size_t pb = par_bytes<LL>(KK);
     const size_t xsb = XS ? xs_bytes<LL>(KK) : 0;
     unsigned char* gbase = smem_raw + pb + xsb;
-    for (int k = threadIdx.x; k < 2 * L + KK; k += blockDim.x) pars[k] = __ldg(a.par32 + k);
+    for (int k = threadIdx.x; k < 2 * L; k += blockDim.x) pars[k] = __ldg(a.par32 + k);
+    // class bias beta_r = (E_min - E_r) log2(e) / (2 sigma^2) from E_r (float64, written by the tail)
+    double emin = __ldg(a.par64);
+    for (int r = 1; r < KK; ++r) emin = fmin(emin, __ldg(a.par64 + r));
+    for (int r = threadIdx.x; r < KK; r += blockDim.x)
+        pars[2 * L + r] = (float)((emin - __ldg(a.par64 + r)) * a.inv_2s2 * 1.4426950408889634074);
     if (XS) {
         const float4* src = a.xhat;
         float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
@@ -244,7 +249,6 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     const float* lr1 = pars;
     const float* lr2 = pars + L;
     const float* beta = pars + 2 * L;
-    const double emin = a.par64[KK];
 
     // line owned by this thread in every pass: pair q, index idx (column k2 / row n1 / column c)
     const bool line_ok = tg < NP * LL;
@@ -589,6 +593,8 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     c->fft_xs = xs;
     c->fft_tacc = TACC;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // = the tail's
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GT * groups, smem);

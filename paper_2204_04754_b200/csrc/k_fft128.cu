@@ -208,7 +208,7 @@ struct Em128Args {
     const double* ysum;   // [n] sum_n y_i[n] (the DC bin Yhat_i[0][0], float64)
     const float4* xhat;   // [2 (hi | lo)][NP][128][65] pair-interleaved (Xhat_2q, Xhat_2q+1) / L_low^2
     const float* par32;   // log2 units: lr1[L] | lr2[L] | beta[KK]
-    const double* par64;  // E[KK] | E_min | xm[KK] (mean of x_r)
+    const double* par64;  // E[KK] | (unused) | xm[KK] (mean of x_r)
     int64_t n;
     int L, K, KK, NP, PB;
     float c2;             // log2(e) / sigma^2
@@ -238,7 +238,11 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const int ra = 2 * q, rb = 2 * q + 1;
     const bool has_b = PAIRS || rb < KK;
 
-    for (int k = t; k < 2 * L + KK; k += NT) pars[k] = __ldg(a.par32 + k);
+    for (int k = t; k < 2 * L; k += NT) pars[k] = __ldg(a.par32 + k);
+    // class bias beta_r = (E_min - E_r) log2(e) / (2 sigma^2) from E_r (float64, written by the tail)
+    double emin = __ldg(a.par64);
+    for (int r = 1; r < KK; ++r) emin = fmin(emin, __ldg(a.par64 + r));
+    for (int r = t; r < KK; r += NT) pars[2 * L + r] = (float)((emin - __ldg(a.par64 + r)) * a.inv_2s2 * 1.4426950408889634074);
     if (t == 0) {
         tc::mbar_init(mbar, 1);
         tc::fence_mbar_init();
@@ -280,7 +284,6 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const int ra2 = ra % K, rb2 = rb % K;
     const float biasA = lr1[ra / K + K * l] + beta[ra];
     const float biasB = has_b ? lr1[rb / K + K * l] + beta[rb] : 0.f;
-    const double emin = a.par64[KK];
     const double xmA = a.par64[KK + 1 + ra], xmB = has_b ? a.par64[KK + 1 + rb] : 0.0;  // means of x_ra, x_rb
 
     float rsumA = 0.f, rsumB = 0.f;        // row sums of the posterior (row l, this half), classes ra / rb
@@ -514,6 +517,8 @@ bool fft128_supported(int K) { return K >= 1 && 2 * MAXNP >= K * K; }
 cudaError_t fft128_plan(srmra_ctx* c) {
     auto kern = (c->KK % 2 == 0) ? k_fft_em128<true> : k_fft_em128<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // = the tail's
     if (e != cudaSuccess) return e;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = em128_config(c, attr, 1);

@@ -3,15 +3,20 @@
 // single-block kernels).  All arithmetic is float64.
 //
 //   phase R  (a5)  fixed-order sum of the per-CTA float32 partials of k_fft_em (deterministic)
-//   phase F  (a5)  b_r = irfft2(Bhat_r) / L_low^2 scattered to b[(K m - r) mod L]   (eq:x_EM numerator,
-//                  PAPER.md:255-263 with P^{-1} := P^T), Bhat_{2q} = (U_q+V_q)/2, Bhat_{2q+1} = i(U_q-V_q)/2;
-//                  class mass, marginals (eq:rho_EM) and LL into the pack
-//   phase X  (a7)  rho' = marginals / total; x' = b / A (A = class mass of class (-p mod K)), keep x_t if A <= tau
-//   phase P  (a8)  projection x <- clamp(box3x3(x'), -1, 1)   (Algorithm 2 step 2)
-//   phase Q  (a1)  next iteration's Xhat_r = rfft2(x_r)/L_low^2 (pair-interleaved) and logit bias (log2 units)
-// With world > 1 the host runs phase R alone, all-reduces the accumulators over NCCL, then F..Q.
+//   phase F  (a5, a7)  b_r = irfft2(Bhat_r) / L_low^2 scattered to b[(K m - r) mod L]   (eq:x_EM numerator,
+//                  PAPER.md:255-263 with P^{-1} := P^T), Bhat_{2q} = (U_q+V_q)/2, Bhat_{2q+1} = i(U_q-V_q)/2,
+//                  and in the same item x' = b / A: every pixel of b_r divides by the class mass of class r
+//                  (A[p] is the mass of class (-p mod K) = r), keep x_t if A <= tau; the last item forms the
+//                  class mass, marginals (eq:rho_EM), rho' and the LL
+//   phase Q  (a8, a1)  projection x'' = clamp(box3x3(x'), -1, 1) (Algorithm 2 step 2) evaluated
+//                  while staging each x''_r, then the next iteration's Xhat_r = rfft2(x''_r)/L_low^2
+//                  (pair-interleaved hi + lo), E_r, mean(x''_r) and log2 rho (the E/M kernel derives
+//                  the class bias from E_r)
+// Two grid barriers per iteration.  With world > 1 the host runs phase R alone, all-reduces the
+// accumulators over NCCL, then F and Q.
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "dft64.cuh"
 #include "srmra_internal.cuh"
@@ -98,8 +103,12 @@ __device__ void phase_reduce(const TailArgs& a) {
     }
 }
 
-// ---- phase F: item (r, ch) -> rows [ch R, ch R + R) of b_r;  item KK*nchunk -> mass, marginals, LL
-__device__ void phase_fold(const TailArgs& a, double* sm) {
+// ---- phase F: item (r, ch) -> rows [ch R, ch R + R) of b_r (and x' there when `update`);
+//      item KK*nchunk -> mass, marginals, LL (and rho', the LL trace when `update`)
+__device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
+    __shared__ double red[32];
+    __shared__ double cm_s;
+    int bad = 0;
     const int L = a.L, K = a.K, Ll = L / K, Lh = Ll / 2 + 1, KK = K * K, M = Ll - 1, NP = (KK + 1) / 2;
     const int R = Ll / a.nchunk;
     double* cs = sm;
@@ -114,6 +123,12 @@ __device__ void phase_fold(const TailArgs& a, double* sm) {
         if (item < KK * a.nchunk) {
             const int r = item / a.nchunk, ch = item - r * a.nchunk, r1 = r / K, r2 = r % K;
             const int m1a = ch * R;
+            if (update && threadIdx.x == 0) {  // class mass of class r, summed as in the marginals item
+                const double2* Rr = A + (size_t)2 * NP * Ll * Lh + (size_t)r * Ll;
+                double cmr = 0.0;
+                for (int t = 0; t < Ll; ++t) cmr += __ldcg(&Rr[t].x);
+                cm_s = cmr;
+            }
             const double2* U = A + (size_t)(r / 2) * 2 * Ll * Lh;
             const double2* V = U + (size_t)Ll * Lh;
             for (int e = threadIdx.x; e < Ll * Lh; e += blockDim.x) {
@@ -143,7 +158,13 @@ __device__ void phase_fold(const TailArgs& a, double* sm) {
                     const int j = (k2 * m2) & M;
                     s += 2.0 * (Tr[k2].x * cs[j] - Tr[k2].y * sn[j]);
                 }
-                a.pack[(size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L)] = s * inv;
+                const size_t p = (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L);
+                a.pack[p] = s * inv;
+                if (update) {  // eq:x_EM: x' = b / A, keep x_t where the class is unobserved (A <= tau)
+                    const double v = cm_s > a.tau ? (s * inv) / cm_s : a.x64[p];
+                    bad |= !isfinite(v);
+                    a.xtmp[p] = v;
+                }
             }
         } else {
             // staged in shared memory (the B / T area is free in this item): row sums R [KK][Ll] (real
@@ -183,71 +204,32 @@ __device__ void phase_fold(const TailArgs& a, double* sm) {
                 a.pack[a.off_m1 + s] = a1;
                 a.pack[a.off_m2 + s] = a2 * invL;
             }
-        }
-    }
-}
-
-// ---- phase X: rho' (block 0) and x' = b / A (grid-strided pixels)
-__device__ void phase_update(const TailArgs& a) {
-    __shared__ double red[32];
-    const int L = a.L, K = a.K, KK = K * K, L2 = L * L;
-    if (blockIdx.x == 0) {
-        // eq:rho_EM marginals; zero prior mass stays exactly zero; per-axis normalisation (finalize.cuh)
-        double m1s = 0.0, m2s = 0.0;
-        for (int k = threadIdx.x; k < L; k += blockDim.x) {
-            m1s += a.rho[k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m1 + k), 0.0);
-            m2s += a.rho[L + k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m2 + k), 0.0);
-        }
-        m1s = block_sum(m1s, red);
-        m2s = block_sum(m2s, red);
-        __syncthreads();
-        if (m1s > 0.0 && m2s > 0.0) {
-            for (int k = threadIdx.x; k < L; k += blockDim.x) {
-                a.rho[k] = a.rho[k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m1 + k), 0.0) / m1s;
-                a.rho[L + k] = a.rho[L + k] == 0.0 ? 0.0 : fmax(__ldcg(a.pack + a.off_m2 + k), 0.0) / m2s;
+            if (update) {
+                // eq:rho_EM marginals; zero prior mass stays exactly zero; per-axis normalisation
+                __syncthreads();  // this block's marginal writes visible to the block
+                double m1s = 0.0, m2s = 0.0;
+                for (int k = threadIdx.x; k < L; k += blockDim.x) {
+                    m1s += a.rho[k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m1 + k], 0.0);
+                    m2s += a.rho[L + k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m2 + k], 0.0);
+                }
+                m1s = block_sum(m1s, red);
+                m2s = block_sum(m2s, red);
+                __syncthreads();
+                if (m1s > 0.0 && m2s > 0.0) {
+                    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+                        a.rho[k] = a.rho[k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m1 + k], 0.0) / m1s;
+                        a.rho[L + k] = a.rho[L + k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m2 + k], 0.0) / m2s;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    const double ll = a.pack[a.off_ll];
+                    if (a.t < a.trace_cap) a.trace[a.t] = ll;
+                    bad |= !isfinite(ll);
+                }
             }
         }
     }
-    int bad = 0;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L2; p += gridDim.x * blockDim.x) {
-        const int p1 = p / L, p2 = p - p1 * L;
-        const double A = __ldcg(a.pack + a.off_cm + imod(-p1, K) * K + imod(-p2, K));
-        const double v = A > a.tau ? __ldcg(a.pack + p) / A : a.x64[p];
-        bad |= !isfinite(v);
-        if (a.project) {
-            a.xtmp[p] = v;
-        } else {
-            a.x64[p] = v;
-            a.x32[p] = (float)v;
-        }
-    }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flag, 1);
-    (void)KK;
-}
-
-// ---- phase P: projection D (3x3 circular box, clamp) and the LL trace
-__device__ void phase_project(const TailArgs& a) {
-    const int L = a.L, L2 = L * L;
-    if (a.project) {
-        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < L2; p += gridDim.x * blockDim.x) {
-            const int p1 = p / L, p2 = p - p1 * L;
-            const int rm = (p1 == 0 ? L - 1 : p1 - 1) * L, r0 = p1 * L, rp = (p1 == L - 1 ? 0 : p1 + 1) * L;
-            const int cm1 = p2 == 0 ? L - 1 : p2 - 1, cp1 = p2 == L - 1 ? 0 : p2 + 1;
-            const double* s = a.xtmp;
-            double acc = __ldcg(s + rm + cm1) + __ldcg(s + rm + p2) + __ldcg(s + rm + cp1);
-            acc += __ldcg(s + r0 + cm1) + __ldcg(s + r0 + p2) + __ldcg(s + r0 + cp1);
-            acc += __ldcg(s + rp + cm1) + __ldcg(s + rp + p2) + __ldcg(s + rp + cp1);
-            double v = acc / 9.0;
-            v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
-            a.x64[p] = v;
-            a.x32[p] = (float)v;
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const double ll = __ldcg(a.pack + a.off_ll);
-        if (a.t < a.trace_cap) a.trace[a.t] = ll;
-        if (!isfinite(ll)) atomicOr(a.flag, 1);
-    }
 }
 
 // ---- phase Q: Xhat of the new x (items (r, ch): columns k2 in chunk ch of class r) and the logit bias
@@ -267,9 +249,47 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
             double* src = sn + Ll;
             double2* tmp = reinterpret_cast<double2*>(src + Ll * Ll);  // [Ll][Wq]
             load_tw(a.tw, cs, sn, Ll);
+            // x''_r[m]: after an update, the projection of x' (or x' itself when this iteration does not
+            // project); at load time, x_0.  The ch == 0 item of class r also stores x'' and E_r, mean(x''_r)
+            const bool from_tmp = (a.mode & TAIL_FINALIZE) != 0;
+            double e2 = 0.0, e1 = 0.0;
             for (int m = threadIdx.x; m < Ll * Ll; m += blockDim.x) {
                 const int m1 = m / Ll, m2 = m - m1 * Ll;
-                src[m] = __ldcg(a.x64 + (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L));  // x_r[m]
+                const int p1 = imod(K * m1 - r1, L), p2 = imod(K * m2 - r2, L);
+                double v;
+                if (!from_tmp) {
+                    v = __ldcg(a.x64 + (size_t)p1 * L + p2);
+                } else if (a.project) {
+                    const int rm = (p1 == 0 ? L - 1 : p1 - 1) * L, r0 = p1 * L, rp = (p1 == L - 1 ? 0 : p1 + 1) * L;
+                    const int cm1 = p2 == 0 ? L - 1 : p2 - 1, cp1 = p2 == L - 1 ? 0 : p2 + 1;
+                    const double* xs = a.xtmp;
+                    double acc = __ldcg(xs + rm + cm1) + __ldcg(xs + rm + p2) + __ldcg(xs + rm + cp1);
+                    acc += __ldcg(xs + r0 + cm1) + __ldcg(xs + r0 + p2) + __ldcg(xs + r0 + cp1);
+                    acc += __ldcg(xs + rp + cm1) + __ldcg(xs + rp + p2) + __ldcg(xs + rp + cp1);
+                    v = acc / 9.0;
+                    v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+                } else {
+                    v = __ldcg(a.xtmp + (size_t)p1 * L + p2);
+                }
+                src[m] = v;
+                if (ch == 0) {
+                    e2 += v * v;
+                    e1 += v;
+                    if (from_tmp) {
+                        a.x64[(size_t)p1 * L + p2] = v;
+                        a.x32[(size_t)p1 * L + p2] = (float)v;
+                    }
+                }
+            }
+            if (ch == 0) {
+                __shared__ double redq[32];
+                e2 = block_sum(e2, redq);
+                __syncthreads();
+                e1 = block_sum(e1, redq);
+                if (threadIdx.x == 0) {
+                    a.par64[r] = e2;                            // E_r = ||x_r||^2
+                    a.par64[KK + 1 + r] = e1 / ((double)Ll * Ll);  // mean of x_r (DC term, k_fft128.cu)
+                }
             }
             __syncthreads();
             for (int e = threadIdx.x; e < Ll * nw; e += blockDim.x) {  // along n2: tmp[n1][k2 - k2a]
@@ -302,38 +322,13 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                 out[lo_plane + ((size_t)k1 * Lh + k2) * 2] = make_float2((float)(vr - hi.x), (float)(vi - hi.y));
             }
         } else {
-            // logit bias in log2 units: lr = log2 rho, beta_r = (E_min - E_r) log2(e) / (2 sigma^2)
-            __shared__ double Es[256];
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-            for (int r = warp; r < KK; r += nw) {  // one warp per class: E_r = ||x_r||^2, mean of x_r
-                const int r1 = r / K, r2 = r % K;
-                double s = 0.0, sx = 0.0;
-                for (int m = lane; m < Ll * Ll; m += 32) {
-                    const int m1 = m / Ll, m2 = m - m1 * Ll;
-                    const double v = __ldcg(a.x64 + (size_t)imod(K * m1 - r1, L) * L + imod(K * m2 - r2, L));
-                    s += v * v;
-                    sx += v;
-                }
-                s = warp_sum(s);
-                sx = warp_sum(sx);
-                if (lane == 0) {
-                    Es[r] = s;
-                    a.par64[KK + 1 + r] = sx / ((double)Ll * Ll);
-                }
-            }
-            __syncthreads();
-            double emin = Es[0];
-            for (int r = 1; r < KK; ++r) emin = fmin(emin, Es[r]);
+            // log2 of the shift marginals (log 0 = -inf); the class bias beta_r = (E_min - E_r) log2(e) /
+            // (2 sigma^2) is formed by the E/M kernel from E_r (written by the ch == 0 items)
             for (int k = threadIdx.x; k < L; k += blockDim.x) {
                 const double p1 = __ldcg(a.rho + k), p2 = __ldcg(a.rho + L + k);
                 a.par32[k] = p1 > 0.0 ? (float)log2(p1) : -INFINITY;
                 a.par32[L + k] = p2 > 0.0 ? (float)log2(p2) : -INFINITY;
             }
-            for (int r = threadIdx.x; r < KK; r += blockDim.x) {
-                a.par32[2 * L + r] = (float)((emin - Es[r]) * a.inv_2s2 * 1.4426950408889634074);
-                a.par64[r] = Es[r];
-            }
-            if (threadIdx.x == 0) a.par64[KK] = emin;
         }
     }
 }
@@ -354,6 +349,11 @@ __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     }
     bool synced = true;
     stamp(a, 0);
+    if (a.stamps && threadIdx.x == 0) {  // earliest block start
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        atomicMin(a.stamps + 6, t0);
+    }
     if (a.mode & TAIL_REDUCE) {
         phase_reduce(a);
         synced = false;
@@ -361,16 +361,7 @@ __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     if (a.mode & TAIL_FOLD) {
         if (!synced) grid_sync();
         stamp(a, 1);
-        phase_fold(a, sm);
-        synced = false;
-    }
-    if (a.mode & TAIL_FINALIZE) {
-        grid_sync();
-        stamp(a, 2);
-        phase_update(a);
-        grid_sync();
-        stamp(a, 3);
-        phase_project(a);
+        phase_fold(a, sm, (a.mode & TAIL_FINALIZE) != 0);
         synced = false;
     }
     if (a.mode & TAIL_PREP) {
@@ -381,8 +372,13 @@ __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     if (a.stamps) {
         __syncthreads();
         stamp(a, 5);
+        if (threadIdx.x == 0) {  // latest block end
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            atomicMax(a.stamps + 7, t1);
+        }
     }
-    // every block read the counter before its first grid barrier; block 0 passed at least two since
+    // every block read the counter before its first grid barrier; block 0 passed at least one since
     if (a.iter && (a.mode & TAIL_FINALIZE) && blockIdx.x == 0 && threadIdx.x == 0) *a.iter = a.t + 1;
 }
 
@@ -443,6 +439,9 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     size_t sm_prep = sizeof(double) * (2 * Ll + (size_t)Ll * Ll) + sizeof(double2) * (size_t)Ll * a.wq;
     const size_t sm = sm_fold > sm_prep ? sm_fold : sm_prep;
     cudaError_t e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    // same L1 / shared-memory split as the E/M kernel before it: no carve-out reconfiguration between them
+    e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     const int grid = fft_tail_grid(c);
     cudaLaunchConfig_t cfg = {};

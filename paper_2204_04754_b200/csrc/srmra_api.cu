@@ -314,8 +314,8 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
     CKI(dalloc(&c->d_iter, 1));
     if (getenv("SRMRA_TAIL_STAMPS")) {
-        CKI(dalloc(&c->d_stamps, 8));
-        CKI(cudaMemset(c->d_stamps, 0, 8 * sizeof(unsigned long long)));
+        CKI(dalloc(&c->d_stamps, 16));
+        CKI(cudaMemset(c->d_stamps, 0, 16 * sizeof(unsigned long long)));
     }
     if (path == SRMRA_PATH_FFT) {
         CKI(dalloc(&c->d_yhat, (size_t)n_local * fft_yhat_stride(c->Ll)));
@@ -581,6 +581,9 @@ int srmra_debug_timestamps(srmra_ctx* c, uint64_t* out8) {
     if (!c->d_stamps) return fail(c, SRMRA_ERR_STATE, "set SRMRA_TAIL_STAMPS before srmra_init");
     CK(cudaMemcpyAsync(out8, c->d_stamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    // re-arm the cross-block extremes: [6] earliest tail-block start (min), [7] latest tail-block end (max)
+    const uint64_t arm[2] = {~0ull, 0ull};
+    CK(cudaMemcpy(c->d_stamps + 6, arm, sizeof(arm), cudaMemcpyHostToDevice));
     return SRMRA_OK;
 }
 
