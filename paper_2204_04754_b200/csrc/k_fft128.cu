@@ -49,7 +49,8 @@ constexpr int OFF_ZC = OFF_PAR + 4224;        // float2 [2][128]  Z columns 0 an
 constexpr int OFF_YC = OFF_ZC + 2048;         // float2 [2][128]  Yhat columns 0 and 64
 constexpr int OFF_RED = OFF_YC + 2048;        // float2 [16]      block reductions
 constexpr int OFF_XCH = OFF_RED + 128;        // float4 [2][MAXNP] cluster softmax exchange
-constexpr int OFF_MBAR = OFF_XCH + 32 * MAXNP;
+constexpr int OFF_LRP = OFF_XCH + 32 * MAXNP;    // float2 [2][65] lr2 table per (half, element)
+constexpr int OFF_MBAR = OFF_LRP + 8 * 2 * 65 + 16;
 constexpr int OFF_TSLOT = OFF_MBAR + 8;
 constexpr int SMEM = OFF_TSLOT + 8;
 
@@ -138,12 +139,6 @@ template <int SIGN, int... Js>
 __device__ __forceinline__ void dit_xall(float2 (&v)[64], bool hb, float sh, std::integer_sequence<int, Js...>) {
     (dit_x1<SIGN, Js>(v, hb, sh), ...);
 }
-template <int SIGN>
-__device__ __forceinline__ void dit_pair(float2 (&v)[64], int h) {
-    fft<64, SIGN>(v);
-    dit_xall<SIGN>(v, h != 0, h ? -1.f : 1.f, std::make_integer_sequence<int, 32>{});
-}
-
 // DIF: in v[j] = x[32h + j], v[32 + j] = x[64 + 32h + j]; a[n] = x[n] + x[n+64],
 // b[n] = (x[n] - x[n+64]) w^n; thread 0 transforms a (X[2k]), thread 1 transforms b (X[2k+1]).
 // out v[k] = X[2k + h].
@@ -164,12 +159,6 @@ template <int SIGN, int... Js>
 __device__ __forceinline__ void dif_xall(float2 (&v)[64], bool hb, std::integer_sequence<int, Js...>) {
     (dif_x1<SIGN, Js>(v, hb), ...);
 }
-template <int SIGN>
-__device__ __forceinline__ void dif_pair(float2 (&v)[64], int h) {
-    dif_xall<SIGN>(v, h != 0, std::make_integer_sequence<int, 32>{});
-    fft<64, SIGN>(v);
-}
-
 // ---------------------------------------------------------------- block reductions (8 warps)
 __device__ __forceinline__ float cta_max(float v, float2* red, int lane, int warp) {
 #pragma unroll
@@ -228,6 +217,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     float2* yc = reinterpret_cast<float2*>(sm + OFF_YC);
     float2* red = reinterpret_cast<float2*>(sm + OFF_RED);
     float4* xch = reinterpret_cast<float4*>(sm + OFF_XCH);
+    float2* lrp = reinterpret_cast<float2*>(sm + OFF_LRP);
     const uint32_t mbar = tc::smem_u32(sm + OFF_MBAR);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + OFF_TSLOT);
 
@@ -286,6 +276,14 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const float biasB = has_b ? lr1[rb / K + K * l] + beta[rb] : 0.f;
     const double xmA = a.par64[KK + 1 + ra], xmB = has_b ? a.par64[KK + 1 + rb] : 0.0;  // means of x_ra, x_rb
 
+    // lr2 of (class ra, class rb) at the n2 of (half h, element j): n2 = 32h + j + 32 (j >= 32); rows
+    // padded to 65 so the two halves of a warp read different banks
+    for (int k = t; k < 2 * 65; k += NT) {
+        const int hh = k / 65, j = k - hh * 65;
+        const int n2 = 32 * hh + j + ((j >> 5) << 5);
+        lrp[k] = j < 64 ? make_float2(lr2[ra2 + K * n2], has_b ? lr2[rb2 + K * n2] : 0.f) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
     float rsumA = 0.f, rsumB = 0.f;        // row sums of the posterior (row l, this half), classes ra / rb
     float2 cu = make_float2(0.f, 0.f);     // sum_i Z_{i,q}[0][l]
     float2 vex = make_float2(0.f, 0.f);    // V_q[t & 127][64 (t >> 7)] (columns 0 / 64)
@@ -299,162 +297,180 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         vex.y += yv.y * z.x + yv.x * z.y;
     };
 
+    // One forward 64-point FFT body serves all four passes (the kernel is otherwise instruction-fetch
+    // bound): the two inverse passes use ifft(z) = conj(fft(conj z)) — the conjugation is folded into
+    // the E-column input (conj Z) and the score read-out (S = conj of the E-row output).
     for (; i < a.n; i += ncl, ++it) {
         tc::mbar_wait(mbar, phase);
         phase ^= 1;
         float2 v[64];
-        // ---- pass 0: E-step, inverse along k1 for column k2 = l of Z = Yhat conj(Xa) + i Yhat conj(Xb)
+        float za = 0.f, zb = 0.f, mt = -INFINITY, mall = 0.f, zall = 1.f;
+        double G = 0.0, Z = 1.0;
+#pragma unroll 1
+        for (int pass = 0; pass < 4; ++pass) {
+            if (pass == 0) {
+                // E-step along k1 for column k2 = l: conj of Z = Yhat conj(Xa) + i Yhat conj(Xb)
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-            float ys[16];
+                for (int ch = 0; ch < 8; ++ch) {
+                    float ys[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int m = ch * 8 + e;
-                const int k1 = 2 * m + h;
-                const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
-                const float2 yv = Ys[sk1 * YR + sk2];
-                const float4 xv = __ldg(XP + sk1 * LH + sk2);
-                const float4 xl = __ldg(XPL + sk1 * LH + sk2);
-                // Yhat conj(Xhat_hi + Xhat_lo): the float32 rounding of Xhat is shared by every observation
-                // and would bias the class logits systematically; the lo part removes it
-                const float2 A = cmul_conj_acc(yv, make_float2(xv.x, xv.y), make_float2(xl.x, xl.y));
-                const float2 B = has_b ? cmul_conj_acc(yv, make_float2(xv.z, xv.w), make_float2(xl.z, xl.w))
-                                       : make_float2(0.f, 0.f);
-                v[m] = make_float2(A.x - sg * B.y, sg * A.y + B.x);
-                // the DC bin (constant over the shifts) is added back in float64 after the transform
-                if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
-                ys[2 * e] = yv.x;
-                ys[2 * e + 1] = yv.y;
-            }
-            tc::tmem_st16(ty + 16 * ch, ys);  // the Yhat values this thread's M-column pass needs
-        }
-        dit_pair<1>(v, h);
+                    for (int e = 0; e < 8; ++e) {
+                        const int m = ch * 8 + e;
+                        const int k1 = 2 * m + h;
+                        const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
+                        const float2 yv = Ys[sk1 * YR + sk2];
+                        const float4 xv = __ldg(XP + sk1 * LH + sk2);
+                        const float4 xl = __ldg(XPL + sk1 * LH + sk2);
+                        // Yhat conj(Xhat_hi + Xhat_lo): the float32 rounding of Xhat is shared by every
+                        // observation and would bias the class logits systematically; the lo part removes it
+                        const float2 A = cmul_conj_acc(yv, make_float2(xv.x, xv.y), make_float2(xl.x, xl.y));
+                        const float2 B = has_b ? cmul_conj_acc(yv, make_float2(xv.z, xv.w), make_float2(xl.z, xl.w))
+                                               : make_float2(0.f, 0.f);
+                        v[m] = make_float2(A.x - sg * B.y, -(sg * A.y + B.x));
+                        // the DC bin (constant over the shifts) is added back in float64 after the transform
+                        if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
+                        ys[2 * e] = yv.x;
+                        ys[2 * e + 1] = yv.y;
+                    }
+                    tc::tmem_st16(ty + 16 * ch, ys);  // the Yhat values this thread's M-column pass needs
+                }
+            } else if (pass == 1) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            W[swz(32 * h + j, l)] = v[j];
-            W[swz(64 + 32 * h + j, l)] = v[32 + j];
-        }
-        __syncthreads();
-        // Yhat_i has been consumed: stream the next observation's spectrum in behind passes 1-3
-        if (t == 0 && i + ncl < a.n) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(mbar, YBYTES);
-            bulk_g2s(tc::smem_u32(Ys), a.yhat + (i + ncl) * (int64_t)(LL * YR), YBYTES, mbar);
-        }
-        if (it > 0) vex_update();  // columns 0 / 64 of the previous observation (zc, yc of its pass 3)
-        // ---- pass 1: E-step, inverse along k2 for row n1 = l -> scores
+                for (int m = 0; m < 64; ++m) v[m] = W[swz(l, 2 * m + h)];
+            } else if (pass == 3) {
 #pragma unroll
-        for (int m = 0; m < 64; ++m) v[m] = W[swz(l, 2 * m + h)];
-        dit_pair<1>(v, h);
-        // v[j] = S_a + i S_b at n2 = 32h + j; v[32 + j] at n2 = 64 + 32h + j, without the DC terms
-        // D_c = ysum_i mean(x_c) (float64): S_c = v + D_c; scores are kept relative to D_a
-        const double ysi = a.ysum[i];
-        const double Da = ysi * xmA;
-        const float dba = has_b ? (float)(ysi * xmB - Da) : 0.f;
-        float lmax = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-            v[j].y += dba;
-            lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
-        }
-        const float sref = cta_max(lmax, red, lane, warp);
-        const double sref_d = Da + (double)sref;  // max score of the pair, float64
-        // posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e / sigma^2 + bias
-        float mt = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-            const int n2 = 32 * h + j + ((j >> 5) << 5);
-            const float va = fmaf(v[j].x - sref, a.c2, biasA + lr2[ra2 + K * n2]);
-            const float vb = has_b ? fmaf(v[j].y - sref, a.c2, biasB + lr2[rb2 + K * n2]) : -INFINITY;
-            v[j] = make_float2(va, vb);
-            mt = fmaxf(mt, fmaxf(va, vb));
-        }
-        const float mref = mt == -INFINITY ? 0.f : mt;
-        float za = 0.f, zb = 0.f;
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-            const float ea = ex2(v[j].x - mref);
-            const float eb = has_b ? ex2(v[j].y - mref) : 0.f;
-            v[j] = make_float2(ea, eb);
-            za += ea;
-            zb += eb;
-        }
-        float mall = mt, zall = za + zb;
-        cta_ms(mall, zall, red, lane, warp);
-        // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64 offsets)
-        double G, Z;
-        float dq;
-        // g_q = log2 of this pair's largest unnormalised weight (float64): Sref c2 + m_q
-        const double gq = mall == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)mall;
-        if (NP > 1) {
-            const int slot = (it & 1) * MAXNP;
-            const unsigned long long gb = (unsigned long long)__double_as_longlong(gq);
-            if (t < NP)
-                st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t,
-                              make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)), zall, 0.f));
-            cluster_sync_all();
-            double g[MAXNP];
-            G = -INFINITY;
-            for (int r = 0; r < NP; ++r) {
-                const float4 e = xch[slot + r];
-                g[r] = __longlong_as_double((long long)(((unsigned long long)__float_as_uint(e.y) << 32) |
-                                                        __float_as_uint(e.x)));
-                G = fmax(G, g[r]);
-            }
-            Z = 0.0;
-            for (int r = 0; r < NP; ++r)
-                if (g[r] != -INFINITY) Z += (double)xch[slot + r].z * (double)ex2((float)(g[r] - G));
-        } else {
-            G = gq;
-            Z = (double)zall;
-        }
-        dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
-        const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f : ex2(mt - mall + dq) / (float)Z;
-        rsumA = fmaf(za, f, rsumA);
-        rsumB = fmaf(zb, f, rsumB);
-#pragma unroll
-        for (int j = 0; j < 64; ++j) v[j] = make_float2(v[j].x * f, v[j].y * f);
-        if (q == 0 && t == 0) {
-            const double lse = 0.69314718055994530942 * (G + log2(Z)) - (emin + a.ynorm[i]) * a.inv_2s2;
-            ll_acc += lse;
-            if (a.llobs) a.llobs[i] = lse;
-        }
-        // ---- pass 2: M-step, forward along n2 for row l (each thread rewrites the elements it read)
-        dif_pair<-1>(v, h);
-#pragma unroll
-        for (int k = 0; k < 64; ++k) W[swz(l, 2 * k + h)] = v[k];
-        __syncthreads();
-        // ---- pass 3: M-step, forward along n1 for column c = l -> Z_{i,q}[k1 = 2m + h][l]
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            v[j] = W[swz(32 * h + j, l)];
-            v[32 + j] = W[swz(64 + 32 * h + j, l)];
-        }
-        dif_pair<-1>(v, h);
-        if (h == 0) {
-            cu.x += v[0].x;
-            cu.y += v[0].y;
-        }
-        // U_q[2m+h][l] += Yhat conj(Z)  (l < 65);  V_q[-(2m+h)][128-l] += Yhat[-(2m+h)][128-l] Z[2m+h][l]
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-            float ys[16], ac[16];
-            tmem_ld16x2(ty + 16 * ch, ys, tacc + 16 * ch, ac);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int m = ch * 8 + e;
-                const float2 z = v[m];
-                const float zy = su * z.y;
-                ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
-                ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
-                if (both) {
-                    zc[(l >> 6) * LL + 2 * m + h] = z;
-                    yc[(l >> 6) * LL + 2 * m + h] = make_float2(ys[2 * e], ys[2 * e + 1]);
+                for (int j = 0; j < 32; ++j) {
+                    v[j] = W[swz(32 * h + j, l)];
+                    v[32 + j] = W[swz(64 + 32 * h + j, l)];
                 }
             }
-            tc::tmem_st16(tacc + 16 * ch, ac);
+            // pass 2: v holds the posterior row of the pair (forward transform along n2)
+            if (pass >= 2) dif_xall<-1>(v, h != 0, std::make_integer_sequence<int, 32>{});
+            fft<64, -1>(v);
+            if (pass < 2) dit_xall<-1>(v, h != 0, h ? -1.f : 1.f, std::make_integer_sequence<int, 32>{});
+
+            if (pass == 0) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    W[swz(32 * h + j, l)] = v[j];
+                    W[swz(64 + 32 * h + j, l)] = v[32 + j];
+                }
+                __syncthreads();
+                // Yhat_i has been consumed: stream the next observation's spectrum in behind passes 1-3
+                if (t == 0 && i + ncl < a.n) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(mbar, YBYTES);
+                    bulk_g2s(tc::smem_u32(Ys), a.yhat + (i + ncl) * (int64_t)(LL * YR), YBYTES, mbar);
+                }
+                if (it > 0) vex_update();  // columns 0 / 64 of the previous observation (zc, yc of its pass 3)
+            } else if (pass == 1) {
+                // S_a + i S_b = conj(v) at n2 = 32h + j (v[j]) and 64 + 32h + j (v[32 + j]), without the DC
+                // terms D_c = ysum_i mean(x_c) (float64): S_c = . + D_c; scores are kept relative to D_a
+                const double ysi = a.ysum[i];
+                const double Da = ysi * xmA;
+                const float dba = has_b ? (float)(ysi * xmB - Da) : 0.f;
+                float lmax = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) {
+                    v[j].y = dba - v[j].y;
+                    lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
+                }
+                const float sref = cta_max(lmax, red, lane, warp);
+                const double sref_d = Da + (double)sref;  // max score of the pair, float64
+                // posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e / sigma^2 + bias
+#pragma unroll
+                for (int j = 0; j < 64; ++j) {
+                    const float2 b2 = lrp[h * 65 + j];  // lr2 of (class ra, class rb) at this thread's n2
+                    const float va = fmaf(v[j].x - sref, a.c2, biasA + b2.x);
+                    const float vb = has_b ? fmaf(v[j].y - sref, a.c2, biasB + b2.y) : -INFINITY;
+                    v[j] = make_float2(va, vb);
+                    mt = fmaxf(mt, fmaxf(va, vb));
+                }
+                const float mref = mt == -INFINITY ? 0.f : mt;
+                float za1 = 0.f, zb1 = 0.f;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) {
+                    const float ea = ex2(v[j].x - mref);
+                    const float eb = has_b ? ex2(v[j].y - mref) : 0.f;
+                    v[j] = make_float2(ea, eb);
+                    if (j & 1) { za1 += ea; zb1 += eb; } else { za += ea; zb += eb; }
+                }
+                za += za1;
+                zb += zb1;
+                mall = mt;
+                zall = za + zb;
+                cta_ms(mall, zall, red, lane, warp);
+                // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64)
+                // g_q = log2 of this pair's largest unnormalised weight: Sref c2 + m_q
+                const double gq = mall == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)mall;
+                if (NP > 1) {
+                    const int slot = (it & 1) * MAXNP;
+                    const unsigned long long gb = (unsigned long long)__double_as_longlong(gq);
+                    if (t < NP)
+                        st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t,
+                                      make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)),
+                                                  zall, 0.f));
+                    cluster_sync_all();
+                    double g[MAXNP];
+                    G = -INFINITY;
+                    for (int r = 0; r < NP; ++r) {
+                        const float4 e = xch[slot + r];
+                        g[r] = __longlong_as_double(
+                            (long long)(((unsigned long long)__float_as_uint(e.y) << 32) | __float_as_uint(e.x)));
+                        G = fmax(G, g[r]);
+                    }
+                    Z = 0.0;
+                    for (int r = 0; r < NP; ++r)
+                        if (g[r] != -INFINITY) Z += (double)xch[slot + r].z * (double)ex2((float)(g[r] - G));
+                } else {
+                    G = gq;
+                    Z = (double)zall;
+                }
+                const float dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
+                const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f : ex2(mt - mall + dq) / (float)Z;
+                rsumA = fmaf(za, f, rsumA);
+                rsumB = fmaf(zb, f, rsumB);
+#pragma unroll
+                for (int j = 0; j < 64; ++j) v[j] = make_float2(v[j].x * f, v[j].y * f);
+                if (q == 0 && t == 0) {
+                    const double lse = 0.69314718055994530942 * (G + (double)log2f((float)Z)) -
+                                       (emin + a.ynorm[i]) * a.inv_2s2;
+                    ll_acc += lse;
+                    if (a.llobs) a.llobs[i] = lse;
+                }
+            } else if (pass == 2) {
+                // each thread rewrites the row elements it read in pass 1
+#pragma unroll
+                for (int k = 0; k < 64; ++k) W[swz(l, 2 * k + h)] = v[k];
+                __syncthreads();
+            } else {
+                // v[m] = Z_{i,q}[k1 = 2m + h][l]
+                if (h == 0) {
+                    cu.x += v[0].x;
+                    cu.y += v[0].y;
+                }
+                // U_q[2m+h][l] += Yhat conj(Z) (l < 65);  V_q[-(2m+h)][128-l] += Yhat[-(2m+h)][128-l] Z[2m+h][l]
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    float ys[16], ac[16];
+                    tmem_ld16x2(ty + 16 * ch, ys, tacc + 16 * ch, ac);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int m = ch * 8 + e;
+                        const float2 z = v[m];
+                        const float zy = su * z.y;
+                        ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
+                        ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
+                        if (both) {
+                            zc[(l >> 6) * LL + 2 * m + h] = z;
+                            yc[(l >> 6) * LL + 2 * m + h] = make_float2(ys[2 * e], ys[2 * e + 1]);
+                        }
+                    }
+                    tc::tmem_st16(tacc + 16 * ch, ac);
+                }
+                tc::tmem_wait_st();
+            }
         }
-        tc::tmem_wait_st();
     }
     __syncthreads();
     if (it > 0) vex_update();
