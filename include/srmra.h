@@ -51,7 +51,7 @@ extern "C" {
 #define SRMRA_ERR_CUDA (-3)
 #define SRMRA_ERR_NCCL (-4)
 #define SRMRA_ERR_OOM (-5)
-#define SRMRA_ERR_STATE (-6)       /* call on a failed context                                        */
+#define SRMRA_ERR_STATE (-6)       /* call on a failed context, or em_iter after a rejected srmra_load */
 #define SRMRA_ERR_NUMERIC (-7)     /* non-finite log-likelihood or estimate detected by finalize      */
 
 /* E-step / M-step implementation ("path") */
@@ -97,7 +97,9 @@ SRMRA_API int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32
                const srmra_options* opt);
 
 /* Replace the observations (same n_local and shape) and theta with new host data, reusing the
- * context's device memory; resets the iteration counter and the trace. */
+ * context's device memory; resets the iteration counter and the trace.  y is validated on the device
+ * (finite): a rejected y returns INVALID_ARG and leaves the context requiring a successful srmra_load
+ * before the next srmra_em_iter (which returns STATE until then). */
 SRMRA_API int srmra_load(srmra_ctx* ctx, const float* y, const float* x0, const double* rho1_0,
                const double* rho2_0);
 

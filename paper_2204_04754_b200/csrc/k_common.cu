@@ -15,7 +15,9 @@ namespace srmra {
 
 // ---------------------------------------------------------------- a0: ||y_i||^2 (float64)
 // One warp per observation; float4 loads (Ll^2 is a multiple of 4 for every supported shape).
-__global__ void k_ynorm(const float* __restrict__ y, int64_t n, int Ll2, double* __restrict__ out) {
+// ||y_i||^2 in float64; it is non-finite exactly when some y_i[n] is, which sets bit 1 of *flag (the
+// init-time validation of y runs here instead of a serial host scan)
+__global__ void k_ynorm(const float* __restrict__ y, int64_t n, int Ll2, double* __restrict__ out, int* flag) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= n) return;
@@ -31,14 +33,17 @@ __global__ void k_ynorm(const float* __restrict__ y, int64_t n, int Ll2, double*
         for (int k = lane; k < Ll2; k += 32) acc += (double)yi[k] * yi[k];
     }
     acc = warp_sum(acc);
-    if (lane == 0) out[i] = acc;
+    if (lane == 0) {
+        out[i] = acc;
+        if (!isfinite(acc)) atomicOr(flag, 2);
+    }
 }
 
 cudaError_t launch_init_obs(srmra_ctx* c) {
     if (c->n_local > 0) {
         const int wpb = 8;
         int64_t blocks = (c->n_local + wpb - 1) / wpb;
-        k_ynorm<<<(unsigned)blocks, wpb * 32, 0, c->stream>>>(c->d_y, c->n_local, c->Ll2, c->d_ynorm);
+        k_ynorm<<<(unsigned)blocks, wpb * 32, 0, c->stream>>>(c->d_y, c->n_local, c->Ll2, c->d_ynorm, c->d_flag);
     }
     return cudaGetLastError();
 }

@@ -137,8 +137,16 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
         CK(launch_fft_init(c));
         CK(launch_fft_tail(c, TAIL_PREP, 0, 0));  // Xhat and logit bias of theta_0
     }
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
     c->iters_done = 0;
+    if (flag & 2) {  // k_ynorm found a non-finite observation value
+        c->needs_load = true;
+        CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
+    }
+    c->needs_load = false;
     return SRMRA_OK;
 }
 
@@ -242,8 +250,6 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     if (opt.proj_every < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "proj_every < 0");
     if (opt.trace_cap < 1) opt.trace_cap = 4096;
     if (!all_finite_f(x0, (size_t)L_high * L_high)) return fail(c, SRMRA_ERR_INVALID_ARG, "x0 not finite");
-    if (n_local > 0 && !all_finite_f(y, (size_t)n_local * L_low * L_low))
-        return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
     std::vector<double> r1, r2;
     if (check_rho(rho1_0, L_high, r1) || check_rho(rho2_0, L_high, r2))
         return fail(c, SRMRA_ERR_INVALID_ARG, "rho must be >= 0, finite and sum to 1 (within 1e-6)");
@@ -375,7 +381,6 @@ int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1
     if (c->failed) return SRMRA_ERR_STATE;
     if (!x0 || !rho1_0 || !rho2_0 || (c->n_local > 0 && !y)) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
     if (!all_finite_f(x0, (size_t)c->L2)) return fail(c, SRMRA_ERR_INVALID_ARG, "x0 not finite");
-    if (c->n_local > 0 && !all_finite_f(y, (size_t)c->n_local * c->Ll2)) return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
     std::vector<double> r1, r2;
     if (check_rho(rho1_0, c->L, r1) || check_rho(rho2_0, c->L, r2))
         return fail(c, SRMRA_ERR_INVALID_ARG, "rho must be >= 0, finite and sum to 1 (within 1e-6)");
@@ -386,6 +391,7 @@ int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
+    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "the last srmra_load was rejected; load valid data first");
     // FFT path on one rank: replay a captured CUDA graph of one iteration (E/M kernel + cooperative
     // tail); the tail takes t and the projection flag from the device counter.  With profiling on, the
     // graph variant carries 4 event-record nodes that are re-pointed to fresh pool events per replay.

@@ -42,6 +42,7 @@ struct srmra_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool failed = false;
+    bool needs_load = false;  // the last srmra_load was rejected (non-finite y found on the device)
     std::string err;
 
     // observation-side buffers (this rank's shard)

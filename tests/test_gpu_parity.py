@@ -242,9 +242,21 @@ def test_invalid_arguments(srm):
         with pytest.raises(srm.SrmraError) as ei:
             srm.Context(**a)
         assert ei.value.code == srm.SRMRA_ERR_INVALID_ARG
-    y = p.y.copy(); y[0, 0, 0] = np.inf
-    with pytest.raises(srm.SrmraError):
+    y = p.y.copy(); y[-1, 1, 0] = np.inf   # validated on the device (k_ynorm)
+    with pytest.raises(srm.SrmraError) as ei:
         srm.Context(**dict(args, y=y))
+    assert ei.value.code == srm.SRMRA_ERR_INVALID_ARG
+    # a rejected load leaves the context needing a valid load; a valid one restores it
+    with srm.Context(**args) as ctx:
+        with pytest.raises(srm.SrmraError) as ei:
+            ctx.load(y, p.x0, p.rho1_0, p.rho2_0)
+        assert ei.value.code == srm.SRMRA_ERR_INVALID_ARG
+        with pytest.raises(srm.SrmraError) as ei:
+            ctx.em_iter(1)
+        assert ei.value.code == srm.SRMRA_ERR_STATE
+        ctx.load(p.y, p.x0, p.rho1_0, p.rho2_0)
+        ctx.em_iter(1)
+        assert np.all(np.isfinite(ctx.get_estimate()[0]))
 
 
 def test_torch_stream(srm):
