@@ -39,11 +39,12 @@ __global__ void k_ynorm(const float* __restrict__ y, int64_t n, int Ll2, double*
     }
 }
 
-cudaError_t launch_init_obs(srmra_ctx* c) {
-    if (c->n_local > 0) {
+cudaError_t launch_init_obs(srmra_ctx* c, int64_t first, int64_t count) {
+    if (count > 0) {
         const int wpb = 8;
-        int64_t blocks = (c->n_local + wpb - 1) / wpb;
-        k_ynorm<<<(unsigned)blocks, wpb * 32, 0, c->stream>>>(c->d_y, c->n_local, c->Ll2, c->d_ynorm, c->d_flag);
+        int64_t blocks = (count + wpb - 1) / wpb;
+        k_ynorm<<<(unsigned)blocks, wpb * 32, 0, c->stream>>>(c->d_y + first * c->Ll2, count, c->Ll2,
+                                                              c->d_ynorm + first, c->d_flag);
     }
     return cudaGetLastError();
 }

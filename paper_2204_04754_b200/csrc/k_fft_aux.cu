@@ -52,14 +52,15 @@ static size_t dft_smem(int Ll) {
     return sizeof(double) * 2 * Ll + sizeof(double2) * Ll * (Ll / 2 + 1) + sizeof(float) * Ll * Ll;
 }
 
-cudaError_t launch_fft_init(srmra_ctx* c) {
-    if (c->n_local == 0) return cudaSuccess;
+cudaError_t launch_fft_init(srmra_ctx* c, int64_t first, int64_t count) {
+    if (count <= 0) return cudaSuccess;
     const size_t sm = dft_smem(c->Ll);
     cudaError_t e = cudaFuncSetAttribute(k_fft_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    const int64_t grid = c->n_local < 65536 ? c->n_local : 65536;
-    k_fft_init<<<(unsigned)grid, 256, sm, c->stream>>>(c->d_y, c->n_local, c->Ll, yrow_of(c->Ll), ystride_of(c->Ll),
-                                                         c->d_tw, c->d_yhat, c->d_ysum);
+    const int64_t grid = count < 65536 ? count : 65536;
+    const int ys = ystride_of(c->Ll);
+    k_fft_init<<<(unsigned)grid, 256, sm, c->stream>>>(c->d_y + first * c->Ll2, count, c->Ll, yrow_of(c->Ll), ys,
+                                                         c->d_tw, c->d_yhat + first * ys, c->d_ysum + first);
     return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 // sequence (prep -> E/M path kernel -> pack -> [NCCL all-reduce] -> finalize/projection) and
 // the NCCL communicator (libnccl.so.2 is dlopen'ed on first use, so single-GPU use has no NCCL
 // dependency and, inside a PyTorch process, the already-loaded NCCL is reused).
+#include <algorithm>
 #include <dlfcn.h>
 #include <math.h>
 #include <nccl.h>
@@ -121,20 +122,36 @@ int choose_path(int requested, int L, int Ll, int K) {
 int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<double>& r1,
            const std::vector<double>& r2) {
     const size_t ny = (size_t)c->n_local * c->Ll2;
-    // pinned caller buffers give an asynchronous DMA; pageable ones are staged by the driver
-    if (ny) CK(cudaMemcpyAsync(c->d_y, y, sizeof(float) * ny, cudaMemcpyHostToDevice, c->stream));
+    // pinned caller buffers give an asynchronous DMA; pageable ones are staged by the driver.  FFT path:
+    // y goes over in ~4 MB chunks on the copy stream and each chunk's init kernels (||y_i||^2, Yhat_i)
+    // run on the context stream as soon as it has landed, overlapping the transfer
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));  // before k_ynorm may set bit 1
+    const bool chunked = c->path == SRMRA_PATH_FFT && c->copy_stream && ny;
+    if (chunked) {
+        const int64_t per = std::max<int64_t>(1, (int64_t)(4 << 20) / (int64_t)(sizeof(float) * c->Ll2));
+        for (int64_t o = 0; o < c->n_local; o += per) {
+            const int64_t m = std::min<int64_t>(per, c->n_local - o);
+            CK(cudaMemcpyAsync(c->d_y + o * c->Ll2, y + o * c->Ll2, sizeof(float) * m * c->Ll2,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+            CK(cudaEventRecord(c->copy_event, c->copy_stream));
+            CK(cudaStreamWaitEvent(c->stream, c->copy_event, 0));  // binds to this record
+            CK(launch_init_obs(c, o, m));
+            CK(launch_fft_init(c, o, m));
+        }
+    } else if (ny) {
+        CK(cudaMemcpyAsync(c->d_y, y, sizeof(float) * ny, cudaMemcpyHostToDevice, c->stream));
+    }
     std::vector<double> x64(c->L2), rho(2 * c->L);
     for (int k = 0; k < c->L2; ++k) x64[k] = (double)x0[k];
     for (int k = 0; k < c->L; ++k) { rho[k] = r1[k]; rho[c->L + k] = r2[k]; }
     CK(cudaMemcpyAsync(c->d_x64, x64.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_x32, x0, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
     CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
-    CK(launch_init_obs(c));
+    if (!chunked) CK(launch_init_obs(c, 0, c->n_local));
     if (c->path == SRMRA_PATH_GEMM) CK(launch_gemm_init(c));
     if (c->path == SRMRA_PATH_FFT) {
-        CK(launch_fft_init(c));
+        if (!chunked) CK(launch_fft_init(c, 0, c->n_local));
         CK(launch_fft_tail(c, TAIL_PREP, 0, 0));  // Xhat and logit bias of theta_0
     }
     int flag = 0;
@@ -300,6 +317,10 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     } else {
         CKI(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
+    }
+    if (path == SRMRA_PATH_FFT) {
+        CKI(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CKI(cudaEventCreateWithFlags(&c->copy_event, cudaEventDisableTiming));
     }
     const size_t ny = (size_t)n_local * c->Ll2;
     CKI(dalloc(&c->d_y, ny));
@@ -621,6 +642,8 @@ void srmra_free(srmra_ctx* c) {
         if (c->prof_ph[k]) cudaEventDestroy(c->prof_ph[k]);
     if (c->d_iter) cudaFree(c->d_iter);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->copy_event) cudaEventDestroy(c->copy_event);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -40,6 +40,8 @@ struct srmra_ctx {
     int device = 0;
     int num_sms = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // H2D of y in chunks, overlapped with the init kernels
+    cudaEvent_t copy_event = nullptr;
     bool own_stream = false;
     bool failed = false;
     bool needs_load = false;  // the last srmra_load was rejected (non-finite y found on the device)
@@ -109,7 +111,7 @@ struct srmra_ctx {
 namespace srmra {
 
 // ---------------------------------------------------------------- launches (k_common.cu)
-cudaError_t launch_init_obs(srmra_ctx* c);      // ||y||^2 (+ Yhat for the fft path)
+cudaError_t launch_init_obs(srmra_ctx* c, int64_t first, int64_t count);  // ||y_i||^2 (+ finiteness flag)
 cudaError_t launch_prep(srmra_ctx* c);          // theta -> IterParams (+ Xhat), zero accumulators
 cudaError_t launch_pack(srmra_ctx* c);          // colsum (+ Bhat) -> packed b | cmass | marg | LL
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
@@ -118,7 +120,7 @@ cudaError_t launch_direct_em(srmra_ctx* c);     // k_direct.cu
 bool direct_supported(int L, int Ll, int K);
 cudaError_t launch_fft_em(srmra_ctx* c);        // k_fft.cu
 bool fft_supported(int L, int Ll, int K);
-cudaError_t launch_fft_init(srmra_ctx* c);
+cudaError_t launch_fft_init(srmra_ctx* c, int64_t first, int64_t count);  // Yhat_i, sum y_i
 // tcgen05 3xTF32 GEMM path (k_gemm.cu)
 bool gemm_supported(int L, int Ll, int K);
 size_t gemm_bytes(const srmra_ctx* c);
