@@ -107,6 +107,30 @@ SRMRA_API int srmra_load(srmra_ctx* ctx, const float* y, const float* x0, const 
  * With world > 1 each iteration performs one NCCL all-reduce of the sufficient statistics. */
 SRMRA_API int srmra_em_iter(srmra_ctx* ctx, int32_t n_iters);
 
+/* Denoiser hook of Algorithm 2: called on the host for every projection
+ * step with the device buffer of the estimate x (float64, [L_high][L_high], modified in place), the
+ * schedule value sigma_t of eq:decaying_function and the context stream (cudaStream_t); work must be
+ * enqueued on that stream.  Return 0 on success (non-zero aborts the run with SRMRA_ERR_NUMERIC). */
+typedef int (*srmra_denoiser_fn)(double* x_dev, int32_t L_high, double sigma_t, void* stream, void* user);
+
+/* Replace the built-in stand-in projection (3x3 circular box filter, clamp to [-1, 1]; north_star)
+ * with `fn` (NULL restores the built-in one).  The context keeps `user` opaque. */
+SRMRA_API int srmra_set_denoiser(srmra_ctx* ctx, srmra_denoiser_fn fn, void* user);
+
+/*
+ * Algorithm 2 (projected EM) run to convergence: up to max_iters EM iterations;
+ * after iteration t the projection D(x, sigma_j) is applied when (t+1) % F == 0 (F = proj_every),
+ * with sigma_j = 2^(-(j-1)/10) for the j-th projection of this run (eq:decaying_function,
+ * PAPER.md:345-349; the built-in stand-in ignores it); the run stops after the first iteration
+ * t >= 1 (t counted within this run) with |LL_t - LL_{t-1}| <= rel_tol |LL_t|, LL_t the
+ * log-likelihood at the input of iteration t (rel_tol <= 0: run max_iters).
+ * FFT path on one rank without a denoiser hook: asynchronous — the convergence test runs on the
+ * device and the remaining enqueued iterations become no-ops; srmra_get_estimate reports the
+ * iterations actually run.  Otherwise the host checks the log-likelihood after every iteration.
+ * Errors: INVALID_ARG (max_iters < 0), STATE, CUDA, NCCL, NUMERIC (denoiser hook failure).
+ */
+SRMRA_API int srmra_run(srmra_ctx* ctx, int32_t max_iters, double rel_tol);
+
 /*
  * Synchronise the stream and copy the current estimate to caller-owned host buffers (any may be
  * NULL): x_out float32 [L_high][L_high], rho1_out / rho2_out float64 [L_high], *loglik_out the

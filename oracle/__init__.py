@@ -118,6 +118,38 @@ def run(y, L_low, K, sigma, x0, rho1_0, rho2_0, iters, proj_every=1, tau=None):
     return x, r1, r2, trace
 
 
+def sigma_schedule(j: int) -> float:
+    """sigma^BM3D of the j-th projection (j = 1, 2, ...): sigma_1 = 1, sigma_j = 2^(-1/10) sigma_{j-1}
+    (eq:decaying_function), evaluated by the recursion as written."""
+    s = 1.0
+    for _ in range(1, j):
+        s *= 2.0 ** (-1.0 / 10.0)
+    return s
+
+
+def run_alg2(y, L_low, K, sigma, x0, rho1_0, rho2_0, max_iters, proj_every=1, rel_tol=0.0, denoiser=None,
+             tau=None):
+    """Algorithm 2 (projected EM): EM steps; after every F-th step (F = proj_every)
+    x <- D(x, sigma_j) with the schedule sigma_j of eq:decaying_function; stop after the first iteration
+    t >= 1 with |LL_t - LL_{t-1}| <= rel_tol |LL_t| (reading R12; rel_tol <= 0: never) or after
+    max_iters.  D is the north_star stand-in (3x3 circular box, clamp) unless `denoiser(x, sigma_j)`
+    is given.  Returns (x, rho1, rho2, [LL_0..], [sigma_1..] of the projections applied)."""
+    x, r1, r2 = _f64(x0), _f64(rho1_0), _f64(rho2_0)
+    trace, sigmas = [], []
+    for t in range(max_iters):
+        proj = proj_every > 0 and (t + 1) % proj_every == 0
+        r = em_iter(y, L_low, K, sigma, x, r1, r2, project=proj and denoiser is None, tau=tau)
+        x, r1, r2 = r.x, r.rho1, r.rho2
+        trace.append(r.loglik)
+        if proj:
+            sigmas.append(sigma_schedule(len(sigmas) + 1))
+            if denoiser is not None:
+                x = _f64(denoiser(x, sigmas[-1]))
+        if rel_tol > 0 and t >= 1 and abs(trace[t] - trace[t - 1]) <= rel_tol * abs(trace[t]):
+            break
+    return x, r1, r2, trace, sigmas
+
+
 def posterior(yi, L_low, K, sigma, x, rho1, rho2):
     """(w [L][L], log-likelihood term) of one observation."""
     lib = _load()

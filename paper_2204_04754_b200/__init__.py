@@ -34,7 +34,7 @@ ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_it
                "srmra_get_loglik_trace", "srmra_get_stats", "srmra_get_obs_loglik", "srmra_local_stats",
                "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
-               "srmra_last_error")
+               "srmra_last_error", "srmra_run", "srmra_set_denoiser")
 
 
 class SrmraError(RuntimeError):
@@ -48,6 +48,10 @@ class srmra_options(ctypes.Structure):
                 ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("trace_cap", ctypes.c_int32)]
 
+
+# int (*)(double* x_dev, int32_t L_high, double sigma_t, void* stream, void* user)
+DENOISER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
+                               ctypes.c_void_p)
 
 _fp = ctypes.POINTER(ctypes.c_float)
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -79,6 +83,8 @@ def _load():
         "srmra_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
         "srmra_free": (None, [_ctxp]),
         "srmra_last_error": (ctypes.c_char_p, [_ctxp]),
+        "srmra_run": (ctypes.c_int, [_ctxp, ctypes.c_int32, ctypes.c_double]),
+        "srmra_set_denoiser": (ctypes.c_int, [_ctxp, DENOISER_FN, ctypes.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -137,6 +143,15 @@ def srmra_load(ctx, y, x0, rho1_0, rho2_0):
 
 def srmra_em_iter(ctx, n_iters: int = 1):
     _check(_lib.srmra_em_iter(ctx, int(n_iters)), ctx)
+
+
+def srmra_run(ctx, max_iters: int, rel_tol: float = 0.0):
+    _check(_lib.srmra_run(ctx, int(max_iters), float(rel_tol)), ctx)
+
+
+def srmra_set_denoiser(ctx, fn):
+    """fn: a DENOISER_FN (keep a reference while it is installed) or None for the built-in stand-in."""
+    _check(_lib.srmra_set_denoiser(ctx, fn if fn is not None else DENOISER_FN(), None), ctx)
 
 
 def srmra_get_estimate(ctx, L_high: int):
@@ -243,6 +258,19 @@ class Context:
 
     def em_iter(self, n_iters=1):
         srmra_em_iter(self.handle, n_iters)
+
+    def run(self, max_iters, rel_tol=0.0):
+        """Algorithm 2 to convergence (srmra_run)."""
+        srmra_run(self.handle, max_iters, rel_tol)
+
+    def set_denoiser(self, fn):
+        """fn(x_dev_ptr: int, L_high: int, sigma_t: float, stream: int) -> int (0 = ok), or None."""
+        if fn is None:
+            self._denoiser = None
+            srmra_set_denoiser(self.handle, None)
+            return
+        self._denoiser = DENOISER_FN(lambda x, L, sig, st, user: int(fn(x, L, sig, st)))
+        srmra_set_denoiser(self.handle, self._denoiser)
 
     def get_estimate(self):
         return srmra_get_estimate(self.handle, self.L_high)

@@ -160,4 +160,13 @@ cudaError_t launch_finalize(srmra_ctx* c, int t, int project) {
     return cudaGetLastError();
 }
 
+// x32 = (float) x64 after a denoiser hook modified x64 (srmra_set_denoiser)
+__global__ void k_x32_from_x64(const double* __restrict__ x64, int n, float* __restrict__ x32) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) x32[p] = (float)x64[p];
+}
+cudaError_t launch_x32_from_x64(srmra_ctx* c) {
+    k_x32_from_x64<<<(c->L2 + 255) / 256, 256, 0, c->stream>>>(c->d_x64, c->L2, c->d_x32);
+    return cudaGetLastError();
+}
+
 }  // namespace srmra

@@ -82,6 +82,7 @@ struct EmArgs {
     double* llpart;         // [gridDim.x] per-CTA log-likelihood partials
     double* llobs;          // [n]
     int tmem_cols;          // TACC: tensor-memory columns allocated per CTA (power of two >= 32)
+    const int* run;         // srmra_run stop flag ([0])
 };
 
 template <int LL>
@@ -189,6 +190,7 @@ template <int LL, bool PAIRS, bool XS, bool TACC>
 __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArgs a) {
     using G = Geo<LL>;
     constexpr int LH = G::LH, WS = G::WS, M = LL - 1;
+    if (*reinterpret_cast<const volatile int*>(a.run)) return;  // converged srmra_run: no-op iteration
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int KK = a.KK, K = a.K, L = a.L;
     const int NP = (KK + 1) / 2;
@@ -651,6 +653,7 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     a.llpart = c->d_llpart;
     a.llobs = c->d_llobs;
     a.tmem_cols = c->fft_tmem_cols;
+    a.run = c->d_run;
     if constexpr (LL >= 32) {
         if (c->fft_tacc) {
             em_kernel<LL, true>(c->KK, c->fft_xs)<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);

@@ -205,12 +205,14 @@ struct Em128Args {
     float2* part;         // [clusters][PB] per-cluster partials (layout of k_fft.cu part_bins)
     double* llpart;       // [clusters]
     double* llobs;        // [n]
+    const int* run;       // srmra_run stop flag ([0])
 };
 
 template <bool PAIRS>
 __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     extern __shared__ __align__(1024) unsigned char sm[];
     float2* W = reinterpret_cast<float2*>(sm + OFF_W);
+    if (*reinterpret_cast<const volatile int*>(a.run)) return;  // converged srmra_run: no-op iteration
     float2* Ys = reinterpret_cast<float2*>(sm + OFF_Y);
     float* pars = reinterpret_cast<float*>(sm + OFF_PAR);
     float2* zc = reinterpret_cast<float2*>(sm + OFF_ZC);
@@ -573,6 +575,7 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.part = c->d_part;
     a.llpart = c->d_llpart;
     a.llobs = c->d_llobs;
+    a.run = c->d_run;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = em128_config(c, attr, c->fft_grid);
     if (c->KK % 2 == 0) return cudaLaunchKernelEx(&cfg, k_fft_em128<true>, a);

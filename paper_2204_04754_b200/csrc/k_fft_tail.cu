@@ -54,6 +54,8 @@ struct TailArgs {
     int nchunk;               // row chunks per class in phase F
     int nchunk_q, wq;         // phase Q: column chunks per class, columns per chunk
     int* iter;                // device iteration counter (t is read here, +1 after finalize) or NULL
+    int* run;                 // srmra_run control: [0] stop flag (set here on convergence), [1] first t of the run
+    const double* rtol;       // convergence tolerance of the run (0: none)
     int proj_every;           // F of Algorithm 2 (project after t when (t+1) % F == 0; 0 = never)
 };
 
@@ -225,6 +227,12 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                     const double ll = a.pack[a.off_ll];
                     if (a.t < a.trace_cap) a.trace[a.t] = ll;
                     bad |= !isfinite(ll);
+                    // Algorithm 2 stopping rule (srmra_run): |LL_t - LL_{t-1}| <= rtol |LL_t| for t >= run start + 1;
+                    // the remaining enqueued iterations of the run become no-ops
+                    const double rt = *a.rtol;
+                    if (rt > 0.0 && a.t - a.run[1] >= 1 && a.t - 1 < a.trace_cap &&
+                        fabs(ll - a.trace[a.t - 1]) <= rt * fabs(ll))
+                        a.run[0] = 1;
                 }
             }
         }
@@ -275,10 +283,8 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                 if (ch == 0) {
                     e2 += v * v;
                     e1 += v;
-                    if (from_tmp) {
-                        a.x64[(size_t)p1 * L + p2] = v;
-                        a.x32[(size_t)p1 * L + p2] = (float)v;
-                    }
+                    if (from_tmp) a.x64[(size_t)p1 * L + p2] = v;
+                    a.x32[(size_t)p1 * L + p2] = (float)v;
                 }
             }
             if (ch == 0) {
@@ -343,6 +349,7 @@ __device__ inline void stamp(const TailArgs& a, int k) {
 
 __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     extern __shared__ double sm[];
+    if (*reinterpret_cast<volatile int*>(a.run)) return;  // a converged srmra_run: nothing left to do
     if (a.iter) {  // graph-replayable: the iteration index and the projection flag come from the device
         a.t = *reinterpret_cast<volatile int*>(a.iter);
         a.project = a.proj_every > 0 && ((a.t + 1) % a.proj_every == 0);
@@ -405,7 +412,9 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     a.t = t;
     a.project = project;
     a.iter = c->d_iter;
-    a.proj_every = c->opt.proj_every;
+    a.run = c->d_run;
+    a.rtol = c->d_rtol;
+    a.proj_every = c->denoiser ? 0 : c->opt.proj_every;  // a denoiser hook replaces the built-in projection
     a.trace_cap = c->opt.trace_cap;
     a.tau = c->tau;
     a.inv_2s2 = c->inv_2s2;

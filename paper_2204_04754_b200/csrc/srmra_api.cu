@@ -148,6 +148,9 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemcpyAsync(c->d_x32, x0, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->d_run, 0, 2 * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->d_rtol, 0, sizeof(double), c->stream));
+    c->n_proj = 0;
     if (!chunked) CK(launch_init_obs(c, 0, c->n_local));
     if (c->path == SRMRA_PATH_GEMM) CK(launch_gemm_init(c));
     if (c->path == SRMRA_PATH_FFT) {
@@ -212,6 +215,150 @@ int local_estep_mstep(srmra_ctx* c) {
         CK(launch_pack(c));
     } else {
         return fail(c, SRMRA_ERR_UNSUPPORTED, "path not available");
+    }
+    return SRMRA_OK;
+}
+
+
+// Run control of the FFT graph path: stop flag, first iteration of the run, tolerance (0 = none).
+int set_run_control(srmra_ctx* c, double rel_tol) {
+    c->h_run[0] = 0;
+    c->h_run[1] = c->iters_done;
+    c->h_rtol = rel_tol > 0 ? rel_tol : 0.0;
+    // pageable sources: the copies are staged before the calls return
+    CK(cudaMemcpyAsync(c->d_run, c->h_run, 2 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_rtol, &c->h_rtol, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    return SRMRA_OK;
+}
+
+// After a denoiser hook replaced x64: the float32 copy and (FFT path) the next iteration's spectra
+int refresh_after_denoise(srmra_ctx* c) {
+    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_tail(c, TAIL_PREP, c->iters_done, 0));  // also writes x32
+    else CK(launch_x32_from_x64(c));
+    return SRMRA_OK;
+}
+
+// n_iters EM iterations of Algorithm 2 (srmra_em_iter: rel_tol = 0; srmra_run: the stopping rule)
+int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
+    const bool device_loop = c->path == SRMRA_PATH_FFT && c->opt.world == 1 && !c->denoiser;
+    int rc;
+    if ((rc = set_run_control(c, device_loop ? rel_tol : 0.0)) != SRMRA_OK) return rc;
+    // FFT path on one rank: replay a captured CUDA graph of one iteration (E/M kernel + cooperative
+    // tail); the tail takes t and the projection flag from the device counter.  With profiling on, the
+    // graph variant carries 4 event-record nodes that are re-pointed to fresh pool events per replay.
+    if (device_loop && !c->graph_failed && n_iters > 0) {
+        cudaGraphExec_t* exec = c->prof ? &c->graph_prof : &c->graph;
+        if (!*exec) {
+            cudaGraph_t g = nullptr;
+            cudaEvent_t ph[4] = {nullptr, nullptr, nullptr, nullptr};
+            bool ok = true;
+            if (c->prof)
+                for (int k = 0; k < 4 && ok; ++k) ok = cudaEventCreate(&ph[k]) == cudaSuccess;
+            ok = ok && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                bool l = true;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[0], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[1], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                l = l && launch_fft_em(c) == cudaSuccess;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[2], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                l = l && launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP, 0, 0) == cudaSuccess;
+                if (c->prof) l = l && cudaEventRecordWithFlags(ph[3], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && l;
+            }
+            if (ok && c->prof) {  // find the event-record nodes by their placeholder events
+                size_t nn = 0;
+                ok = cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess;
+                std::vector<cudaGraphNode_t> nodes(nn);
+                ok = ok && cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess;
+                for (size_t k = 0; ok && k < nn; ++k) {
+                    cudaGraphNodeType ty;
+                    if (cudaGraphNodeGetType(nodes[k], &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord) continue;
+                    cudaEvent_t ev;
+                    if (cudaGraphEventRecordNodeGetEvent(nodes[k], &ev) != cudaSuccess) continue;
+                    for (int j = 0; j < 4; ++j)
+                        if (ev == ph[j]) c->prof_nodes[j] = nodes[k];
+                }
+                for (int j = 0; j < 4; ++j) ok = ok && c->prof_nodes[j] != nullptr;
+            }
+            if (ok) ok = cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
+            // the profiling variant keeps its graph: exec-node updates refer to the graph's node handles
+            if (g && ok && c->prof) c->graph_prof_src = g;
+            else if (g) cudaGraphDestroy(g);
+            if (!ok) {
+                cudaGetLastError();  // clear the capture error; stream launches are used instead
+                *exec = nullptr;
+                c->graph_failed = true;
+            }
+            // placeholders must outlive the exec (destroying them invalidates its event-record nodes)
+            for (int k = 0; k < 4; ++k) {
+                if (ok && c->prof) c->prof_ph[k] = ph[k];
+                else if (ph[k]) cudaEventDestroy(ph[k]);
+            }
+        }
+        if (*exec) {
+            for (int it = 0; it < n_iters; ++it) {
+                if (c->prof) {
+                    for (int j = 0; j < 4; ++j) {
+                        cudaEvent_t e = c->prof_event();
+                        if (!e) return fail(c, SRMRA_ERR_CUDA, "cudaEventCreate failed");
+                        CK(cudaGraphExecEventRecordNodeSetEvent(*exec, c->prof_nodes[j], e));
+                    }
+                }
+                CK(cudaGraphLaunch(*exec, c->stream));
+                c->iters_done++;
+            }
+            return SRMRA_OK;
+        }
+    }
+    const int t0 = c->iters_done;
+    for (int it = 0; it < n_iters; ++it) {
+        const int t = c->iters_done;
+        if ((rc = record(c)) != SRMRA_OK) return rc;
+        if ((rc = local_estep_mstep(c)) != SRMRA_OK) return rc;
+        const int F = c->opt.proj_every;
+        const bool proj_step = F > 0 && ((t + 1) % F == 0);
+        const int project = proj_step && !c->denoiser;  // the built-in stand-in projection
+        if (c->path == SRMRA_PATH_FFT) {
+            // reduce -> [all-reduce] -> fold / update -> projection / next prep: one cooperative kernel
+            // (two when the NCCL all-reduce has to sit between the reduce and the fold)
+            const int rest = TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP;
+            if (c->opt.world > 1) {
+                CK(launch_fft_tail(c, TAIL_REDUCE, t, project));
+                if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
+                CK(launch_fft_tail(c, rest, t, project));
+            } else {
+                CK(launch_fft_tail(c, TAIL_REDUCE | rest, t, project));
+            }
+        } else {
+            if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
+            CK(launch_finalize(c, t, project));
+        }
+        if ((rc = record(c)) != SRMRA_OK) return rc;
+        c->iters_done++;
+        if (proj_step && c->denoiser) {  // Algorithm 2: x <- D(x, sigma_j), sigma_j = 2^(-(j-1)/10)
+            const double sig = pow(2.0, -(double)(c->n_proj++) / 10.0);
+            if (c->denoiser(c->d_x64, c->L, sig, (void*)c->stream, c->denoiser_user) != 0)
+                return fail(c, SRMRA_ERR_NUMERIC, "denoiser hook failed");
+            if ((rc = refresh_after_denoise(c)) != SRMRA_OK) return rc;
+        }
+        if (rel_tol > 0 && t - t0 >= 1 && t < c->opt.trace_cap) {  // host-side stopping rule
+            double ll[2];
+            CK(cudaMemcpyAsync(ll, c->d_trace + (t - 1), 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            if (fabs(ll[1] - ll[0]) <= rel_tol * fabs(ll[1])) break;
+        }
+    }
+    return SRMRA_OK;
+}
+
+// Iterations actually run: the FFT tail's device counter is authoritative (a converged srmra_run
+// turns the remaining enqueued iterations into no-ops); other paths count on the host.
+int sync_iters(srmra_ctx* c) {
+    if (c->path == SRMRA_PATH_FFT) {
+        int t = 0;
+        CK(cudaMemcpyAsync(&t, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->iters_done = t;
     }
     return SRMRA_OK;
 }
@@ -340,6 +487,10 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->d_counter, 1));
     CKI(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
     CKI(dalloc(&c->d_iter, 1));
+    CKI(dalloc(&c->d_run, 2));
+    CKI(cudaMemset(c->d_run, 0, 2 * sizeof(int)));
+    CKI(dalloc(&c->d_rtol, 1));
+    CKI(cudaMemset(c->d_rtol, 0, sizeof(double)));
     if (getenv("SRMRA_TAIL_STAMPS")) {
         CKI(dalloc(&c->d_stamps, 16));
         CKI(cudaMemset(c->d_stamps, 0, 16 * sizeof(unsigned long long)));
@@ -408,103 +559,31 @@ int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1
     return upload(c, y, x0, r1, r2);
 }
 
+
 int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
     if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "the last srmra_load was rejected; load valid data first");
-    // FFT path on one rank: replay a captured CUDA graph of one iteration (E/M kernel + cooperative
-    // tail); the tail takes t and the projection flag from the device counter.  With profiling on, the
-    // graph variant carries 4 event-record nodes that are re-pointed to fresh pool events per replay.
-    if (c->path == SRMRA_PATH_FFT && c->opt.world == 1 && !c->graph_failed && n_iters > 0) {
-        cudaGraphExec_t* exec = c->prof ? &c->graph_prof : &c->graph;
-        if (!*exec) {
-            cudaGraph_t g = nullptr;
-            cudaEvent_t ph[4] = {nullptr, nullptr, nullptr, nullptr};
-            bool ok = true;
-            if (c->prof)
-                for (int k = 0; k < 4 && ok; ++k) ok = cudaEventCreate(&ph[k]) == cudaSuccess;
-            ok = ok && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-            if (ok) {
-                bool l = true;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[0], c->stream, cudaEventRecordExternal) == cudaSuccess;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[1], c->stream, cudaEventRecordExternal) == cudaSuccess;
-                l = l && launch_fft_em(c) == cudaSuccess;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[2], c->stream, cudaEventRecordExternal) == cudaSuccess;
-                l = l && launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP, 0, 0) == cudaSuccess;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[3], c->stream, cudaEventRecordExternal) == cudaSuccess;
-                ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && l;
-            }
-            if (ok && c->prof) {  // find the event-record nodes by their placeholder events
-                size_t nn = 0;
-                ok = cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess;
-                std::vector<cudaGraphNode_t> nodes(nn);
-                ok = ok && cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess;
-                for (size_t k = 0; ok && k < nn; ++k) {
-                    cudaGraphNodeType ty;
-                    if (cudaGraphNodeGetType(nodes[k], &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord) continue;
-                    cudaEvent_t ev;
-                    if (cudaGraphEventRecordNodeGetEvent(nodes[k], &ev) != cudaSuccess) continue;
-                    for (int j = 0; j < 4; ++j)
-                        if (ev == ph[j]) c->prof_nodes[j] = nodes[k];
-                }
-                for (int j = 0; j < 4; ++j) ok = ok && c->prof_nodes[j] != nullptr;
-            }
-            if (ok) ok = cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
-            // the profiling variant keeps its graph: exec-node updates refer to the graph's node handles
-            if (g && ok && c->prof) c->graph_prof_src = g;
-            else if (g) cudaGraphDestroy(g);
-            if (!ok) {
-                cudaGetLastError();  // clear the capture error; stream launches are used instead
-                *exec = nullptr;
-                c->graph_failed = true;
-            }
-            // placeholders must outlive the exec (destroying them invalidates its event-record nodes)
-            for (int k = 0; k < 4; ++k) {
-                if (ok && c->prof) c->prof_ph[k] = ph[k];
-                else if (ph[k]) cudaEventDestroy(ph[k]);
-            }
-        }
-        if (*exec) {
-            for (int it = 0; it < n_iters; ++it) {
-                if (c->prof) {
-                    for (int j = 0; j < 4; ++j) {
-                        cudaEvent_t e = c->prof_event();
-                        if (!e) return fail(c, SRMRA_ERR_CUDA, "cudaEventCreate failed");
-                        CK(cudaGraphExecEventRecordNodeSetEvent(*exec, c->prof_nodes[j], e));
-                    }
-                }
-                CK(cudaGraphLaunch(*exec, c->stream));
-                c->iters_done++;
-            }
-            return SRMRA_OK;
-        }
-    }
-    for (int it = 0; it < n_iters; ++it) {
-        const int t = c->iters_done;
-        int rc;
-        if ((rc = record(c)) != SRMRA_OK) return rc;
-        if ((rc = local_estep_mstep(c)) != SRMRA_OK) return rc;
-        const int F = c->opt.proj_every;
-        const int project = F > 0 && ((t + 1) % F == 0);
-        if (c->path == SRMRA_PATH_FFT) {
-            // reduce -> [all-reduce] -> fold -> finalize -> projection -> next prep: one cooperative kernel
-            // (two when the NCCL all-reduce has to sit between the reduce and the fold)
-            const int rest = TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP;
-            if (c->opt.world > 1) {
-                CK(launch_fft_tail(c, TAIL_REDUCE, t, project));
-                if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
-                CK(launch_fft_tail(c, rest, t, project));
-            } else {
-                CK(launch_fft_tail(c, TAIL_REDUCE | rest, t, project));
-            }
-        } else {
-            if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
-            CK(launch_finalize(c, t, project));
-        }
-        if ((rc = record(c)) != SRMRA_OK) return rc;
-        c->iters_done++;
-    }
+    return iterate(c, n_iters, 0.0);
+}
+
+int srmra_run(srmra_ctx* c, int32_t max_iters, double rel_tol) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (max_iters < 0 || !(rel_tol == rel_tol)) return fail(c, SRMRA_ERR_INVALID_ARG, "max_iters < 0 or rel_tol NaN");
+    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "the last srmra_load was rejected; load valid data first");
+    int rc;
+    if ((rc = sync_iters(c)) != SRMRA_OK) return rc;  // the run's first iteration index
+    c->n_proj = 0;
+    return iterate(c, max_iters, rel_tol);
+}
+
+int srmra_set_denoiser(srmra_ctx* c, srmra_denoiser_fn fn, void* user) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    c->denoiser = fn;
+    c->denoiser_user = user;
     return SRMRA_OK;
 }
 
@@ -546,6 +625,8 @@ int srmra_get_estimate(srmra_ctx* c, float* x_out, double* rho1_out, double* rho
     if (rho2_out) CK(cudaMemcpyAsync(rho2_out, c->d_rho + c->L, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
     double ll = NAN;
     int flag = 0;
+    int rc;
+    if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
     const int t = c->iters_done;
     if (t > 0 && t <= c->opt.trace_cap)
         CK(cudaMemcpyAsync(&ll, c->d_trace + (t - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -560,6 +641,8 @@ int srmra_get_estimate(srmra_ctx* c, float* x_out, double* rho1_out, double* rho
 int srmra_get_loglik_trace(srmra_ctx* c, double* out, int32_t cap, int32_t* n) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
+    int rc;
+    if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
     int m = c->iters_done < c->opt.trace_cap ? c->iters_done : c->opt.trace_cap;
     if (m > cap) m = cap;
     if (m > 0 && out) CK(cudaMemcpyAsync(out, c->d_trace, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
@@ -641,6 +724,8 @@ void srmra_free(srmra_ctx* c) {
     for (int k = 0; k < 4; ++k)
         if (c->prof_ph[k]) cudaEventDestroy(c->prof_ph[k]);
     if (c->d_iter) cudaFree(c->d_iter);
+    if (c->d_run) cudaFree(c->d_run);
+    if (c->d_rtol) cudaFree(c->d_rtol);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->copy_event) cudaEventDestroy(c->copy_event);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);

@@ -79,6 +79,13 @@ struct srmra_ctx {
     int* d_flag = nullptr;      // [1] numeric error flag
     unsigned* d_counter = nullptr;  // [1] grid "last block" counter of the fused fold + finalize
     int* d_iter = nullptr;          // [1] device iteration counter (FFT tail reads t from it)
+    int* d_run = nullptr;           // [2] run control of srmra_run: stop flag, first iteration of the run
+    double* d_rtol = nullptr;       // [1] convergence tolerance of the current run (0: none)
+    srmra_denoiser_fn denoiser = nullptr;  // Algorithm 2 denoiser hook (NULL: built-in stand-in)
+    void* denoiser_user = nullptr;
+    int n_proj = 0;                 // projections applied in the current run (sigma schedule index)
+    int h_run[2] = {0, 0};          // host staging of d_run / d_rtol
+    double h_rtol = 0.0;
     cudaGraphExec_t graph = nullptr;  // captured FFT iteration (E/M kernel + tail), world == 1
     cudaGraphExec_t graph_prof = nullptr;  // same with 4 event-record nodes (profiling quadruple)
     cudaGraphNode_t prof_nodes[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -115,6 +122,7 @@ cudaError_t launch_init_obs(srmra_ctx* c, int64_t first, int64_t count);  // ||y
 cudaError_t launch_prep(srmra_ctx* c);          // theta -> IterParams (+ Xhat), zero accumulators
 cudaError_t launch_pack(srmra_ctx* c);          // colsum (+ Bhat) -> packed b | cmass | marg | LL
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
+cudaError_t launch_x32_from_x64(srmra_ctx* c);   // after a denoiser hook changed x
 // ---------------------------------------------------------------- path kernels
 cudaError_t launch_direct_em(srmra_ctx* c);     // k_direct.cu
 bool direct_supported(int L, int Ll, int K);

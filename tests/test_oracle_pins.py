@@ -366,3 +366,40 @@ def test_unobserved_class_keeps_previous_value(oracle_mod):
     assert np.all(r.A[odd] == 0)
     np.testing.assert_array_equal(r.x[odd], x[odd])
     assert np.all(r.A[::2, ::2] > 0)
+
+
+# ---------------------------------------------------------------- NEXT-1: Algorithm 2 driver
+def test_sigma_schedule_closed_form(oracle_mod):
+    """eq:decaying_function (PAPER.md:345-349): sigma_1 = 1, sigma_j = 2^(-1/10) sigma_{j-1}, i.e. the
+    closed form 2^(-(j-1)/10); sigma halves every 10 projections."""
+    for j in range(1, 40):
+        assert abs(oracle_mod.sigma_schedule(j) - 2.0 ** (-(j - 1) / 10.0)) <= 1e-14
+    assert abs(oracle_mod.sigma_schedule(11) - 0.5) <= 1e-14
+
+
+def test_alg2_stopping_rule_and_identity_denoiser(oracle_mod):
+    import synth
+    p = synth.make_random(4, 2, 23, 0.5, 5)
+    args = (p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0)
+    # a huge tolerance stops after the first checkable iteration (t = 1): two LL values recorded
+    *_, tr, _ = oracle_mod.run_alg2(*args, 10, proj_every=1, rel_tol=1e30)
+    assert len(tr) == 2
+    # no tolerance: max_iters iterations, identical to run()
+    x, r1, r2, tr, sig = oracle_mod.run_alg2(*args, 5, proj_every=2)
+    xr, rr1, rr2, trr = oracle_mod.run(*args, 5, proj_every=2)
+    np.testing.assert_array_equal(x, xr)
+    np.testing.assert_array_equal(tr, trr)
+    assert len(sig) == 2
+    # the identity denoiser makes Algorithm 2 plain EM (PAPER.md:226-268 without the projection step)
+    xi, *_, tri, sigi = oracle_mod.run_alg2(*args, 5, proj_every=2, denoiser=lambda v, s: v)
+    x0, *_, tr0 = oracle_mod.run(*args, 5, proj_every=0)
+    np.testing.assert_array_equal(xi, x0)
+    np.testing.assert_array_equal(tri, tr0)
+    assert sigi == [1.0, 2.0 ** -0.1]
+    # the stopping point: the first t >= 1 with |LL_t - LL_{t-1}| <= tol |LL_t|
+    *_, full, _ = oracle_mod.run_alg2(*args, 12, proj_every=0)
+    d = [abs(full[t] - full[t - 1]) / abs(full[t]) for t in range(1, len(full))]
+    tol = sorted(d)[len(d) // 2]
+    t_star = 1 + next(k for k, v in enumerate(d) if v <= tol)
+    *_, trs, _ = oracle_mod.run_alg2(*args, 12, proj_every=0, rel_tol=tol)
+    assert len(trs) == t_star + 1
