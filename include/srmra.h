@@ -131,6 +131,15 @@ SRMRA_API int srmra_set_denoiser(srmra_ctx* ctx, srmra_denoiser_fn fn, void* use
  */
 SRMRA_API int srmra_run(srmra_ctx* ctx, int32_t max_iters, double rel_tol);
 
+/* Evaluation (NEXT-4): error(x_hat) = min_s ||R_s x_hat - x_true||_F / ||x_true||_F over
+ * all L_high^2 circular shifts s, for the context's current estimate x_hat (float64), with
+ * (R_s z)[p] = z[(p - s) mod L_high] (Eq. (2) sign).  x_true: host float32 [L_high][L_high] (copied,
+ * must be finite and non-zero); *err_out the error, (*s1_out, *s2_out) the minimising shift (ties:
+ * the smallest s1 L_high + s2).  Any output may be NULL.  Synchronises.  The correlation over all
+ * shifts runs on the device in float64 (L_high^4 products). */
+SRMRA_API int srmra_relative_error(srmra_ctx* ctx, const float* x_true, double* err_out, int32_t* s1_out,
+                                   int32_t* s2_out);
+
 /*
  * Synchronise the stream and copy the current estimate to caller-owned host buffers (any may be
  * NULL): x_out float32 [L_high][L_high], rho1_out / rho2_out float64 [L_high], *loglik_out the

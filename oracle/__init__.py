@@ -150,6 +150,22 @@ def run_alg2(y, L_low, K, sigma, x0, rho1_0, rho2_0, max_iters, proj_every=1, re
     return x, r1, r2, trace, sigmas
 
 
+def relative_error(xhat, x):
+    """error(x_hat) = min_s ||R_s x_hat - x||_F / ||x||_F, (R_s z)[p] = z[p - s]
+    (Eq. (2) sign, np.roll), brute force over every shift; returns (error, (s1, s2)), ties: the
+    smallest s1 L + s2."""
+    xhat = _f64(xhat)
+    x = _f64(x)
+    L = x.shape[0]
+    best, arg = np.inf, (0, 0)
+    for s1 in range(L):
+        for s2 in range(L):
+            d = np.linalg.norm(np.roll(xhat, (s1, s2), axis=(0, 1)) - x)
+            if d < best:
+                best, arg = d, (s1, s2)
+    return float(best / np.linalg.norm(x)), arg
+
+
 def posterior(yi, L_low, K, sigma, x, rho1, rho2):
     """(w [L][L], log-likelihood term) of one observation."""
     lib = _load()

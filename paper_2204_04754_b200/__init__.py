@@ -34,7 +34,7 @@ ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_it
                "srmra_get_loglik_trace", "srmra_get_stats", "srmra_get_obs_loglik", "srmra_local_stats",
                "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
-               "srmra_last_error", "srmra_run", "srmra_set_denoiser")
+               "srmra_last_error", "srmra_run", "srmra_set_denoiser", "srmra_relative_error")
 
 
 class SrmraError(RuntimeError):
@@ -85,6 +85,7 @@ def _load():
         "srmra_last_error": (ctypes.c_char_p, [_ctxp]),
         "srmra_run": (ctypes.c_int, [_ctxp, ctypes.c_int32, ctypes.c_double]),
         "srmra_set_denoiser": (ctypes.c_int, [_ctxp, DENOISER_FN, ctypes.c_void_p]),
+        "srmra_relative_error": (ctypes.c_int, [_ctxp, _fp, _dp, _ip, _ip]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -152,6 +153,22 @@ def srmra_run(ctx, max_iters: int, rel_tol: float = 0.0):
 def srmra_set_denoiser(ctx, fn):
     """fn: a DENOISER_FN (keep a reference while it is installed) or None for the built-in stand-in."""
     _check(_lib.srmra_set_denoiser(ctx, fn if fn is not None else DENOISER_FN(), None), ctx)
+
+
+def srmra_relative_error(ctx, x_true):
+    """(error, (s1, s2)): min_s ||R_s x_hat - x_true||_F / ||x_true||_F and its shift."""
+    xt = np.ascontiguousarray(x_true, dtype=np.float32)
+    err = ctypes.c_double()
+    s1 = ctypes.c_int32()
+    s2 = ctypes.c_int32()
+    _check(_lib.srmra_relative_error(ctx, _ptr(xt, _fp), ctypes.byref(err), ctypes.byref(s1), ctypes.byref(s2)), ctx)
+    return err.value, (s1.value, s2.value)
+
+
+def snr(x_true, sigma: float) -> float:
+    """SNR = ||x||_F^2 / (L_high^2 sigma^2); a definition, evaluated on the host."""
+    x = np.asarray(x_true, dtype=np.float64)
+    return float((x * x).sum() / (x.shape[0] * x.shape[1] * sigma * sigma))
 
 
 def srmra_get_estimate(ctx, L_high: int):
@@ -271,6 +288,9 @@ class Context:
             return
         self._denoiser = DENOISER_FN(lambda x, L, sig, st, user: int(fn(x, L, sig, st)))
         srmra_set_denoiser(self.handle, self._denoiser)
+
+    def relative_error(self, x_true):
+        return srmra_relative_error(self.handle, x_true)
 
     def get_estimate(self):
         return srmra_get_estimate(self.handle, self.L_high)

@@ -169,4 +169,24 @@ cudaError_t launch_x32_from_x64(srmra_ctx* c) {
     return cudaGetLastError();
 }
 
+// NEXT-4, evaluation: corr[s] = sum_p xhat[(p - s) mod L] xref[p] for every shift s, so
+// that ||R_s xhat - xref||^2 = ||xhat||^2 + ||xref||^2 - 2 corr[s]; one block per shift, float64.
+__global__ void k_shift_corr(const double* __restrict__ xhat, const double* __restrict__ xref, int L,
+                             double* __restrict__ corr) {
+    __shared__ double red[32];
+    const int s = blockIdx.x, s1 = s / L, s2 = s - s1 * L;
+    double acc = 0.0;
+    for (int p = threadIdx.x; p < L * L; p += blockDim.x) {
+        const int p1 = p / L, p2 = p - p1 * L;
+        const int q1 = p1 - s1 < 0 ? p1 - s1 + L : p1 - s1, q2 = p2 - s2 < 0 ? p2 - s2 + L : p2 - s2;
+        acc = fma(xhat[q1 * L + q2], xref[p], acc);
+    }
+    acc = block_sum(acc, red);
+    if (threadIdx.x == 0) corr[s] = acc;
+}
+cudaError_t launch_shift_corr(srmra_ctx* c, const double* xref_dev, double* corr_dev) {
+    k_shift_corr<<<c->L2, 256, 0, c->stream>>>(c->d_x64, xref_dev, c->L, corr_dev);
+    return cudaGetLastError();
+}
+
 }  // namespace srmra

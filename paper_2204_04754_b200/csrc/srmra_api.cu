@@ -579,6 +579,42 @@ int srmra_run(srmra_ctx* c, int32_t max_iters, double rel_tol) {
     return iterate(c, max_iters, rel_tol);
 }
 
+int srmra_relative_error(srmra_ctx* c, const float* x_true, double* err_out, int32_t* s1_out, int32_t* s2_out) {
+    if (!c || !x_true) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
+    if (c->failed) return SRMRA_ERR_STATE;
+    std::vector<double> xr(c->L2), corr(c->L2), xh(c->L2);
+    double nr = 0.0;
+    for (int p = 0; p < c->L2; ++p) {
+        xr[p] = (double)x_true[p];
+        nr += xr[p] * xr[p];
+    }
+    if (!(nr > 0.0) || !isfinite(nr)) return fail(c, SRMRA_ERR_INVALID_ARG, "x_true must be finite and non-zero");
+    double* d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof(double) * 2 * c->L2, c->stream));
+    cudaError_t e = cudaMemcpyAsync(d, xr.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = launch_shift_corr(c, d, d + c->L2);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(corr.data(), d + c->L2, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(xh.data(), c->d_x64, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream);
+    cudaFreeAsync(d, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "srmra_relative_error");
+    int best = 0;  // the minimiser maximises the correlation; ties: the smallest flattened shift
+    for (int s = 1; s < c->L2; ++s)
+        if (corr[s] > corr[best]) best = s;
+    // the distance at the minimiser directly (||x_hat||^2 + ||x||^2 - 2 corr cancels for small errors)
+    const int L = c->L, b1 = best / L, b2 = best % L;
+    double d2 = 0.0;
+    for (int p1 = 0; p1 < L; ++p1)
+        for (int p2 = 0; p2 < L; ++p2) {
+            const double d = xh[(size_t)((p1 - b1 + L) % L) * L + (p2 - b2 + L) % L] - xr[(size_t)p1 * L + p2];
+            d2 += d * d;
+        }
+    if (err_out) *err_out = sqrt(d2) / sqrt(nr);
+    if (s1_out) *s1_out = best / c->L;
+    if (s2_out) *s2_out = best % c->L;
+    return SRMRA_OK;
+}
+
 int srmra_set_denoiser(srmra_ctx* c, srmra_denoiser_fn fn, void* user) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;

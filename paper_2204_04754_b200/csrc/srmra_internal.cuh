@@ -123,6 +123,7 @@ cudaError_t launch_prep(srmra_ctx* c);          // theta -> IterParams (+ Xhat),
 cudaError_t launch_pack(srmra_ctx* c);          // colsum (+ Bhat) -> packed b | cmass | marg | LL
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
 cudaError_t launch_x32_from_x64(srmra_ctx* c);   // after a denoiser hook changed x
+cudaError_t launch_shift_corr(srmra_ctx* c, const double* xref_dev, double* corr_dev);  // NEXT-4
 // ---------------------------------------------------------------- path kernels
 cudaError_t launch_direct_em(srmra_ctx* c);     // k_direct.cu
 bool direct_supported(int L, int Ll, int K);

@@ -403,3 +403,23 @@ def test_alg2_stopping_rule_and_identity_denoiser(oracle_mod):
     t_star = 1 + next(k for k, v in enumerate(d) if v <= tol)
     *_, trs, _ = oracle_mod.run_alg2(*args, 12, proj_every=0, rel_tol=tol)
     assert len(trs) == t_star + 1
+
+
+# ---------------------------------------------------------------- NEXT-4: evaluation
+def test_relative_error_closed_forms(oracle_mod):
+    """error(x_hat) = min_s ||R_s x_hat - x||_F / ||x||_F: zero for any circular shift
+    of x, attained at the inverse shift; 1 for x_hat = 0 and for x_hat = 2x (Cauchy-Schwarz:
+    <R_s x, x> <= ||x||^2, so ||R_s 2x - x||^2 = 5||x||^2 - 4<R_s x, x> >= ||x||^2, equality at s = 0)."""
+    rng = np.random.default_rng(3)
+    L = 12
+    x = rng.standard_normal((L, L))
+    for u in [(0, 0), (3, 5), (11, 1)]:
+        err, s = oracle_mod.relative_error(np.roll(x, u, axis=(0, 1)), x)
+        assert err <= 1e-14 and s == ((-u[0]) % L, (-u[1]) % L)
+    assert abs(oracle_mod.relative_error(np.zeros((L, L)), x)[0] - 1.0) <= 1e-14
+    err, s = oracle_mod.relative_error(2 * x, x)
+    assert abs(err - 1.0) <= 1e-13 and s == (0, 0)
+    # a perturbed shift: the distance is exactly the perturbation's norm while it stays the minimiser
+    e = 1e-3 * rng.standard_normal((L, L))
+    err, s = oracle_mod.relative_error(np.roll(x, (4, 7), axis=(0, 1)) + e, x)
+    assert s == (L - 4, L - 7) and abs(err - np.linalg.norm(e) / np.linalg.norm(x)) <= 1e-12
