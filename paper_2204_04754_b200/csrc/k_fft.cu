@@ -116,8 +116,13 @@ __host__ __device__ inline size_t group_smem(int KK, int ystride) {
     return (b + 15) & ~(size_t)15;
 }
 template <int LL>
-__host__ __device__ inline size_t par_bytes(int KK) {  // logit-bias table lr1 | lr2 | beta, L = K LL <= 8 LL
+__host__ __device__ inline size_t par_off_lrp(int KK) {  // logit-bias table lr1 | lr2 | beta, L = K LL <= 8 LL
     return ((size_t)(2 * 8 * LL + KK) * sizeof(float) + 15) & ~(size_t)15;
+}
+// ... followed by the per-pair lr2 table lrp [NP][LL] float2 = (lr2 of class 2q, lr2 of class 2q+1) at n2
+template <int LL>
+__host__ __device__ inline size_t par_bytes(int KK) {
+    return par_off_lrp<LL>(KK) + sizeof(float2) * (size_t)((KK + 1) / 2) * LL;
 }
 template <int LL>
 __host__ __device__ inline size_t smem_bytes(int KK, int groups, int ystride) {
@@ -212,6 +217,14 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     for (int r = 1; r < KK; ++r) emin = fmin(emin, __ldg(a.par64 + r));
     for (int r = threadIdx.x; r < KK; r += blockDim.x)
         pars[2 * L + r] = (float)((emin - __ldg(a.par64 + r)) * a.inv_2s2 * 1.4426950408889634074);
+    {  // per-pair lr2 table: one 128-bit load gives two n2 of both classes in the softmax
+        float2* lrp_w = reinterpret_cast<float2*>(smem_raw + par_off_lrp<LL>(KK));
+        for (int k = threadIdx.x; k < NP * LL; k += blockDim.x) {
+            const int qq = k / LL, n2 = k - qq * LL, rA = 2 * qq, rB = 2 * qq + 1;
+            lrp_w[k] = make_float2(__ldg(a.par32 + L + rA % K + K * n2),
+                                   rB < KK ? __ldg(a.par32 + L + rB % K + K * n2) : 0.f);
+        }
+    }
     if (XS) {
         const float4* src = a.xhat;
         float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const float zx = role_u ? zu.x : zv.x, zy = su * (role_u ? zu.y : zv.y);
                             ac[2 * e] = fmaf(yv.x, zx, fmaf(-yv.y, zy, ac[2 * e]));
                             ac[2 * e + 1] = fmaf(yv.y, zx, fmaf(yv.x, zy, ac[2 * e + 1]));
-                            if (vsrc) {
+                            if (vsrc) {  // (a separate loop after the chunks measured slower)
                                 const int col = idx == 0 ? 0 : LL;
                                 zc[2 * q * LL + col + k1] = zu;
                                 yc[2 * q * LL + col + k1] = yv;
@@ -417,10 +430,16 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 // ---- posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e/sigma^2 + bias
                 float mt = -INFINITY, za = 0.f, zb = 0.f;
                 if (line_ok) {
+                    const float4* lq = reinterpret_cast<const float4*>(smem_raw + par_off_lrp<LL>(KK)) + q * (LL / 2);
 #pragma unroll
                     for (int n2 = 0; n2 < LL; ++n2) {
-                        const float va = fmaf(v[n2].x - sref, a.c2, biasA + lr2[ra2 + K * n2]);
-                        const float vb = has_b ? fmaf(v[n2].y - sref, a.c2, biasB + lr2[rb2 + K * n2]) : -INFINITY;
+                        float2 b2;
+                        if constexpr (LL >= 2) {
+                            const float4 l4 = lq[n2 >> 1];
+                            b2 = (n2 & 1) ? make_float2(l4.z, l4.w) : make_float2(l4.x, l4.y);
+                        }
+                        const float va = fmaf(v[n2].x - sref, a.c2, biasA + b2.x);
+                        const float vb = has_b ? fmaf(v[n2].y - sref, a.c2, biasB + b2.y) : -INFINITY;
                         v[n2] = make_float2(va, vb);
                         mt = fmaxf(mt, fmaxf(va, vb));
                     }
