@@ -182,6 +182,37 @@ __device__ __forceinline__ void group_reduce_ms(float& m, float& z, float2* scra
     z = Zs;
 }
 
+// (s, m, z) triples: a set of unnormalised weights 2^(s c2 + v) with log2 maximum s c2 + m and scaled
+// sum z = sum 2^(v - m); two sets combine through the difference of their maxima, (s - s') c2 + (m - m'),
+// so every thread may use its own score reference s (no separate max reduction)
+__device__ __forceinline__ void smz_combine(float& s, float& m, float& z, float s2, float m2, float z2, float c2) {
+    if (m2 == -INFINITY) return;  // the other set is empty
+    const float d = fmaf(s - s2, c2, m - m2);  // -inf when this set is empty
+    const bool keep = d >= 0.f;
+    const float e = ex2(-fabsf(d));
+    z = keep ? fmaf(z2, e, z) : fmaf(z, e, z2);
+    s = keep ? s : s2;
+    m = keep ? m : m2;
+}
+__device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, float c2, float4* scratch, int gwarp,
+                                                 int nwarps, int lane, int bar_id, int gthreads) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float z2 = __shfl_xor_sync(0xffffffffu, z, o);
+        smz_combine(s, m, z, s2, m2, z2, c2);
+    }
+    if (nwarps == 1) return;
+    if (lane == 0) scratch[gwarp] = make_float4(s, m, z, 0.f);
+    group_bar(bar_id, gthreads);
+    float S = scratch[0].x, Mx = scratch[0].y, Zs = scratch[0].z;
+    for (int w = 1; w < nwarps; ++w) smz_combine(S, Mx, Zs, scratch[w].x, scratch[w].y, scratch[w].z, c2);
+    s = S;
+    m = Mx;
+    z = Zs;
+}
+
 // PAIRS = true when K^2 is even (every complex transform carries two classes); for odd K^2 the
 // imaginary half of the last pair is empty.
 // XS = true: the pair-interleaved Xhat of this iteration is staged once per CTA in shared memory
@@ -417,17 +448,18 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 }
             }
             if (pass == 1) {
-                // ---- scores S_ra = Re, S_rb = -Im (inverse via conjugation); row reference Sref
-                float lmax = -INFINITY;
+                // ---- scores S_ra = Re, S_rb = -Im (inverse via conjugation); this row's reference
+                float lmax = 0.f;
                 if (line_ok) {
+                    lmax = -INFINITY;
 #pragma unroll
                     for (int n2 = 0; n2 < LL; ++n2) {
                         v[n2].y = -v[n2].y;
                         lmax = fmaxf(lmax, has_b ? fmaxf(v[n2].x, v[n2].y) : v[n2].x);
                     }
                 }
-                sref = group_reduce<float, true>(lmax, redf, gwarp, nwarps, lane, bar_id, GT);
-                // ---- posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e/sigma^2 + bias
+                const float sref_t = lmax;
+                // ---- posterior (eq:weights_EM) in log2 units: v2 = (S - sref_t) log2e/sigma^2 + bias
                 float mt = -INFINITY, za = 0.f, zb = 0.f;
                 if (line_ok) {
                     const float4* lq = reinterpret_cast<const float4*>(smem_raw + par_off_lrp<LL>(KK)) + q * (LL / 2);
@@ -438,8 +470,8 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const float4 l4 = lq[n2 >> 1];
                             b2 = (n2 & 1) ? make_float2(l4.z, l4.w) : make_float2(l4.x, l4.y);
                         }
-                        const float va = fmaf(v[n2].x - sref, a.c2, biasA + b2.x);
-                        const float vb = has_b ? fmaf(v[n2].y - sref, a.c2, biasB + b2.y) : -INFINITY;
+                        const float va = fmaf(v[n2].x - sref_t, a.c2, biasA + b2.x);
+                        const float vb = has_b ? fmaf(v[n2].y - sref_t, a.c2, biasB + b2.y) : -INFINITY;
                         v[n2] = make_float2(va, vb);
                         mt = fmaxf(mt, fmaxf(va, vb));
                     }
@@ -454,11 +486,14 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                         zb += eb;
                     }
                 }
+                sref = sref_t;
                 mall = mt;
                 zall = za + zb;
-                group_reduce_ms(mall, zall, red2 + 8, gwarp, nwarps, lane, bar_id, GT);  // scratch disjoint from the max
+                group_reduce_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red2) + 8, gwarp, nwarps, lane,
+                                 bar_id, GT);
                 if (line_ok) {
-                    const float f = ex2(mt - mall) / zall;  // w = e 2^(mt - M) / Z
+                    // w = e 2^((sref_t - Sref) c2 + mt - M) / Z
+                    const float f = mt == -INFINITY ? 0.f : ex2(fmaf(sref_t - sref, a.c2, mt - mall)) / zall;
                     rsumA = fmaf(za, f, rsumA);
                     rsumB = fmaf(zb, f, rsumB);
 #pragma unroll
