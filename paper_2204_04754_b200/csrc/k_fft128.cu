@@ -176,6 +176,33 @@ __device__ __forceinline__ void ms_combine(float& m, float& z, float m2, float z
     z = z * ex2(m - M) + z2 * ex2(m2 - M);
     m = M;
 }
+// (s, m, z): log2 maximum s c2 + m and scaled sum z of a set of unnormalised weights; sets with different
+// score references s combine through (s - s') c2 + (m - m') (see k_fft.cu)
+__device__ __forceinline__ void smz_combine(float& s, float& m, float& z, float s2, float m2, float z2, float c2) {
+    if (m2 == -INFINITY) return;
+    const float d = fmaf(s - s2, c2, m - m2);
+    const bool keep = d >= 0.f;
+    const float e = ex2(-fabsf(d));
+    z = keep ? fmaf(z2, e, z) : fmaf(z, e, z2);
+    s = keep ? s : s2;
+    m = keep ? m : m2;
+}
+__device__ __forceinline__ void cta_smz(float& s, float& m, float& z, float c2, float4* red4, int lane, int warp) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o), m2 = __shfl_xor_sync(0xffffffffu, m, o),
+                    z2 = __shfl_xor_sync(0xffffffffu, z, o);
+        smz_combine(s, m, z, s2, m2, z2, c2);
+    }
+    if (lane == 0) red4[warp] = make_float4(s, m, z, 0.f);
+    __syncthreads();
+    float S = red4[0].x, Mx = red4[0].y, Z = red4[0].z;
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) smz_combine(S, Mx, Z, red4[w].x, red4[w].y, red4[w].z, c2);
+    s = S;
+    m = Mx;
+    z = Z;
+}
 __device__ __forceinline__ void cta_ms(float& m, float& z, float2* red, int lane, int warp) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -377,14 +404,13 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                     v[j].y = dba - v[j].y;
                     lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
                 }
-                const float sref = cta_max(lmax, red, lane, warp);
-                const double sref_d = Da + (double)sref;  // max score of the pair, float64
-                // posterior (eq:weights_EM) in log2 units: v2 = (S - Sref) log2e / sigma^2 + bias
+                const float sref_t = lmax;  // this thread's score reference (relative to D_a)
+                // posterior (eq:weights_EM) in log2 units: v2 = (S - sref_t) log2e / sigma^2 + bias
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
                     const float2 b2 = lrp[h * 65 + j];  // lr2 of (class ra, class rb) at this thread's n2
-                    const float va = fmaf(v[j].x - sref, a.c2, biasA + b2.x);
-                    const float vb = has_b ? fmaf(v[j].y - sref, a.c2, biasB + b2.y) : -INFINITY;
+                    const float va = fmaf(v[j].x - sref_t, a.c2, biasA + b2.x);
+                    const float vb = has_b ? fmaf(v[j].y - sref_t, a.c2, biasB + b2.y) : -INFINITY;
                     v[j] = make_float2(va, vb);
                     mt = fmaxf(mt, fmaxf(va, vb));
                 }
@@ -399,9 +425,11 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 }
                 za += za1;
                 zb += zb1;
+                float sref = sref_t;
                 mall = mt;
                 zall = za + zb;
-                cta_ms(mall, zall, red, lane, warp);
+                cta_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red), lane, warp);
+                const double sref_d = Da + (double)sref;  // the pair's score reference, float64
                 // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64)
                 // g_q = log2 of this pair's largest unnormalised weight: Sref c2 + m_q
                 const double gq = mall == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)mall;
@@ -429,7 +457,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                     Z = (double)zall;
                 }
                 const float dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
-                const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f : ex2(mt - mall + dq) / (float)Z;
+                const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f
+                                                                      : ex2(fmaf(sref_t - sref, a.c2, mt - mall) + dq) / (float)Z;
                 rsumA = fmaf(za, f, rsumA);
                 rsumB = fmaf(zb, f, rsumB);
 #pragma unroll
