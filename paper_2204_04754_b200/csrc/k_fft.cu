@@ -129,7 +129,7 @@ __host__ __device__ inline size_t smem_bytes(int KK, int groups, int ystride) {
     return group_smem<LL>(KK, ystride) * groups + par_bytes<LL>(KK);
 }
 
-// TACC (L_low >= 32): the M-step accumulators U_q / V_q live in tensor memory instead of the group's
+// TACC (L_low >= 32): the M-step accumulators U_q / V_q (and the Yhat values of pass 0) live in tensor memory instead of the group's
 // shared memory, which leaves room for more groups (warps) per SM.  Group shared memory then holds
 // Yb [2][ystride] | Wk [NP][LL][WS] | zc [NP][2][LL] | yc [NP][2][LL] | red [32]; at the end the group's
 // partial (layout part_bins) is staged over Yb / Wk.
@@ -282,7 +282,11 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     // TMEM: warp w reaches lanes 32 (w & 3); a thread's accumulator line (2 LL columns) starts at column
     // 2 LL (w >> 2) of its lane
     const int warp = threadIdx.x >> 5;
-    const uint32_t tacc = TACC ? tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * LL) : 0u;
+    // TMEM per thread: its accumulator line (2 LL columns) and the Yhat values its pass 0 read (2 LL
+    // columns), which are exactly the ones its pass 3 needs (for a mirrored column c >= LH pass 0 reads
+    // Yhat[-k1][LL - c], so index k1 carries V_q[-k1][LL - c] and Z[k1] needs no reflection)
+    const uint32_t tacc = TACC ? tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 4 * LL) : 0u;
+    const uint32_t tys = tacc + 2 * LL;
     if (TACC) {
         float z[16];
 #pragma unroll
@@ -320,7 +324,6 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     // vex0 / vexh, owned by thread (q, k1 = idx)
     const bool role_u = idx < LH;
     const float su = role_u ? -1.f : 1.f;
-    const int ycol = role_u ? idx : LL - idx;
     const bool vsrc = line_ok && (idx == 0 || idx == LL / 2);
     float2 vex0 = make_float2(0.f, 0.f), vexh = make_float2(0.f, 0.f);
     auto vex_update = [&]() {
@@ -371,14 +374,22 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     const int sk2 = flip ? LL - k2 : k2;
                     const float sgn = flip ? -1.f : 1.f;
 #pragma unroll
-                    for (int k1 = 0; k1 < LL; ++k1) {
-                        const int sk1 = flip ? ((LL - k1) & M) : k1;
-                        const int o = sk1 * LH + sk2;
-                        const float2 yv = Y[o];
-                        const float4 xv = XS ? XP[o] : __ldg(XP + o);
-                        const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
-                        const float2 B = cmul_conj(yv, make_float2(xv.z, xv.w));
-                        v[k1] = make_float2(A.x - sgn * B.y, -sgn * A.y - B.x);
+                    for (int c8 = 0; c8 < LL; c8 += 8) {
+                        float ys[16];
+#pragma unroll
+                        for (int e = 0; e < 8 && c8 + e < LL; ++e) {
+                            const int k1 = c8 + e;
+                            const int sk1 = flip ? ((LL - k1) & M) : k1;
+                            const int o = sk1 * LH + sk2;
+                            const float2 yv = Y[o];
+                            const float4 xv = XS ? XP[o] : __ldg(XP + o);
+                            const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
+                            const float2 B = cmul_conj(yv, make_float2(xv.z, xv.w));
+                            v[k1] = make_float2(A.x - sgn * B.y, -sgn * A.y - B.x);
+                            ys[2 * e] = yv.x;
+                            ys[2 * e + 1] = yv.y;
+                        }
+                        if constexpr (TACC) tc::tmem_st16(tys + 2 * c8, ys);
                     }
                 } else if (pass == 1) {
                     // E-step along k2 (row n1 = idx) of the conjugated column result
@@ -401,20 +412,19 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     // U_q[k1][c] += Yhat[k1][c] conj(Z[k1]) (c < LH) | V_q[k1][LL-c] += Yhat[k1][LL-c] Z[-k1]
 #pragma unroll
                     for (int ch = 0; ch < 2 * LL / 16; ++ch) {
-                        float ac[16];
-                        tc::tmem_ld16(tacc + 16 * ch, ac);
+                        float ac[16], ys[16];
+                        tc::tmem_ld16x2(tys + 16 * ch, ys, tacc + 16 * ch, ac);
 #pragma unroll
                         for (int e = 0; e < 8; ++e) {
                             const int k1 = 8 * ch + e;
-                            const float2 yv = Y[k1 * LH + ycol];
-                            const float2 zu = v[k1], zv = v[(LL - k1) & M];
-                            const float zx = role_u ? zu.x : zv.x, zy = su * (role_u ? zu.y : zv.y);
-                            ac[2 * e] = fmaf(yv.x, zx, fmaf(-yv.y, zy, ac[2 * e]));
-                            ac[2 * e + 1] = fmaf(yv.y, zx, fmaf(yv.x, zy, ac[2 * e + 1]));
+                            const float2 z = v[k1];
+                            const float zy = su * z.y;
+                            ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
+                            ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
                             if (vsrc) {  // (a separate loop after the chunks measured slower)
                                 const int col = idx == 0 ? 0 : LL;
-                                zc[2 * q * LL + col + k1] = zu;
-                                yc[2 * q * LL + col + k1] = yv;
+                                zc[2 * q * LL + col + k1] = z;
+                                yc[2 * q * LL + col + k1] = make_float2(ys[2 * e], ys[2 * e + 1]);
                             }
                         }
                         tc::tmem_st16(tacc + 16 * ch, ac);
@@ -537,7 +547,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     const int k1 = 8 * ch + e;
                     const float2 val = make_float2(ac[2 * e], ac[2 * e + 1]);
                     if (role_u) Uq[k1 * LH + idx] = val;
-                    else Vq[k1 * LH + (LL - idx)] = val;
+                    else Vq[((LL - k1) & M) * LH + (LL - idx)] = val;
                 }
             }
         }
@@ -659,7 +669,7 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     // TACC: tensor-memory columns per CTA (one 2 LL-column line per thread, 4 warps share the 128 lanes);
     // the CTAs resident on one SM must fit the 512 columns together
     int cols = 32;
-    while (cols < ((GT * groups / 32 + 3) / 4) * 2 * LL) cols *= 2;
+    while (cols < ((GT * groups / 32 + 3) / 4) * 4 * LL) cols *= 2;  // accumulator + Yhat stash lines
     if (TACC && cols > 512) return cudaErrorInvalidConfiguration;
     if (TACC && per_sm * cols > 512) per_sm = 512 / cols;
     c->fft_tmem_cols = TACC ? cols : 0;

@@ -99,24 +99,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  "l"(src), "r"(bytes), "r"(mbar)
                  : "memory");
 }
-// two 16-column loads and the wait in ONE asm statement (no use of the outputs can be scheduled
-// before the wait)
-__device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float (&va)[16], uint32_t tb, float (&vb)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%32];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
-        "%29, %30, %31}, [%33];\n\t"
-        "tcgen05.wait::ld.sync.aligned;"
-        : "=f"(va[0]), "=f"(va[1]), "=f"(va[2]), "=f"(va[3]), "=f"(va[4]), "=f"(va[5]), "=f"(va[6]), "=f"(va[7]),
-          "=f"(va[8]), "=f"(va[9]), "=f"(va[10]), "=f"(va[11]), "=f"(va[12]), "=f"(va[13]), "=f"(va[14]),
-          "=f"(va[15]), "=f"(vb[0]), "=f"(vb[1]), "=f"(vb[2]), "=f"(vb[3]), "=f"(vb[4]), "=f"(vb[5]), "=f"(vb[6]),
-          "=f"(vb[7]), "=f"(vb[8]), "=f"(vb[9]), "=f"(vb[10]), "=f"(vb[11]), "=f"(vb[12]), "=f"(vb[13]),
-          "=f"(vb[14]), "=f"(vb[15])
-        : "r"(ta), "r"(tb)
-        : "memory");
-}
-
 // ---------------------------------------------------------------- 128-point FFT over a thread pair
 // w = exp(SIGN 2 pi i / 128).  DIT: in v[m] = x[2m + h]; 64-point FFT F_h; G_1[k] = w^k F_1[k];
 // X[k] = G_0[k] + G_1[k], X[k + 64] = G_0[k] - G_1[k].  Thread h keeps k in [32h, 32h + 32).
@@ -484,7 +466,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
 #pragma unroll
                 for (int ch = 0; ch < 8; ++ch) {
                     float ys[16], ac[16];
-                    tmem_ld16x2(ty + 16 * ch, ys, tacc + 16 * ch, ac);
+                    tc::tmem_ld16x2(ty + 16 * ch, ys, tacc + 16 * ch, ac);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         const int m = ch * 8 + e;
@@ -513,7 +495,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
 #pragma unroll
     for (int ch = 0; ch < 8; ch += 2) {
         float ac0[16], ac1[16];
-        tmem_ld16x2(tacc + 16 * ch, ac0, tacc + 16 * ch + 16, ac1);
+        tc::tmem_ld16x2(tacc + 16 * ch, ac0, tacc + 16 * ch + 16, ac1);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const int m = ch * 8 + e;

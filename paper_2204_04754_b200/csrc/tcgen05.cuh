@@ -118,6 +118,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// two 16-column loads and the wait in one statement
+__device__ __forceinline__ void tmem_ld16x2(uint32_t ta, float (&va)[16], uint32_t tb, float (&vb)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=f"(va[0]), "=f"(va[1]), "=f"(va[2]), "=f"(va[3]), "=f"(va[4]), "=f"(va[5]), "=f"(va[6]), "=f"(va[7]),
+          "=f"(va[8]), "=f"(va[9]), "=f"(va[10]), "=f"(va[11]), "=f"(va[12]), "=f"(va[13]), "=f"(va[14]),
+          "=f"(va[15]), "=f"(vb[0]), "=f"(vb[1]), "=f"(vb[2]), "=f"(vb[3]), "=f"(vb[4]), "=f"(vb[5]), "=f"(vb[6]),
+          "=f"(vb[7]), "=f"(vb[8]), "=f"(vb[9]), "=f"(vb[10]), "=f"(vb[11]), "=f"(vb[12]), "=f"(vb[13]),
+          "=f"(vb[14]), "=f"(vb[15])
+        : "r"(ta), "r"(tb)
+        : "memory");
+}
+
 // tf32 split x = hi + lo (round to nearest on both parts): 3xTF32 products keep ~fp32 accuracy
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
