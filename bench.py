@@ -235,7 +235,7 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": int(p.N * p.L_low * (p.L_low // 2 + 1) * 8),
             "kernel": roof_kernel(path, p.L_low),
             "flop_per_unit": fpu, "kernel_ms_avg": em_avg_s * 1e3,
-            "kernel_share_of_step": em_ms / max(iter_ms, 1e-12),
+            "kernel_share_of_step": em_ms / max(tot_ms, 1e-12),
             "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md)"}
 
     # end-to-end through the public API with pinned host buffers: load (H2D) + cfg.iters iterations + D2H

@@ -175,13 +175,16 @@ SRMRA_API int srmra_get_path(const srmra_ctx* ctx);
 /* Number of kernel launches one srmra_em_iter(ctx, 1) enqueues (for launch accounting). */
 SRMRA_API int srmra_launches_per_iter(const srmra_ctx* ctx);
 
-/* Profiling: enable != 0 starts recording CUDA events on the context stream around each
- * iteration and around its dominant E/M kernel (clearing earlier records); 0 stops. */
+/* Profiling: enable != 0 opens a measuring window (clearing earlier records); 0 closes it.
+ * FFT path: every E/M launch stamps its first-CTA start and last-CTA end with the GPU's globaltimer
+ * (no event nodes in the CUDA graph: they cost ~9 % of a c1 iteration); GEMM / direct paths: CUDA
+ * events on the context stream around each iteration and its E/M kernels. */
 SRMRA_API int srmra_profile(srmra_ctx* ctx, int32_t enable);
 
-/* Synchronise and return, over the iterations recorded since srmra_profile(ctx, 1): the summed
- * duration of the dominant E/M kernel launches (*em_kernel_ms), of whole iterations (*iter_ms),
- * and the number of iterations (*n_iters).  Any pointer may be NULL.  Clears the records. */
+/* Synchronise and return, over the iterations run since srmra_profile(ctx, 1) (or the previous
+ * read): the summed duration of the dominant E/M kernel launches (*em_kernel_ms), of whole
+ * iterations (*iter_ms; FFT path: from the spacing of consecutive E/M starts), and the number of
+ * iterations (*n_iters).  Any pointer may be NULL.  Clears the records. */
 SRMRA_API int srmra_profile_read(srmra_ctx* ctx, double* em_kernel_ms, double* iter_ms, int32_t* n_iters);
 
 /* Debug hook: globaltimer stamps (ns) of the FFT path's tail-kernel phase boundaries of the last

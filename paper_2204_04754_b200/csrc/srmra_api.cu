@@ -184,7 +184,7 @@ int allreduce_stats(srmra_ctx* c) {
 }
 
 int record(srmra_ctx* c) {
-    if (!c->prof) return SRMRA_OK;
+    if (!c->prof || c->path == SRMRA_PATH_FFT) return SRMRA_OK;  // FFT: the E/M kernel stamps itself
     cudaEvent_t e = c->prof_event();
     if (!e) return fail(c, SRMRA_ERR_CUDA, "cudaEventCreate failed");
     CK(cudaEventRecord(e, c->stream));
@@ -247,25 +247,26 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
     // tail); the tail takes t and the projection flag from the device counter.  With profiling on, the
     // graph variant carries 4 event-record nodes that are re-pointed to fresh pool events per replay.
     if (device_loop && !c->graph_failed && n_iters > 0) {
-        cudaGraphExec_t* exec = c->prof ? &c->graph_prof : &c->graph;
+        cudaGraphExec_t* exec = &c->graph;  // profiling needs no event nodes: the E/M kernel stamps itself
         if (!*exec) {
             cudaGraph_t g = nullptr;
             cudaEvent_t ph[4] = {nullptr, nullptr, nullptr, nullptr};
             bool ok = true;
-            if (c->prof)
+            const bool prof_nodes = false;
+            if (prof_nodes)
                 for (int k = 0; k < 4 && ok; ++k) ok = cudaEventCreate(&ph[k]) == cudaSuccess;
             ok = ok && cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             if (ok) {
                 bool l = true;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[0], c->stream, cudaEventRecordExternal) == cudaSuccess;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[1], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[0], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[1], c->stream, cudaEventRecordExternal) == cudaSuccess;
                 l = l && launch_fft_em(c) == cudaSuccess;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[2], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[2], c->stream, cudaEventRecordExternal) == cudaSuccess;
                 l = l && launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP, 0, 0) == cudaSuccess;
-                if (c->prof) l = l && cudaEventRecordWithFlags(ph[3], c->stream, cudaEventRecordExternal) == cudaSuccess;
+                if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[3], c->stream, cudaEventRecordExternal) == cudaSuccess;
                 ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && l;
             }
-            if (ok && c->prof) {  // find the event-record nodes by their placeholder events
+            if (ok && prof_nodes) {  // find the event-record nodes by their placeholder events
                 size_t nn = 0;
                 ok = cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess;
                 std::vector<cudaGraphNode_t> nodes(nn);
@@ -282,7 +283,7 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
             }
             if (ok) ok = cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
             // the profiling variant keeps its graph: exec-node updates refer to the graph's node handles
-            if (g && ok && c->prof) c->graph_prof_src = g;
+            if (g && ok && prof_nodes) c->graph_prof_src = g;
             else if (g) cudaGraphDestroy(g);
             if (!ok) {
                 cudaGetLastError();  // clear the capture error; stream launches are used instead
@@ -291,19 +292,12 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
             }
             // placeholders must outlive the exec (destroying them invalidates its event-record nodes)
             for (int k = 0; k < 4; ++k) {
-                if (ok && c->prof) c->prof_ph[k] = ph[k];
+                if (ok && prof_nodes) c->prof_ph[k] = ph[k];
                 else if (ph[k]) cudaEventDestroy(ph[k]);
             }
         }
         if (*exec) {
             for (int it = 0; it < n_iters; ++it) {
-                if (c->prof) {
-                    for (int j = 0; j < 4; ++j) {
-                        cudaEvent_t e = c->prof_event();
-                        if (!e) return fail(c, SRMRA_ERR_CUDA, "cudaEventCreate failed");
-                        CK(cudaGraphExecEventRecordNodeSetEvent(*exec, c->prof_nodes[j], e));
-                    }
-                }
                 CK(cudaGraphLaunch(*exec, c->stream));
                 c->iters_done++;
             }
@@ -487,6 +481,8 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->d_counter, 1));
     CKI(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
     CKI(dalloc(&c->d_iter, 1));
+    CKI(dalloc(&c->d_emt, 2 * (size_t)opt.trace_cap));
+    CKI(cudaMemset(c->d_emt, 0, sizeof(unsigned long long) * 2 * (size_t)opt.trace_cap));
     CKI(dalloc(&c->d_run, 2));
     CKI(cudaMemset(c->d_run, 0, 2 * sizeof(int)));
     CKI(dalloc(&c->d_rtol, 1));
@@ -629,6 +625,17 @@ int srmra_profile(srmra_ctx* c, int32_t enable) {
     CK(cudaStreamSynchronize(c->stream));
     c->prof = enable != 0;
     c->ev_used = 0;
+    if (c->path == SRMRA_PATH_FFT && c->prof) {  // arm the E/M launch stamps of the window
+        int rc;
+        if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
+        c->prof_t0 = c->iters_done;
+        std::vector<unsigned long long> arm(2 * (size_t)c->opt.trace_cap);
+        for (size_t k = 0; k < arm.size(); k += 2) {
+            arm[k] = ~0ull;
+            arm[k + 1] = 0ull;
+        }
+        CK(cudaMemcpy(c->d_emt, arm.data(), sizeof(unsigned long long) * arm.size(), cudaMemcpyHostToDevice));
+    }
     return SRMRA_OK;
 }
 
@@ -638,6 +645,29 @@ int srmra_profile_read(srmra_ctx* c, double* em_ms, double* iter_ms, int32_t* n_
     CK(cudaStreamSynchronize(c->stream));
     double em = 0, tot = 0;
     int n = 0;
+    if (c->path == SRMRA_PATH_FFT) {
+        // E/M launch duration = last-CTA end - first-CTA start (globaltimer ns); iteration = the time
+        // between consecutive E/M starts (the window's last iteration contributes its E/M time only)
+        int rc;
+        if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
+        const int t1 = std::min(c->iters_done, c->opt.trace_cap);
+        const int m = t1 - c->prof_t0;
+        if (m > 0) {
+            std::vector<unsigned long long> st(2 * (size_t)m);
+            CK(cudaMemcpy(st.data(), c->d_emt + 2 * (size_t)c->prof_t0, sizeof(unsigned long long) * st.size(),
+                          cudaMemcpyDeviceToHost));
+            for (int k = 0; k < m; ++k, ++n) {
+                em += (double)(st[2 * k + 1] - st[2 * k]) * 1e-6;
+                if (k + 1 < m) tot += (double)(st[2 * k + 2] - st[2 * k]) * 1e-6;
+            }
+            if (m > 1) tot *= (double)m / (m - 1);  // per-iteration mean over the m - 1 full intervals
+        }
+        c->prof_t0 = c->iters_done;
+        if (em_ms) *em_ms = em;
+        if (iter_ms) *iter_ms = tot;
+        if (n_iters) *n_iters = n;
+        return SRMRA_OK;
+    }
     for (size_t k = 0; k + 4 <= c->ev_used; k += 4, ++n) {
         float a = 0, b = 0;
         CK(cudaEventElapsedTime(&a, c->ev_pool[k + 1], c->ev_pool[k + 2]));
@@ -761,6 +791,7 @@ void srmra_free(srmra_ctx* c) {
         if (c->prof_ph[k]) cudaEventDestroy(c->prof_ph[k]);
     if (c->d_iter) cudaFree(c->d_iter);
     if (c->d_run) cudaFree(c->d_run);
+    if (c->d_emt) cudaFree(c->d_emt);
     if (c->d_rtol) cudaFree(c->d_rtol);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->copy_event) cudaEventDestroy(c->copy_event);

@@ -93,6 +93,8 @@ struct srmra_ctx {
     cudaEvent_t prof_ph[4] = {nullptr, nullptr, nullptr, nullptr};  // capture placeholders, same
     bool graph_failed = false;
     unsigned long long* d_stamps = nullptr;  // [8] tail-kernel phase timestamps (env SRMRA_TAIL_STAMPS)
+    unsigned long long* d_emt = nullptr;     // [trace_cap][2] E/M kernel first-CTA start / last-CTA end (globaltimer ns)
+    int prof_t0 = 0;                         // first iteration of the current profiling window
     int iters_done = 0;
 
     // gemm path (k_gemm.cu): tf32 hi|lo splits, scores, transposed posterior, Z = W^T Y, rotated x copies
