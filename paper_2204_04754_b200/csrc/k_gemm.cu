@@ -51,6 +51,18 @@ struct GemmArgs {
     int64_t ldc;
 };
 
+// GEMM column order: j = (r Ll + t1) Ll + t2 for shift s = (r1 + K t1, r2 + K t2), class r = r1 K + r2 — the
+// shifts of one class and one t1 are Ll consecutive columns (their T(x) rows are circular shifts of one
+// row of x_r, which makes a B tile a rectangular box of the circulant factor used by the TMA mainloop)
+__device__ __forceinline__ void j_to_s(int j, int Ll, int K, int& s1, int& s2) {
+    const int t2 = j % Ll, rt = j / Ll, t1 = rt % Ll, r = rt / Ll;
+    s1 = r / K + K * t1;
+    s2 = r % K + K * t2;
+}
+__device__ __forceinline__ int s_to_j(int s1, int s2, int Ll, int K) {
+    return (((s1 % K) * K + (s2 % K)) * Ll + s1 / K) * Ll + s2 / K;
+}
+
 // rotated, periodically extended polyphase copies: xe[h][r][rot][row][c] = x_r[row][(c + rot) mod Ll]
 __device__ __forceinline__ size_t xe_index(int h, int r, int rot, int row, int c, int KK, int Ll) {
     return ((((size_t)h * KK + r) * 4 + rot) * Ll + row) * (2 * Ll) + c;
@@ -91,11 +103,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_gemm3(GemmArgs g) {
     // rotation rot = st0 & 3 is fixed per row and the extended column is c0 = (st0 & ~3) + n2.
     int t1 = 0, rot = 0, c0base = 0, rcls = 0;
     if (IMPLICIT_B) {
-        const int s = b_ok ? brow : 0;
-        const int s1 = s / g.L, s2 = s - s1 * g.L;
-        rcls = (s1 % g.K_ds) * g.K_ds + (s2 % g.K_ds);
-        t1 = s1 / g.K_ds;
-        const int t2 = s2 / g.K_ds;
+        const int j = b_ok ? brow : 0;  // column order j = (r Ll + t1) Ll + t2
+        const int t2 = j % g.Ll;
+        t1 = (j / g.Ll) % g.Ll;
+        rcls = j / (g.Ll * g.Ll);
         const int st0 = (g.Ll - t2) % g.Ll;
         rot = st0 & 3;
         c0base = st0 - rot;
@@ -293,10 +304,12 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
         const float sref = warp_max(mx);
         float vm = -INFINITY;
         int am = 0;
-        for (int s = lane; s < L2; s += 32) {
-            const int s1 = s / L, s2 = s - s1 * L;
+        const int Llc = L / K;
+        for (int s = lane; s < L2; s += 32) {  // s: GEMM column j
+            int s1, s2;
+            j_to_s(s, Llc, K, s1, s2);
             const float v = fmaf(Si[s] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
-            if (v > vm) { vm = v; am = s; }
+            if (v > vm || (v == vm && s2 + L * s1 < am)) { vm = v; am = s2 + L * s1; }  // am: shift index
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {  // argmax (ties: smaller shift index)
@@ -307,7 +320,8 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
         const float m = vm;
         float z = 0.f;
         for (int s = lane; s < L2; s += 32) {
-            const int s1 = s / L, s2 = s - s1 * L;
+            int s1, s2;
+            j_to_s(s, Llc, K, s1, s2);
             const float v = fmaf(Si[s] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
             z += expf(v - m);
         }
@@ -343,7 +357,8 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
             const int s = s0 + tx;
             float w = 0.f;
             if (i < n && s < L2) {
-                const int s1 = s / L, s2 = s - s1 * L;
+                int s1, s2;
+                j_to_s(s, L / K, K, s1, s2);
                 const float v = fmaf(S[(size_t)i * L2 + s] - sref_s[rr], inv_s2f,
                                      lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
                 w = expf(v - m_s[rr]) * iz_s[rr];
@@ -375,13 +390,14 @@ __global__ void k_gemm_fold(const float* __restrict__ Z, int64_t ldz, int L, int
         double acc = 0.0;
         for (int nn = lane; nn < Ll2; nn += 32) {
             const int n1 = nn / Ll, n2 = nn - n1 * Ll;
-            const int s = imod(n1 * K - p1, L) * L + imod(n2 * K - p2, L);
-            acc += (double)Z[(size_t)s * ldz + nn];
+            const int j = s_to_j(imod(n1 * K - p1, L), imod(n2 * K - p2, L), Ll, K);
+            acc += (double)Z[(size_t)j * ldz + nn];
         }
         acc = warp_sum(acc);
         if (lane == 0) {
             b[p] = acc;
-            colsum[p] = (double)Z[(size_t)p * ldz + Ll2];  // column Ll2 = W^T . ones
+            // colsum of shift s = p (the loop index doubles as a shift): column Ll2 = W^T . ones
+            colsum[p] = (double)Z[(size_t)s_to_j(p1, p2, Ll, K) * ldz + Ll2];
         }
     }
 }
