@@ -15,6 +15,7 @@
 // 3-stage cp.async ring; one elected thread issues 3 x 4 tcgen05.mma.kind::tf32 (hi*hi, hi*lo, lo*hi)
 // per step and commits them to the stage's mbarrier, which the loads of the stage's next use wait on.
 #include <math.h>
+#include <stdlib.h>
 
 #include "srmra_internal.cuh"
 #include "tcgen05.cuh"
@@ -407,6 +408,19 @@ __global__ void k_gemm_fold(const float* __restrict__ Z, int64_t ldz, int L, int
 // ==================================================================== host side
 using namespace gemmk;
 
+bool gemm_tma_supported(int Ll);
+size_t gemm_circ_floats(int L, int K);
+cudaError_t launch_gemm_circ(const float* x32, int L, int K, float* cf, cudaStream_t st);
+cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
+                            const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
+                            float* c, int64_t ldc, cudaStream_t st);
+
+// TMA mainloop (k_gemm_tma.cu) for L_low in {32, 64}; SRMRA_GEMM_TMA=0 selects the cp.async mainloop
+static bool use_tma(const srmra_ctx* c) {
+    const char* e = getenv("SRMRA_GEMM_TMA");
+    return gemm_tma_supported(c->Ll) && !(e && atoi(e) == 0);
+}
+
 // L_low <= 64: the fp32 tensor-core accumulation chains (L_low^2 / KSPLIT terms) keep the scores within the
 // parity tolerance; at L_low = 128 the FFT path (k_fft128.cu) is the path.
 bool gemm_supported(int L, int Ll, int K) { return Ll >= 4 && Ll <= 64 && (Ll % 4) == 0 && L <= 4096 && K * K <= 256; }
@@ -422,6 +436,7 @@ size_t gemm_bytes(const srmra_ctx* c) {
     b += sizeof(float) * 2 * (size_t)c->L2 * ldw;                // W^T hi/lo
     b += sizeof(float) * (size_t)c->L2 * (c->Ll2 + 16);          // Z
     b += sizeof(float) * 2 * (size_t)c->KK * 4 * c->Ll * 2 * c->Ll;  // rotated x copies
+    b += sizeof(float) * gemm_circ_floats(c->L, c->K);              // circulant factor (TMA mainloop)
     return b;
 }
 
@@ -434,6 +449,9 @@ cudaError_t gemm_alloc(srmra_ctx* c) {
     if ((e = cudaMalloc(&c->g_wthl, sizeof(float) * 2 * (size_t)c->L2 * ldw)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->g_z, sizeof(float) * (size_t)c->L2 * (c->Ll2 + 16))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->g_xe, sizeof(float) * 2 * (size_t)c->KK * 4 * c->Ll * 2 * c->Ll)) != cudaSuccess) return e;
+    if (gemm_tma_supported(c->Ll) &&
+        (e = cudaMalloc(&c->g_cf, sizeof(float) * gemm_circ_floats(c->L, c->K))) != cudaSuccess)
+        return e;
     c->g_ldw = ldw;
     return cudaFuncSetAttribute(k_gemm3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess
                ? cudaGetLastError()
@@ -441,7 +459,7 @@ cudaError_t gemm_alloc(srmra_ctx* c) {
 }
 
 void gemm_free(srmra_ctx* c) {
-    void* bufs[] = {c->g_yhl, c->g_ythl, c->g_s, c->g_wthl, c->g_z, c->g_xe};
+    void* bufs[] = {c->g_yhl, c->g_ythl, c->g_s, c->g_wthl, c->g_z, c->g_xe, c->g_cf};
     for (void* p : bufs)
         if (p) cudaFree(p);
 }
@@ -458,10 +476,33 @@ cudaError_t launch_gemm_init(srmra_ctx* c) {
 // prep (k_prep of k_common.cu runs first) -> GEMM1 -> softmax -> GEMM2 -> fold; the pack kernel follows
 cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1) {
     const int64_t n = c->n_local;
-    const int total = c->KK * 4 * c->Ll * 2 * c->Ll;
-    k_gemm_prep<<<(total + 255) / 256, 256, 0, c->stream>>>(c->d_x32, c->L, c->K, c->g_xe);
+    const bool tma = use_tma(c);
+    if (tma) {
+        cudaError_t e = launch_gemm_circ(c->d_x32, c->L, c->K, c->g_cf, c->stream);
+        if (e != cudaSuccess) return e;
+    } else {
+        const int total = c->KK * 4 * c->Ll * 2 * c->Ll;
+        k_gemm_prep<<<(total + 255) / 256, 256, 0, c->stream>>>(c->d_x32, c->L, c->K, c->g_xe);
+    }
     if (n == 0) return cudaGetLastError();
     if (ev_em0) cudaEventRecord(ev_em0, c->stream);
+    if (tma) {
+        const size_t cfp = gemm_circ_floats(c->L, c->K) / 2;  // one plane
+        cudaError_t e = launch_gemm_tma(c->g_yhl, c->g_yhl + (size_t)n * c->Ll2, n, c->Ll2, c->g_cf, c->g_cf + cfp,
+                                        (int64_t)c->KK * c->Ll2, c->Ll, c->L2, c->Ll2, 1, c->Ll, c->g_s, c->L2, c->stream);
+        if (e != cudaSuccess) return e;
+        k_gemm_softmax<<<(unsigned)((n + 31) / 32), 256, 0, c->stream>>>(
+            c->g_s, n, c->L, c->K, c->par.f32, c->par.f64, c->d_ynorm, (float)c->inv_s2, c->inv_s2, c->inv_2s2, c->g_ldw,
+            c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho);
+        e = launch_gemm_tma(c->g_wthl, c->g_wthl + (size_t)c->L2 * c->g_ldw, c->L2, c->g_ldw, c->g_ythl,
+                            c->g_ythl + (size_t)(c->Ll2 + 16) * c->g_ldw, c->Ll2 + 16, c->g_ldw, c->Ll2 + 16, c->g_ldw,
+                            0, c->Ll, c->g_z, c->Ll2 + 16, c->stream);
+        if (e != cudaSuccess) return e;
+        if (ev_em1) cudaEventRecord(ev_em1, c->stream);
+        k_gemm_fold<<<(c->L2 * 32 + 255) / 256, 256, 0, c->stream>>>(c->g_z, c->Ll2 + 16, c->L, c->K,
+                                                                      c->d_pack + c->pk.b, c->d_colsum);
+        return cudaGetLastError();
+    }
     GemmArgs g1{};
     g1.a_hi = c->g_yhl;
     g1.a_lo = c->g_yhl + (size_t)n * c->Ll2;

@@ -104,6 +104,7 @@ struct srmra_ctx {
     float* g_wthl = nullptr;  // [2][L2][ldw]
     float* g_z = nullptr;     // [L2][Ll2 + 16]
     float* g_xe = nullptr;    // [2][KK][4][Ll][2 Ll]
+    float* g_cf = nullptr;    // [2][KK Ll Ll][Ll] circulant factor of the polyphase components (TMA mainloop)
     int64_t g_ldw = 0;        // n rounded up to a multiple of 4
 
     // multi-GPU
