@@ -275,8 +275,11 @@ __global__ void k_gemm_prep(const float* __restrict__ x32, int L, int K, float* 
 }
 
 // ---------------------------------------------------------------- softmax (posterior), transposed W^T
-// Block: 32 observations.  Phase 1 (warp per row): Sref, m, Z, LL_i (logits of k_common.cu, natural
-// units).  Phase 2: 32 x 32 tiles, w = exp(v - m) / Z, transposed through shared memory into W^T hi / lo.
+// Block: 8 observations, one warp per row.  Phase 1: the row maximum Sref, then ONE pass forming the
+// logits (those of k_common.cu, natural units) with an online (max, argmax, sum); the LL is anchored at
+// the argmax shift with an exact float64 residual.  Phase 2: one thread per GEMM column j writes
+// w = exp(v - m) / Z of the block's 8 observations as 32 contiguous bytes of row j of W^T (hi and lo).
+// Rows n..ldw-1 of the last block are zero (the padding of GEMM2's contraction).
 __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ S, int64_t n, int L, int K,
                                                       const float* __restrict__ par32, const double* __restrict__ par64,
                                                       const double* __restrict__ ynorm, float inv_s2f, double inv_s2,
@@ -284,99 +287,109 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
                                                       double* __restrict__ llobs, double* __restrict__ ll_out,
                                                       const float* __restrict__ y, const double* __restrict__ x64,
                                                       const double* __restrict__ rho) {
-    __shared__ float sref_s[32], m_s[32], iz_s[32];
-    __shared__ float tile[32][33];
-    __shared__ double llsum;
-    const int L2 = L * L, KK = K * K;
+    constexpr int R = 8;
+    __shared__ float sref_s[R], m_s[R], iz_s[R];
+    __shared__ double lls[R];
+    const int L2 = L * L, Ll = L / K;
     const float* lr1 = par32;
     const float* lr2 = par32 + L;
     const float* beta = par32 + 2 * L;
     (void)par64;
-    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    (void)ynorm;
+    (void)inv_s2;
+    const int64_t i0 = (int64_t)blockIdx.x * R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) llsum = 0.0;
-    __syncthreads();
-    for (int rr = warp; rr < 32; rr += 8) {
-        const int64_t i = i0 + rr;
-        if (i >= n) continue;
-        const float* Si = S + (size_t)i * L2;
-        float mx = -INFINITY;
-        for (int s = lane; s < L2; s += 32) mx = fmaxf(mx, Si[s]);
-        const float sref = warp_max(mx);
-        float vm = -INFINITY;
-        int am = 0;
-        const int Llc = L / K;
-        for (int s = lane; s < L2; s += 32) {  // s: GEMM column j
-            int s1, s2;
-            j_to_s(s, Llc, K, s1, s2);
-            const float v = fmaf(Si[s] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
-            if (v > vm || (v == vm && s2 + L * s1 < am)) { vm = v; am = s2 + L * s1; }  // am: shift index
-        }
+    {
+        const int64_t i = i0 + warp;
+        if (i < n) {
+            const float4* Si4 = reinterpret_cast<const float4*>(S + (size_t)i * L2);
+            float mx = -INFINITY;
+            for (int q = lane; q < L2 / 4; q += 32) {
+                const float4 v4 = __ldcg(Si4 + q);
+                mx = fmaxf(fmaxf(mx, fmaxf(v4.x, v4.y)), fmaxf(v4.z, v4.w));
+            }
+            const float sref = warp_max(mx);
+            float vm = -INFINITY, z = 0.f;
+            int am = 0;
+            for (int q = lane; q < L2 / 4; q += 32) {
+                const float4 v4 = __ldcg(Si4 + q);
+                const float sv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {  // argmax (ties: smaller shift index)
-            const float v2 = __shfl_xor_sync(0xffffffffu, vm, o);
-            const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
-            if (v2 > vm || (v2 == vm && a2 < am)) { vm = v2; am = a2; }
-        }
-        const float m = vm;
-        float z = 0.f;
-        for (int s = lane; s < L2; s += 32) {
-            int s1, s2;
-            j_to_s(s, Llc, K, s1, s2);
-            const float v = fmaf(Si[s] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
-            z += expf(v - m);
-        }
-        const double Z = warp_sum((double)z);
-        // log-sum-exp anchored at the argmax shift s*: lse = ell[s*] + log sum_s exp(v_s - v_s*), with
-        // ell[s*] = log rho1 + log rho2 - ||y_i - P R_s* x||^2 / (2 sigma^2) from an exact float64 residual,
-        // so the fp32 score error only enters through the (small) log-sum term (eq:likelihood_EM)
-        const int a1 = am / L, a2 = am - a1 * L, Ll = L / K;
-        double d = 0.0;
-        for (int nn = lane; nn < Ll * Ll; nn += 32) {
-            const int n1 = nn / Ll, n2 = nn - n1 * Ll;
-            const double e = (double)y[(size_t)i * Ll * Ll + nn] - x64[(size_t)imod(n1 * K - a1, L) * L + imod(n2 * K - a2, L)];
-            d += e * e;
-        }
-        d = warp_sum(d);
-        if (lane == 0) {
-            sref_s[rr] = sref;
-            m_s[rr] = m;
-            iz_s[rr] = (float)(1.0 / Z);
-            const double lse = log(rho[a1]) + log(rho[L + a2]) - d * inv_2s2 + log(Z);
-            if (llobs) llobs[i] = lse;
-            atomicAdd(&llsum, lse);
+                for (int u = 0; u < 4; ++u) {
+                    int s1, s2;
+                    j_to_s(4 * q + u, Ll, K, s1, s2);
+                    const float v = fmaf(sv[u] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
+                    const int sh = s2 + L * s1;
+                    if (v > vm) {  // online max / sum; argmax ties: the smaller shift index
+                        z = (vm == -INFINITY ? 0.f : z * expf(vm - v)) + 1.f;
+                        vm = v;
+                        am = sh;
+                    } else if (v > -INFINITY) {  // zero prior mass (log 0 = -inf) contributes nothing
+                        z += expf(v - vm);
+                        if (v == vm && sh < am) am = sh;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float v2 = __shfl_xor_sync(0xffffffffu, vm, o), z2 = __shfl_xor_sync(0xffffffffu, z, o);
+                const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+                const float M = fmaxf(vm, v2);
+                const float zc = (vm == -INFINITY ? 0.f : z * expf(vm - M)) + (v2 == -INFINITY ? 0.f : z2 * expf(v2 - M));
+                if (v2 > vm || (v2 == vm && a2 < am)) am = a2;
+                vm = M;
+                z = zc;
+            }
+            // log-sum-exp anchored at the argmax shift s*: lse = ell[s*] + log sum_s exp(v_s - v_s*), with
+            // ell[s*] = log rho1 + log rho2 - ||y_i - P R_s* x||^2 / (2 sigma^2) from an exact float64 residual,
+            // so the fp32 score error only enters through the (small) log-sum term (eq:likelihood_EM)
+            const int a1 = am / L, a2 = am - a1 * L;
+            double d = 0.0;
+            for (int nn = lane; nn < Ll * Ll; nn += 32) {
+                const int n1 = nn / Ll, n2 = nn - n1 * Ll;
+                const double e = (double)y[(size_t)i * Ll * Ll + nn] - x64[(size_t)imod(n1 * K - a1, L) * L + imod(n2 * K - a2, L)];
+                d += e * e;
+            }
+            d = warp_sum(d);
+            if (lane == 0) {
+                sref_s[warp] = sref;
+                m_s[warp] = vm;
+                iz_s[warp] = 1.f / z;
+                const double lse = log(rho[a1]) + log(rho[L + a2]) - d * inv_2s2 + log((double)z);
+                if (llobs) llobs[i] = lse;
+                lls[warp] = lse;
+            }
+        } else if (lane == 0) {
+            sref_s[warp] = 0.f;
+            m_s[warp] = 0.f;
+            iz_s[warp] = 0.f;  // padding rows: w = 0
+            lls[warp] = 0.0;
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(ll_out, llsum);
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int r = 0; r < R; ++r) s += lls[r];
+        atomicAdd(ll_out, s);
+    }
     const size_t plane = (size_t)L2 * ldw;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int s0 = 0; s0 < L2; s0 += 32) {
-        __syncthreads();
-        for (int rr = ty; rr < 32; rr += 8) {  // rows = observations, coalesced along shifts
-            const int64_t i = i0 + rr;
-            const int s = s0 + tx;
+    for (int j = threadIdx.x; j < L2; j += blockDim.x) {
+        int s1, s2;
+        j_to_s(j, Ll, K, s1, s2);
+        const float bias = lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K];
+        float hi[R], lo[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
             float w = 0.f;
-            if (i < n && s < L2) {
-                int s1, s2;
-                j_to_s(s, L / K, K, s1, s2);
-                const float v = fmaf(S[(size_t)i * L2 + s] - sref_s[rr], inv_s2f,
-                                     lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
-                w = expf(v - m_s[rr]) * iz_s[rr];
-            }
-            tile[rr][tx] = w;
+            if (i0 + r < n) w = expf(fmaf(__ldcg(S + (size_t)(i0 + r) * L2 + j) - sref_s[r], inv_s2f, bias) - m_s[r]) * iz_s[r];
+            tc::split_tf32(w, hi[r], lo[r]);
         }
-        __syncthreads();
-        for (int rr = ty; rr < 32; rr += 8) {  // rows = shifts, coalesced along observations
-            const int s = s0 + rr;
-            const int64_t i = i0 + tx;
-            if (s < L2 && i < ldw) {
-                float hi, lo;
-                tc::split_tf32(tile[tx][rr], hi, lo);
-                wthl[(size_t)s * ldw + i] = hi;
-                wthl[plane + (size_t)s * ldw + i] = lo;
-            }
-        }
+        float4* dh = reinterpret_cast<float4*>(wthl + (size_t)j * ldw + i0);
+        float4* dl = reinterpret_cast<float4*>(wthl + plane + (size_t)j * ldw + i0);
+        dh[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        dh[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+        dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
     }
 }
 
@@ -425,7 +438,8 @@ static bool use_tma(const srmra_ctx* c) {
 // parity tolerance; at L_low = 128 the FFT path (k_fft128.cu) is the path.
 bool gemm_supported(int L, int Ll, int K) { return Ll >= 4 && Ll <= 64 && (Ll % 4) == 0 && L <= 4096 && K * K <= 256; }
 
-static int64_t ldw_of(int64_t n) { return ((n + 3) / 4) * 4 > 0 ? ((n + 3) / 4) * 4 : 4; }
+// observations padded to a multiple of 8 (the softmax writes 8 observations = 32 B per W^T row segment)
+static int64_t ldw_of(int64_t n) { return ((n + 7) / 8) * 8 > 0 ? ((n + 7) / 8) * 8 : 8; }
 
 size_t gemm_bytes(const srmra_ctx* c) {
     const int64_t n = c->n_local, ldw = ldw_of(n);
@@ -491,7 +505,7 @@ cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1)
         cudaError_t e = launch_gemm_tma(c->g_yhl, c->g_yhl + (size_t)n * c->Ll2, n, c->Ll2, c->g_cf, c->g_cf + cfp,
                                         (int64_t)c->KK * c->Ll2, c->Ll, c->L2, c->Ll2, 1, c->Ll, c->g_s, c->L2, c->stream);
         if (e != cudaSuccess) return e;
-        k_gemm_softmax<<<(unsigned)((n + 31) / 32), 256, 0, c->stream>>>(
+        k_gemm_softmax<<<(unsigned)(c->g_ldw / 8), 256, 0, c->stream>>>(
             c->g_s, n, c->L, c->K, c->par.f32, c->par.f64, c->d_ynorm, (float)c->inv_s2, c->inv_s2, c->inv_2s2, c->g_ldw,
             c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho);
         e = launch_gemm_tma(c->g_wthl, c->g_wthl + (size_t)c->L2 * c->g_ldw, c->L2, c->g_ldw, c->g_ythl,
@@ -517,7 +531,7 @@ cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1)
     g1.c = c->g_s;
     g1.ldc = c->L2;
     k_gemm3<true><<<dim3((c->L2 + BN - 1) / BN, (unsigned)((n + BM - 1) / BM)), THREADS, SMEM_BYTES, c->stream>>>(g1);
-    k_gemm_softmax<<<(unsigned)((n + 31) / 32), 256, 0, c->stream>>>(
+    k_gemm_softmax<<<(unsigned)(c->g_ldw / 8), 256, 0, c->stream>>>(
         c->g_s, n, c->L, c->K, c->par.f32, c->par.f64, c->d_ynorm, (float)c->inv_s2, c->inv_s2, c->inv_2s2, c->g_ldw,
         c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho);
     GemmArgs g2{};
