@@ -11,4 +11,6 @@ python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_ou
 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/ncul_$T.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_fft_em -s 3 -c 1 -o gpurun_out/prof_$T python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/ncuf_$T.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_fft_em128 -s 1 -c 1 -o gpurun_out/prof128_$T python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/ncuf128_$T.log 2>&1
+ncu --set full --clock-control none -k regex:k_gemm_tma -c 2 -o gpurun_out/profgemm_$T python tools/path_timing.py c1 gemm > gpurun_out/ncug_$T.log 2>&1
+ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none -c 14 --csv --log-file gpurun_out/launches_gemm_$T.csv python tools/path_timing.py c1 gemm > /dev/null 2>&1
 cat gpurun_out/smoke_$T.log; tail -1 gpurun_out/bench_$T.log; tail -1 gpurun_out/bench_ref_$T.log; cat gpurun_out/paths_$T.log
