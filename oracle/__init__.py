@@ -42,6 +42,10 @@ def _load():
         lib.oracle_em_iter.argtypes = [_fp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_double, _dp, _dp, _dp, ctypes.c_int, ctypes.c_double,
                                        _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        lib.oracle_em_iter_joint.restype = ctypes.c_int
+        lib.oracle_em_iter_joint.argtypes = [_fp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_double, _dp, _dp, ctypes.c_int, ctypes.c_double,
+                                             _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         lib.oracle_posterior.restype = ctypes.c_double
         lib.oracle_posterior.argtypes = [_fp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                          _dp, _dp, _dp, _dp]
@@ -102,6 +106,39 @@ def em_iter(y, L_low, K, sigma, x, rho1, rho2, project=True, tau=None) -> IterRe
     if rc != 0:
         raise ValueError(f"oracle_em_iter failed rc={rc}")
     return IterResult(xo, r1, r2, float(ll[0]), b, A, cs, llo)
+
+
+@dataclass
+class JointResult:
+    x: np.ndarray        # float64 [L][L]
+    rho: np.ndarray      # float64 [L][L] joint prior rho'[s1, s2]
+    rho1: np.ndarray     # its marginals
+    rho2: np.ndarray
+    loglik: float
+    b: np.ndarray
+    A: np.ndarray
+    colsum: np.ndarray
+    ll_obs: np.ndarray
+
+
+def em_iter_joint(y, L_low, K, sigma, x, rho, project=True, tau=None) -> JointResult:
+    """NEXT-3: one EM iteration with a joint shift prior rho [L][L] (eq:rho_EM as written)."""
+    lib = _load()
+    y = _f32(y)
+    N = y.shape[0]
+    L = L_low * K
+    x = _f64(x).reshape(L, L)
+    rho = _f64(rho).reshape(L, L)
+    if tau is None:
+        tau = 1e-12 * N
+    xo = np.empty((L, L)); ro = np.empty((L, L)); r1 = np.empty(L); r2 = np.empty(L); ll = np.empty(1)
+    b = np.empty((L, L)); A = np.empty((L, L)); cs = np.empty((L, L)); llo = np.empty(N)
+    rc = lib.oracle_em_iter_joint(_p(y, _fp), N, L, L_low, K, float(sigma), _p(x, _dp), _p(rho, _dp),
+                                  int(bool(project)), float(tau), _p(xo, _dp), _p(ro, _dp), _p(r1, _dp),
+                                  _p(r2, _dp), _p(ll, _dp), _p(b, _dp), _p(A, _dp), _p(cs, _dp), _p(llo, _dp))
+    if rc != 0:
+        raise ValueError(f"oracle_em_iter_joint failed rc={rc}")
+    return JointResult(xo, ro, r1, r2, float(ll[0]), b, A, cs, llo)
 
 
 def run(y, L_low, K, sigma, x0, rho1_0, rho2_0, iters, proj_every=1, tau=None):

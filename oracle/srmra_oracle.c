@@ -67,7 +67,7 @@ static double* build_col_table(const double* x, int L, int Ll, int K) {
 /* ell[s] = log rho1[s1] + log rho2[s2] - ||y_i - P R_s x||^2 / (2 sigma^2) for all s;
  * returns lse = log sum_s exp(ell[s])  (eq:likelihood_EM inner term). */
 static double obs_logits(const float* yi, int L, int Ll, int K, double inv2s2,
-                         const double* xs, const double* lr1, const double* lr2,
+                         const double* xs, const double* lr1, const double* lr2, const double* lrj,
                          double* ell) {
     for (int s1 = 0; s1 < L; ++s1) {
         for (int s2 = 0; s2 < L; ++s2) {
@@ -81,7 +81,8 @@ static double obs_logits(const float* yi, int L, int Ll, int K, double inv2s2,
                     d += e * e;
                 }
             }
-            ell[s1 * L + s2] = lr1[s1] + lr2[s2] - d * inv2s2;
+            /* log prior: separable log rho1[s1] + log rho2[s2], or the joint log rho[s] (NEXT-3) */
+            ell[s1 * L + s2] = (lrj ? lrj[s1 * L + s2] : lr1[s1] + lr2[s2]) - d * inv2s2;
         }
     }
     int L2 = L * L;
@@ -113,7 +114,7 @@ double oracle_posterior(const float* yi, int L, int Ll, int K, double sigma,
     double* lr1 = (double*)malloc(sizeof(double) * L);
     double* lr2 = (double*)malloc(sizeof(double) * L);
     for (int k = 0; k < L; ++k) { lr1[k] = safe_log(rho1[k]); lr2[k] = safe_log(rho2[k]); }
-    double lse = obs_logits(yi, L, Ll, K, 1.0 / (2.0 * sigma * sigma), xs, lr1, lr2, w_out);
+    double lse = obs_logits(yi, L, Ll, K, 1.0 / (2.0 * sigma * sigma), xs, lr1, lr2, NULL, w_out);
     for (int s = 0; s < L * L; ++s) w_out[s] = exp(w_out[s] - lse);
     free(xs); free(lr1); free(lr2);
     return lse;
@@ -135,7 +136,7 @@ int oracle_loglik_obs(const float* y, const int64_t* idx, int64_t n_idx,
         double* ell = (double*)malloc(sizeof(double) * L2);
 #pragma omp for schedule(dynamic, 1)
         for (int64_t j = 0; j < n_idx; ++j)
-            ll_out[j] = obs_logits(y + (size_t)idx[j] * Ll * Ll, L, Ll, K, inv2s2, xs, lr1, lr2, ell);
+            ll_out[j] = obs_logits(y + (size_t)idx[j] * Ll * Ll, L, Ll, K, inv2s2, xs, lr1, lr2, NULL, ell);
         free(ell);
     }
     free(xs);
@@ -151,15 +152,22 @@ int oracle_loglik_obs(const float* y, const int64_t* idx, int64_t n_idx,
  * tau: pixel p keeps x[p] when A[p] <= tau (reading R6).  project: apply the stand-in D.
  * Returns 0, or -1 on invalid sizes, -5 on allocation failure.
  */
-int oracle_em_iter(const float* y, int64_t N, int L, int Ll, int K, double sigma,
-                   const double* x, const double* rho1, const double* rho2,
-                   int project, double tau,
-                   double* x_out, double* rho1_out, double* rho2_out, double* ll_out,
-                   double* b_out, double* A_out, double* colsum_out, double* ll_obs_out) {
+static int em_iter_impl(const float* y, int64_t N, int L, int Ll, int K, double sigma,
+                        const double* x, const double* rho1, const double* rho2, const double* rhoj,
+                        int project, double tau,
+                        double* x_out, double* rho1_out, double* rho2_out, double* rhoj_out, double* ll_out,
+                        double* b_out, double* A_out, double* colsum_out, double* ll_obs_out) {
     if (N < 0 || L <= 0 || Ll <= 0 || K <= 0 || Ll * K != L || !(sigma > 0.0) || L > 4096) return -1;
     const int L2 = L * L, Ll2 = Ll * Ll;
     double lr1[4096], lr2[4096];
-    for (int k = 0; k < L; ++k) { lr1[k] = safe_log(rho1[k]); lr2[k] = safe_log(rho2[k]); }
+    double* lrj = NULL;
+    if (rhoj) {  /* joint prior rho[s] (NEXT-3): its log per shift */
+        lrj = (double*)malloc(sizeof(double) * L2);
+        if (!lrj) return -5;
+        for (int s = 0; s < L2; ++s) lrj[s] = safe_log(rhoj[s]);
+    } else {
+        for (int k = 0; k < L; ++k) { lr1[k] = safe_log(rho1[k]); lr2[k] = safe_log(rho2[k]); }
+    }
     const double inv2s2 = 1.0 / (2.0 * sigma * sigma);
     double* xs = build_col_table(x, L, Ll, K);
     if (!xs) return -5;
@@ -187,7 +195,7 @@ int oracle_em_iter(const float* y, int64_t N, int L, int Ll, int K, double sigma
         for (int64_t i = 0; i < N; ++i) {
             const float* yi = y + (size_t)i * Ll2;
             /* E-step: logits and normaliser C^i (eq:weights_EM) */
-            double lse = obs_logits(yi, L, Ll, K, inv2s2, xs, lr1, lr2, ell);
+            double lse = obs_logits(yi, L, Ll, K, inv2s2, xs, lr1, lr2, lrj, ell);
             *ll += lse;
             if (ll_obs_out) ll_obs_out[i] = lse;
             /* M-step accumulation (eq:x_EM with P^{-1} := P^T, eq:rho_EM) */
@@ -225,7 +233,8 @@ int oracle_em_iter(const float* y, int64_t N, int L, int Ll, int K, double sigma
     }
     free(acc);
 
-    /* rho update: marginals of eq:rho_EM */
+    /* rho update: marginals of eq:rho_EM (separable), or eq:rho_EM as written (joint, NEXT-3) with the
+     * marginals of the new joint prior reported in rho1_out / rho2_out */
     double tot = 0.0;
     for (int s = 0; s < L2; ++s) tot += cs[s];
     for (int k = 0; k < L; ++k) { rho1_out[k] = 0.0; rho2_out[k] = 0.0; }
@@ -235,9 +244,12 @@ int oracle_em_iter(const float* y, int64_t N, int L, int Ll, int K, double sigma
             rho2_out[s2] += cs[s1 * L + s2];
         }
     for (int k = 0; k < L; ++k) {
-        rho1_out[k] = tot > 0 ? rho1_out[k] / tot : rho1[k];
-        rho2_out[k] = tot > 0 ? rho2_out[k] / tot : rho2[k];
+        rho1_out[k] = tot > 0 ? rho1_out[k] / tot : (rhoj ? 0.0 : rho1[k]);
+        rho2_out[k] = tot > 0 ? rho2_out[k] / tot : (rhoj ? 0.0 : rho2[k]);
     }
+    if (rhoj && rhoj_out)
+        for (int s = 0; s < L2; ++s) rhoj_out[s] = tot > 0 ? cs[s] / tot : rhoj[s];
+    free(lrj);
 
     /* x update: A x' = b, A diagonal */
     double* xn = (double*)malloc(sizeof(double) * L2);
@@ -252,4 +264,24 @@ int oracle_em_iter(const float* y, int64_t N, int L, int Ll, int K, double sigma
     if (colsum_out) memcpy(colsum_out, cs, sizeof(double) * L2);
     free(b);
     return 0;
+}
+
+int oracle_em_iter(const float* y, int64_t N, int L, int Ll, int K, double sigma,
+                   const double* x, const double* rho1, const double* rho2,
+                   int project, double tau,
+                   double* x_out, double* rho1_out, double* rho2_out, double* ll_out,
+                   double* b_out, double* A_out, double* colsum_out, double* ll_obs_out) {
+    return em_iter_impl(y, N, L, Ll, K, sigma, x, rho1, rho2, NULL, project, tau, x_out, rho1_out, rho2_out,
+                        NULL, ll_out, b_out, A_out, colsum_out, ll_obs_out);
+}
+
+/* NEXT-3: one EM iteration with a joint (non-separable) shift prior rho[s1 L + s2] (PAPER.md:230-231
+ * with rho[s] as the weight of shift s; eq:rho_EM as written):
+ * rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'}.  rho_out [L^2]; rho1_out / rho2_out its marginals. */
+int oracle_em_iter_joint(const float* y, int64_t N, int L, int Ll, int K, double sigma,
+                         const double* x, const double* rho, int project, double tau,
+                         double* x_out, double* rho_out, double* rho1_out, double* rho2_out, double* ll_out,
+                         double* b_out, double* A_out, double* colsum_out, double* ll_obs_out) {
+    return em_iter_impl(y, N, L, Ll, K, sigma, x, NULL, NULL, rho, project, tau, x_out, rho1_out, rho2_out,
+                        rho_out, ll_out, b_out, A_out, colsum_out, ll_obs_out);
 }

@@ -38,9 +38,10 @@ def P_matrix(L, K):
     return M
 
 
-def dense_em(y, K, sigma, x, rho1, rho2):
+def dense_em(y, K, sigma, x, rho1, rho2, prior=None):
     """EM iteration in the paper's matrix form (eq:likelihood_EM, eq:weights_EM, eq:x_EM with
-    P^{-1} := P^T, eq:rho_EM marginals), dense and brute force."""
+    P^{-1} := P^T, eq:rho_EM marginals), dense and brute force.  `prior` [L][L]: a joint shift prior
+    rho[s] in place of rho1[s1] rho2[s2] (NEXT-3)."""
     N, Ll, _ = y.shape
     L = Ll * K
     P = P_matrix(L, K)
@@ -57,7 +58,8 @@ def dense_em(y, K, sigma, x, rho1, rho2):
         for (a, b), R in Rs.items():
             r = yi - P @ R @ xv
             with np.errstate(divide="ignore"):
-                ell[a, b] = np.log(rho1[a]) + np.log(rho2[b]) - r @ r / (2 * sigma ** 2)
+                lp = np.log(prior[a, b]) if prior is not None else np.log(rho1[a]) + np.log(rho2[b])
+                ell[a, b] = lp - r @ r / (2 * sigma ** 2)
         m = ell.max()
         lse = m + np.log(np.exp(ell - m).sum())
         LL += lse
@@ -423,3 +425,59 @@ def test_relative_error_closed_forms(oracle_mod):
     e = 1e-3 * rng.standard_normal((L, L))
     err, s = oracle_mod.relative_error(np.roll(x, (4, 7), axis=(0, 1)) + e, x)
     assert s == (L - 4, L - 7) and abs(err - np.linalg.norm(e) / np.linalg.norm(x)) <= 1e-12
+
+
+# ---------------------------------------------------------------- NEXT-3: joint (non-separable) prior
+def _joint_prior(L, seed, zeros=0):
+    rng = np.random.default_rng(seed)
+    pr = rng.uniform(0.05, 1.0, (L, L)) ** 3          # far from a product of marginals
+    if zeros:
+        idx = rng.choice(L * L, size=zeros, replace=False)
+        pr.reshape(-1)[idx] = 0.0
+    return pr / pr.sum()
+
+
+@pytest.mark.parametrize("seed,zeros", [(0, 0), (1, 3)])
+def test_joint_bruteforce_dense_4x4(oracle_mod, seed, zeros):
+    """eq:rho_EM as written (PAPER.md:266-268): rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'}, with the
+    joint prior in eq:weights_EM, against the dense matrix form."""
+    p = tiny(seed=seed)
+    L = p.L_high
+    x = p.x0.astype(np.float64)
+    pr = _joint_prior(L, seed, zeros)
+    d = dense_em(p.y, p.K, p.sigma, x, None, None, prior=pr)
+    r = oracle_mod.em_iter_joint(p.y, p.L_low, p.K, p.sigma, x, pr, project=False, tau=0.0)
+    assert abs(r.loglik - d["LL"]) <= 1e-12 * abs(d["LL"])
+    np.testing.assert_allclose(r.colsum, d["colsum"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(r.rho, d["colsum"] / d["colsum"].sum(), rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(r.rho1, r.rho.sum(1), rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(r.b.reshape(-1), d["b"], rtol=1e-12, atol=1e-13)
+    xs = np.linalg.solve(d["A"], d["b"]).reshape(x.shape)
+    np.testing.assert_allclose(r.x, xs, rtol=1e-11, atol=1e-12)
+    assert np.all(r.rho.reshape(-1)[pr.reshape(-1) == 0] == 0.0)   # zero prior mass stays zero
+
+
+def test_joint_with_product_prior_is_the_separable_iteration(oracle_mod):
+    """With rho = rho1 rho2^T the joint iteration is the separable one, and the marginals of the joint
+    update are the separable update (the latter is the marginal form of eq:rho_EM, reading R2)."""
+    p = synth.make_random(4, 2, 31, 0.45, 4, rho_zeros=1)
+    x = p.x0.astype(np.float64)
+    sep = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=True)
+    jnt = oracle_mod.em_iter_joint(p.y, p.L_low, p.K, p.sigma, x, np.outer(p.rho1_0, p.rho2_0), project=True)
+    assert abs(jnt.loglik - sep.loglik) <= 1e-12 * abs(sep.loglik)
+    np.testing.assert_allclose(jnt.x, sep.x, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(jnt.rho1, sep.rho1, rtol=1e-12, atol=1e-16)
+    np.testing.assert_allclose(jnt.rho2, sep.rho2, rtol=1e-12, atol=1e-16)
+
+
+def test_joint_em_monotone(oracle_mod):
+    """EM ascent with the joint prior update, projection off."""
+    p = synth.make_random(4, 2, 40, 0.4, 6)
+    x = p.x0.astype(np.float64)
+    rho = _joint_prior(p.L_high, 9, zeros=2)
+    lls = []
+    for _ in range(15):
+        r = oracle_mod.em_iter_joint(p.y, p.L_low, p.K, p.sigma, x, rho, project=False)
+        lls.append(r.loglik)
+        x, rho = r.x, r.rho
+    assert np.all(np.diff(lls) >= -1e-9 * np.abs(lls[:-1])), lls
