@@ -107,6 +107,16 @@ SRMRA_API int srmra_load(srmra_ctx* ctx, const float* y, const float* x0, const 
  * With world > 1 each iteration performs one NCCL all-reduce of the sufficient statistics. */
 SRMRA_API int srmra_em_iter(srmra_ctx* ctx, int32_t n_iters);
 
+/* NEXT-3: a joint (non-separable) shift prior rho[s1 L_high + s2] (host, float64, [L_high][L_high],
+ * >= 0, summing to 1 within 1e-6; copied) replaces (rho1, rho2) in eq:weights_EM, and the M-step
+ * becomes eq:rho_EM as written: rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'};
+ * srmra_get_estimate then reports its marginals.  GEMM and direct paths only (the FFT kernels
+ * accumulate the marginals, not every shift's posterior mass): UNSUPPORTED elsewhere.  A later
+ * srmra_load returns the context to a separable prior. */
+SRMRA_API int srmra_set_joint_rho(srmra_ctx* ctx, const double* rho);
+/* Copy the current joint prior [L_high][L_high] (STATE if none is set).  Synchronises. */
+SRMRA_API int srmra_get_joint_rho(srmra_ctx* ctx, double* out);
+
 /* Denoiser hook of Algorithm 2: called on the host for every projection
  * step with the device buffer of the estimate x (float64, [L_high][L_high], modified in place), the
  * schedule value sigma_t of eq:decaying_function and the context stream (cudaStream_t); work must be

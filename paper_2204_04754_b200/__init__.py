@@ -34,7 +34,8 @@ ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_it
                "srmra_get_loglik_trace", "srmra_get_stats", "srmra_get_obs_loglik", "srmra_local_stats",
                "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
-               "srmra_last_error", "srmra_run", "srmra_set_denoiser", "srmra_relative_error")
+               "srmra_last_error", "srmra_run", "srmra_set_denoiser", "srmra_relative_error",
+               "srmra_set_joint_rho", "srmra_get_joint_rho")
 
 
 class SrmraError(RuntimeError):
@@ -86,6 +87,8 @@ def _load():
         "srmra_run": (ctypes.c_int, [_ctxp, ctypes.c_int32, ctypes.c_double]),
         "srmra_set_denoiser": (ctypes.c_int, [_ctxp, DENOISER_FN, ctypes.c_void_p]),
         "srmra_relative_error": (ctypes.c_int, [_ctxp, _fp, _dp, _ip, _ip]),
+        "srmra_set_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
+        "srmra_get_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -163,6 +166,17 @@ def srmra_relative_error(ctx, x_true):
     s2 = ctypes.c_int32()
     _check(_lib.srmra_relative_error(ctx, _ptr(xt, _fp), ctypes.byref(err), ctypes.byref(s1), ctypes.byref(s2)), ctx)
     return err.value, (s1.value, s2.value)
+
+
+def srmra_set_joint_rho(ctx, rho):
+    r = np.ascontiguousarray(rho, dtype=np.float64)
+    _check(_lib.srmra_set_joint_rho(ctx, _ptr(r, _dp)), ctx)
+
+
+def srmra_get_joint_rho(ctx, L_high: int):
+    out = np.empty((L_high, L_high))
+    _check(_lib.srmra_get_joint_rho(ctx, _ptr(out, _dp)), ctx)
+    return out
 
 
 def snr(x_true, sigma: float) -> float:
@@ -288,6 +302,12 @@ class Context:
             return
         self._denoiser = DENOISER_FN(lambda x, L, sig, st, user: int(fn(x, L, sig, st)))
         srmra_set_denoiser(self.handle, self._denoiser)
+
+    def set_joint_rho(self, rho):
+        srmra_set_joint_rho(self.handle, rho)
+
+    def joint_rho(self):
+        return srmra_get_joint_rho(self.handle, self.L_high)
 
     def relative_error(self, x_true):
         return srmra_relative_error(self.handle, x_true)

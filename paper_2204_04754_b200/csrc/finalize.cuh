@@ -12,7 +12,8 @@ __device__ inline void finalize_body(const double* __restrict__ pack, int64_t of
                               int64_t off_m2, int64_t off_ll, int L, int K, double tau, int project,
                               double* __restrict__ x64, float* __restrict__ x32, double* __restrict__ rho,
                               double* __restrict__ xtmp, double* __restrict__ trace, int t, int trace_cap,
-                              int* __restrict__ flag, double* xs_dyn) {
+                              int* __restrict__ flag, double* xs_dyn, const double* __restrict__ colsum = nullptr,
+                              double* __restrict__ rhoj = nullptr) {
     __shared__ double red[32];
     __shared__ double cm[256];
     const int KK = K * K, L2 = L * L;
@@ -24,15 +25,27 @@ __device__ inline void finalize_body(const double* __restrict__ pack, int64_t of
     // so its marginal is exactly 0 (kept exact here; the frequency-domain path would otherwise leave
     // rounding noise there); other marginals are clamped at 0 and each axis is normalised by its own
     // total sum_i sum_s w (the eq:rho_EM denominator) so that sum rho = 1 to rounding.
+    if (rhoj) {
+        // joint prior (NEXT-3): eq:rho_EM as written, rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'}
+        // (zero prior mass gives w = 0 exactly); rho1 | rho2 become its marginals
+        if (tot > 0.0) {
+            for (int s = threadIdx.x; s < L2; s += blockDim.x) rhoj[s] = fmax(colsum[s], 0.0) / tot;
+            for (int k = threadIdx.x; k < L; k += blockDim.x) {
+                rho[k] = fmax(pack[off_m1 + k], 0.0) / tot;
+                rho[L + k] = fmax(pack[off_m2 + k], 0.0) / tot;
+            }
+        }
+        __syncthreads();
+    }
     double m1s = 0.0, m2s = 0.0;
-    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    for (int k = threadIdx.x; k < L && !rhoj; k += blockDim.x) {
         m1s += rho[k] == 0.0 ? 0.0 : fmax(pack[off_m1 + k], 0.0);
         m2s += rho[L + k] == 0.0 ? 0.0 : fmax(pack[off_m2 + k], 0.0);
     }
     m1s = block_sum(m1s, red);
     m2s = block_sum(m2s, red);
     __syncthreads();  // every thread has read rho_t above
-    if (tot > 0.0 && m1s > 0.0 && m2s > 0.0) {
+    if (!rhoj && tot > 0.0 && m1s > 0.0 && m2s > 0.0) {
         for (int k = threadIdx.x; k < L; k += blockDim.x) {
             rho[k] = rho[k] == 0.0 ? 0.0 : fmax(pack[off_m1 + k], 0.0) / m1s;
             rho[L + k] = rho[L + k] == 0.0 ? 0.0 : fmax(pack[off_m2 + k], 0.0) / m2s;

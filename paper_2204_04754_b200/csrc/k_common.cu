@@ -57,7 +57,8 @@ cudaError_t launch_init_obs(srmra_ctx* c, int64_t first, int64_t count) {
 //   beta_r = (E_min - E_r) / (2 sigma^2),  E_r = ||x_r||^2 = ||P R_s x||^2 for every s in class r.
 // E_r, E_min and beta are formed in float64; lr and beta are stored as float32 for the hot loop.
 __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ rho, int L, int K,
-                       double inv_2s2, float* __restrict__ f32, double* __restrict__ f64) {
+                       double inv_2s2, float* __restrict__ f32, double* __restrict__ f64,
+                       const double* __restrict__ rhoj, float* __restrict__ lrj) {
     __shared__ double red[32];
     __shared__ double Es[256];
     const int KK = K * K, Ll = L / K;
@@ -80,9 +81,12 @@ __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ 
     float* beta = f32 + 2 * L;
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
         const double a = rho[k], b = rho[L + k];
-        lr1[k] = a > 0.0 ? (float)log(a) : -INFINITY;
-        lr2[k] = b > 0.0 ? (float)log(b) : -INFINITY;
+        // joint prior (NEXT-3): the whole log prior sits in the per-shift table lrj
+        lr1[k] = rhoj ? 0.f : (a > 0.0 ? (float)log(a) : -INFINITY);
+        lr2[k] = rhoj ? 0.f : (b > 0.0 ? (float)log(b) : -INFINITY);
     }
+    if (rhoj)
+        for (int s = threadIdx.x; s < L * L; s += blockDim.x) lrj[s] = rhoj[s] > 0.0 ? (float)log(rhoj[s]) : -INFINITY;
     for (int r = threadIdx.x; r < KK; r += blockDim.x) {
         beta[r] = (float)((emin - Es[r]) * inv_2s2);
         f64[r] = Es[r];
@@ -96,7 +100,8 @@ cudaError_t launch_prep(srmra_ctx* c) {
         (e = cudaMemsetAsync(c->d_colsum, 0, sizeof(double) * c->L2, c->stream)) != cudaSuccess)
         return e;
     if ((e = cudaMemsetAsync(c->d_pack, 0, sizeof(double) * c->pk.total, c->stream)) != cudaSuccess) return e;
-    k_prep<<<1, 1024, 0, c->stream>>>(c->d_x64, c->d_rho, c->L, c->K, c->inv_2s2, c->par.f32, c->par.f64);
+    k_prep<<<1, 1024, 0, c->stream>>>(c->d_x64, c->d_rho, c->L, c->K, c->inv_2s2, c->par.f32, c->par.f64,
+                                      c->joint ? c->d_rhoj : nullptr, c->d_lrj);
     return cudaGetLastError();
 }
 
@@ -140,10 +145,10 @@ __global__ void k_finalize(const double* __restrict__ pack, int64_t off_cm, int6
                            int64_t off_m2, int64_t off_ll, int L, int K, double tau, int project,
                            double* __restrict__ x64, float* __restrict__ x32, double* __restrict__ rho,
                            double* __restrict__ xtmp, double* __restrict__ trace, int t, int trace_cap,
-                           int* __restrict__ flag) {
+                           int* __restrict__ flag, const double* __restrict__ colsum, double* __restrict__ rhoj) {
     extern __shared__ double xs_dyn[];
     finalize_body(pack, off_cm, off_m1, off_m2, off_ll, L, K, tau, project, x64, x32, rho, xtmp, trace, t,
-                  trace_cap, flag, xs_dyn);
+                  trace_cap, flag, xs_dyn, colsum, rhoj);
 }
 
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project) {
@@ -156,7 +161,8 @@ cudaError_t launch_finalize(srmra_ctx* c, int t, int project) {
     }
     k_finalize<<<1, 1024, sm, c->stream>>>(c->d_pack, c->pk.cmass, c->pk.m1, c->pk.m2, c->pk.ll, c->L, c->K,
                                           c->tau, project, c->d_x64, c->d_x32, c->d_rho, c->d_xtmp,
-                                          c->d_trace, t, c->opt.trace_cap, c->d_flag);
+                                          c->d_trace, t, c->opt.trace_cap, c->d_flag, c->d_colsum,
+                                          c->joint ? c->d_rhoj : nullptr);
     return cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ k_direct_em(const float* __restrict__ y, const double* __restrict__ ynorm, int64
             const float* __restrict__ x32, const float* __restrict__ par32,
             const double* __restrict__ par64, int L, int K, float inv_s2f, double inv_s2,
             double inv_2s2, double* __restrict__ b_out, double* __restrict__ colsum_out,
-            double* __restrict__ ll_out, double* __restrict__ llobs) {
+            double* __restrict__ ll_out, double* __restrict__ llobs, const float* __restrict__ lrj) {
     extern __shared__ float smem[];
     const int Ll = L / K, L2 = L * L, Ll2 = Ll * Ll, KK = K * K;
     float* xs = smem;           // [L2]
@@ -79,7 +79,8 @@ k_direct_em(const float* __restrict__ y, const double* __restrict__ ynorm, int64
         float vmax = -INFINITY;
         for (int s = tid; s < L2; s += blockDim.x) {
             const int s1 = s / L, s2 = s - s1 * L;
-            const float v = (sc[s] - sref) * inv_s2f + lr1[s1] + lr2[s2] + beta[(s1 % K) * K + (s2 % K)];
+            const float v = (sc[s] - sref) * inv_s2f + lr1[s1] + lr2[s2] + beta[(s1 % K) * K + (s2 % K)] +
+                            (lrj ? __ldg(lrj + s) : 0.f);  // joint log prior (NEXT-3)
             sc[s] = v;
             vmax = fmaxf(vmax, v);
         }
@@ -149,7 +150,8 @@ cudaError_t launch_direct_em(srmra_ctx* c) {
     if (grid > c->n_local) grid = c->n_local;
     k_direct_em<<<(unsigned)grid, kDirectThreads, smem, c->stream>>>(
         c->d_y, c->d_ynorm, c->n_local, c->d_x32, c->par.f32, c->par.f64, c->L, c->K, (float)c->inv_s2,
-        c->inv_s2, c->inv_2s2, c->d_pack + c->pk.b, c->d_colsum, c->d_pack + c->pk.ll, c->d_llobs);
+        c->inv_s2, c->inv_2s2, c->d_pack + c->pk.b, c->d_colsum, c->d_pack + c->pk.ll, c->d_llobs,
+        c->joint ? c->d_lrj : nullptr);
     return cudaGetLastError();
 }
 

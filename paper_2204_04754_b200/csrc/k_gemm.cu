@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
                                                       double inv_2s2, int64_t ldw, float* __restrict__ wthl,
                                                       double* __restrict__ llobs, double* __restrict__ ll_out,
                                                       const float* __restrict__ y, const double* __restrict__ x64,
-                                                      const double* __restrict__ rho) {
+                                                      const double* __restrict__ rho, const float* __restrict__ lrj,
+                                                      const double* __restrict__ rhoj) {
     constexpr int R = 8;
     __shared__ float sref_s[R], m_s[R], iz_s[R];
     __shared__ double lls[R];
@@ -318,8 +319,9 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
                 for (int u = 0; u < 4; ++u) {
                     int s1, s2;
                     j_to_s(4 * q + u, Ll, K, s1, s2);
-                    const float v = fmaf(sv[u] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K]);
                     const int sh = s2 + L * s1;
+                    const float v = fmaf(sv[u] - sref, inv_s2f, lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K] +
+                                                                  (lrj ? __ldg(lrj + sh) : 0.f));
                     if (v > vm) {  // online max / sum; argmax ties: the smaller shift index
                         z = (vm == -INFINITY ? 0.f : z * expf(vm - v)) + 1.f;
                         vm = v;
@@ -355,7 +357,8 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
                 sref_s[warp] = sref;
                 m_s[warp] = vm;
                 iz_s[warp] = 1.f / z;
-                const double lse = log(rho[a1]) + log(rho[L + a2]) - d * inv_2s2 + log((double)z);
+                const double lp = rhoj ? log(rhoj[am]) : log(rho[a1]) + log(rho[L + a2]);  // log prior at s*
+                const double lse = lp - d * inv_2s2 + log((double)z);
                 if (llobs) llobs[i] = lse;
                 lls[warp] = lse;
             }
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(256) k_gemm_softmax(const float* __restrict__ 
     for (int j = threadIdx.x; j < L2; j += blockDim.x) {
         int s1, s2;
         j_to_s(j, Ll, K, s1, s2);
-        const float bias = lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K];
+        const float bias = lr1[s1] + lr2[s2] + beta[(s1 % K) * K + s2 % K] + (lrj ? __ldg(lrj + s2 + L * s1) : 0.f);
         float hi[R], lo[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -507,7 +510,8 @@ cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1)
         if (e != cudaSuccess) return e;
         k_gemm_softmax<<<(unsigned)(c->g_ldw / 8), 256, 0, c->stream>>>(
             c->g_s, n, c->L, c->K, c->par.f32, c->par.f64, c->d_ynorm, (float)c->inv_s2, c->inv_s2, c->inv_2s2, c->g_ldw,
-            c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho);
+            c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho,
+            c->joint ? c->d_lrj : nullptr, c->joint ? c->d_rhoj : nullptr);
         e = launch_gemm_tma(c->g_wthl, c->g_wthl + (size_t)c->L2 * c->g_ldw, c->L2, c->g_ldw, c->g_ythl,
                             c->g_ythl + (size_t)(c->Ll2 + 16) * c->g_ldw, c->Ll2 + 16, c->g_ldw, c->Ll2 + 16, c->g_ldw,
                             0, c->Ll, c->g_z, c->Ll2 + 16, c->stream);
@@ -533,7 +537,8 @@ cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1)
     k_gemm3<true><<<dim3((c->L2 + BN - 1) / BN, (unsigned)((n + BM - 1) / BM)), THREADS, SMEM_BYTES, c->stream>>>(g1);
     k_gemm_softmax<<<(unsigned)(c->g_ldw / 8), 256, 0, c->stream>>>(
         c->g_s, n, c->L, c->K, c->par.f32, c->par.f64, c->d_ynorm, (float)c->inv_s2, c->inv_s2, c->inv_2s2, c->g_ldw,
-        c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho);
+        c->g_wthl, c->d_llobs, c->d_pack + c->pk.ll, c->d_y, c->d_x64, c->d_rho,
+            c->joint ? c->d_lrj : nullptr, c->joint ? c->d_rhoj : nullptr);
     GemmArgs g2{};
     g2.a_hi = c->g_wthl;
     g2.a_lo = c->g_wthl + (size_t)c->L2 * c->g_ldw;

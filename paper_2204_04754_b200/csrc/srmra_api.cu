@@ -148,6 +148,7 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemcpyAsync(c->d_x32, x0, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+    c->joint = false;  // (rho1, rho2): a separable prior again
     CK(cudaMemsetAsync(c->d_run, 0, 2 * sizeof(int), c->stream));
     CK(cudaMemsetAsync(c->d_rtol, 0, sizeof(double), c->stream));
     c->n_proj = 0;
@@ -611,6 +612,46 @@ int srmra_relative_error(srmra_ctx* c, const float* x_true, double* err_out, int
     return SRMRA_OK;
 }
 
+int srmra_set_joint_rho(srmra_ctx* c, const double* rho) {
+    if (!c || !rho) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (c->path != SRMRA_PATH_GEMM && c->path != SRMRA_PATH_DIRECT)
+        return fail(c, SRMRA_ERR_UNSUPPORTED, "joint shift prior: GEMM and direct paths only (init with path = gemm | direct)");
+    std::vector<double> r(rho, rho + c->L2);
+    double s = 0.0;
+    for (double v : r) {
+        if (!isfinite(v) || v < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "joint rho must be finite and >= 0");
+        s += v;
+    }
+    if (fabs(s - 1.0) > 1e-6) return fail(c, SRMRA_ERR_INVALID_ARG, "joint rho must sum to 1 (within 1e-6)");
+    std::vector<double> marg(2 * (size_t)c->L, 0.0);
+    for (int s1 = 0; s1 < c->L; ++s1)
+        for (int s2 = 0; s2 < c->L; ++s2) {
+            const double v = r[(size_t)s1 * c->L + s2] / s;
+            r[(size_t)s1 * c->L + s2] = v;
+            marg[s1] += v;
+            marg[c->L + s2] += v;
+        }
+    if (!c->d_rhoj) {
+        CK(cudaMalloc(&c->d_rhoj, sizeof(double) * c->L2));
+        CK(cudaMalloc(&c->d_lrj, sizeof(float) * c->L2));
+    }
+    CK(cudaMemcpyAsync(c->d_rhoj, r.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_rho, marg.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->joint = true;
+    return SRMRA_OK;
+}
+
+int srmra_get_joint_rho(srmra_ctx* c, double* out) {
+    if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (!c->joint) return fail(c, SRMRA_ERR_STATE, "no joint shift prior set (srmra_set_joint_rho)");
+    CK(cudaMemcpyAsync(out, c->d_rhoj, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
+
 int srmra_set_denoiser(srmra_ctx* c, srmra_denoiser_fn fn, void* user) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
@@ -792,6 +833,8 @@ void srmra_free(srmra_ctx* c) {
     if (c->d_iter) cudaFree(c->d_iter);
     if (c->d_run) cudaFree(c->d_run);
     if (c->d_emt) cudaFree(c->d_emt);
+    if (c->d_rhoj) cudaFree(c->d_rhoj);
+    if (c->d_lrj) cudaFree(c->d_lrj);
     if (c->d_rtol) cudaFree(c->d_rtol);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->copy_event) cudaEventDestroy(c->copy_event);

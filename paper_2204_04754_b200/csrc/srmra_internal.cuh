@@ -58,6 +58,9 @@ struct srmra_ctx {
     double* d_x64 = nullptr;  // [L2]
     float* d_x32 = nullptr;   // [L2]
     double* d_rho = nullptr;  // [2L] rho1 | rho2
+    double* d_rhoj = nullptr; // [L2] joint shift prior (NEXT-3, GEMM / direct paths), valid when `joint`
+    float* d_lrj = nullptr;   // [L2] its natural log (float32), the per-shift logit bias
+    bool joint = false;
     double* d_xtmp = nullptr; // [L2] finalize scratch
 
     // per-iteration
