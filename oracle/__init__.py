@@ -203,6 +203,36 @@ def relative_error(xhat, x):
     return float(best / np.linalg.norm(x)), arg
 
 
+# ---------------------------------------------------------------- NEXT-2: method of moments
+def empirical_moments(y):
+    """eq:empiric_MOM with D = 2: M1 = (1/N) sum_i y_i, M2 = (1/N) sum_i y_i y_i^T over
+    vec(y_i) (row-major, L_low^2 entries), float64."""
+    Y = _f32(y).reshape(y.shape[0], -1).astype(np.float64)
+    N = Y.shape[0]
+    return Y.sum(0) / N, (Y.T @ Y) / N
+
+
+def analytic_moments(x, rho1, rho2, K, sigma, rho=None):
+    """The first two moments of the model: M1 = P C_x rho, M2 = P C_x D_rho C_x^T P^T +
+    sigma^2 P P^T, written as sums over the shifts s: (P C_x)[:, s] = vec(P R_s x), so
+    M1 = sum_s rho[s] P R_s x and M2 = sum_s rho[s] (P R_s x)(P R_s x)^T + sigma^2 I (P P^T = I).
+    rho[s] = rho1[s1] rho2[s2] (D_rho = diag vec(rho1 rho2^T)), or a joint `rho`."""
+    x = _f64(x)
+    L = x.shape[0]
+    Ll = L // K
+    pr = np.outer(rho1, rho2) if rho is None else _f64(rho).reshape(L, L)
+    M1 = np.zeros(Ll * Ll)
+    M2 = sigma ** 2 * np.eye(Ll * Ll)
+    for s1 in range(L):
+        for s2 in range(L):
+            if pr[s1, s2] == 0.0:
+                continue
+            v = np.roll(x, (s1, s2), axis=(0, 1))[::K, ::K].reshape(-1)   # vec(P R_s x), Eq. (2)
+            M1 += pr[s1, s2] * v
+            M2 += pr[s1, s2] * np.outer(v, v)
+    return M1, M2
+
+
 def posterior(yi, L_low, K, sigma, x, rho1, rho2):
     """(w [L][L], log-likelihood term) of one observation."""
     lib = _load()

@@ -481,3 +481,52 @@ def test_joint_em_monotone(oracle_mod):
         lls.append(r.loglik)
         x, rho = r.x, r.rho
     assert np.all(np.diff(lls) >= -1e-9 * np.abs(lls[:-1])), lls
+
+
+# ---------------------------------------------------------------- NEXT-2: moments
+def test_empirical_moments_closed_forms(oracle_mod):
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((37, 4, 4)).astype(np.float32)
+    M1, M2 = oracle_mod.empirical_moments(y)
+    Y = y.reshape(37, -1).astype(np.float64)
+    np.testing.assert_allclose(M1, Y.mean(0), rtol=1e-14)
+    np.testing.assert_allclose(M2, M2.T, rtol=0, atol=0)                       # symmetric
+    assert np.linalg.eigvalsh(M2 - np.outer(M1, M1)).min() >= -1e-12           # covariance is PSD
+    assert abs(np.trace(M2) - (Y * Y).sum(1).mean()) <= 1e-12 * np.trace(M2)   # trace = mean ||y||^2
+    one = np.repeat(y[:1], 5, axis=0)                                           # identical observations
+    m1, m2 = oracle_mod.empirical_moments(one)
+    np.testing.assert_allclose(m2, np.outer(m1, m1), rtol=1e-14)
+
+
+def test_analytic_moments_definition_and_invariances(oracle_mod):
+    """M1 = P C_x rho from the BCCB columns (dense construction of PAPER.md:201-212), M2 symmetric PSD +
+    sigma^2 I; a point-mass prior gives M2 = v v^T + sigma^2 I with v = P R_s x."""
+    L, K, sigma = 8, 2, 0.3
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((L, L))
+    r1 = rng.dirichlet(np.ones(L)); r2 = rng.dirichlet(np.ones(L))
+    M1, M2 = oracle_mod.analytic_moments(x, r1, r2, K, sigma)
+    C = np.stack([R_matrix(L, (a, b)) @ x.reshape(-1) for a in range(L) for b in range(L)], axis=1)  # C_x
+    P = P_matrix(L, K)
+    rho = np.outer(r1, r2).reshape(-1)
+    np.testing.assert_allclose(M1, P @ C @ rho, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(M2, P @ C @ np.diag(rho) @ C.T @ P.T + sigma ** 2 * P @ P.T, rtol=1e-12, atol=1e-13)
+    e1 = np.zeros(L); e1[3] = 1.0
+    e2 = np.zeros(L); e2[5] = 1.0
+    m1, m2 = oracle_mod.analytic_moments(x, e1, e2, K, sigma)
+    v = np.roll(x, (3, 5), axis=(0, 1))[::K, ::K].reshape(-1)
+    np.testing.assert_allclose(m2, np.outer(v, v) + sigma ** 2 * np.eye(v.size), rtol=1e-13)
+    np.testing.assert_allclose(m1, v, rtol=1e-13)
+
+
+def test_moments_law_of_large_numbers(oracle_mod):
+    """eq:moments_convergence: the empirical moments of data drawn from the model with
+    known (x, rho, sigma) approach the analytic ones at the 1/sqrt(N) rate."""
+    errs = []
+    for N in (400, 6400):
+        p = synth.make_random(4, 2, N, 0.5, 21)
+        M1, M2 = oracle_mod.empirical_moments(p.y)
+        A1, A2 = oracle_mod.analytic_moments(p.x_true, p.rho1_true, p.rho2_true, p.K, p.sigma)
+        errs.append(np.abs(M2 - A2).max())
+        assert np.abs(M1 - A1).max() <= 6.0 / np.sqrt(N)
+    assert errs[1] < errs[0] / 2.0   # 16x the observations: ~4x smaller
