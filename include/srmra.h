@@ -151,6 +151,20 @@ SRMRA_API int srmra_relative_error(srmra_ctx* ctx, const float* x_true, double* 
                                    int32_t* s2_out);
 
 /*
+ * NEXT-2, the data term of the projected method of moments (Algorithm 1): the
+ * empirical moments of eq:empiric_MOM with D = 2 over ALL ranks' observations,
+ *     m1[a]          = (1/N) sum_i y_i[a],
+ *     m2[a L_low^2 + b] = (1/N) sum_i y_i[a] y_i[b],      a, b = p1 L_low + p2 (row-major y_i),
+ * N the global number of observations.  m1: caller-owned float64 [L_low^2]; m2: float64
+ * [L_low^2][L_low^2] (symmetric); either may be NULL (not both).  The sums run on the tensor cores
+ * (3xTF32 tcgen05 GEMM of the transposed observations with themselves, float32 accumulation in
+ * TMEM, float64 split-K combine) and are all-reduced over NCCL in float64 when world > 1.  Uses
+ * O(L_low^2 n_local) temporary device memory; independent of the EM state.  Synchronises.
+ * Errors: INVALID_ARG (both NULL), STATE (failed context / rejected load), CUDA, NCCL.
+ */
+SRMRA_API int srmra_moments(srmra_ctx* ctx, double* m1, double* m2);
+
+/*
  * Synchronise the stream and copy the current estimate to caller-owned host buffers (any may be
  * NULL): x_out float32 [L_high][L_high], rho1_out / rho2_out float64 [L_high], *loglik_out the
  * log-likelihood at the INPUT of the last iteration (NaN if none ran), *iters_done the number of

@@ -35,7 +35,7 @@ ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_it
                "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
                "srmra_last_error", "srmra_run", "srmra_set_denoiser", "srmra_relative_error",
-               "srmra_set_joint_rho", "srmra_get_joint_rho")
+               "srmra_set_joint_rho", "srmra_get_joint_rho", "srmra_moments")
 
 
 class SrmraError(RuntimeError):
@@ -89,6 +89,7 @@ def _load():
         "srmra_relative_error": (ctypes.c_int, [_ctxp, _fp, _dp, _ip, _ip]),
         "srmra_set_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
         "srmra_get_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
+        "srmra_moments": (ctypes.c_int, [_ctxp, _dp, _dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -177,6 +178,15 @@ def srmra_get_joint_rho(ctx, L_high: int):
     out = np.empty((L_high, L_high))
     _check(_lib.srmra_get_joint_rho(ctx, _ptr(out, _dp)), ctx)
     return out
+
+
+def srmra_moments(ctx, L_low: int):
+    """(M1 [L_low^2], M2 [L_low^2, L_low^2]): the empirical moments of eq:empiric_MOM."""
+    d = L_low * L_low
+    m1 = np.empty(d)
+    m2 = np.empty((d, d))
+    _check(_lib.srmra_moments(ctx, _ptr(m1, _dp), _ptr(m2, _dp)), ctx)
+    return m1, m2
 
 
 def snr(x_true, sigma: float) -> float:
@@ -285,6 +295,10 @@ class Context:
         return PATH_NAMES[srmra_get_path(self.handle)]
 
     def load(self, y, x0, rho1_0, rho2_0):
+        """Replace the observations (same n_local as at init: srmra_load takes no size) and theta."""
+        if np.asarray(y).size != self.n_local * self.L_low * self.L_low:
+            raise ValueError(f"srmra_load: y must hold n_local = {self.n_local} observations of "
+                             f"{self.L_low} x {self.L_low}")
         srmra_load(self.handle, y, x0, rho1_0, rho2_0)
 
     def em_iter(self, n_iters=1):
@@ -311,6 +325,9 @@ class Context:
 
     def relative_error(self, x_true):
         return srmra_relative_error(self.handle, x_true)
+
+    def moments(self):
+        return srmra_moments(self.handle, self.L_low)
 
     def get_estimate(self):
         return srmra_get_estimate(self.handle, self.L_high)

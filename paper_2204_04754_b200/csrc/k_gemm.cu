@@ -427,9 +427,6 @@ using namespace gemmk;
 bool gemm_tma_supported(int Ll);
 size_t gemm_circ_floats(int L, int K);
 cudaError_t launch_gemm_circ(const float* x32, int L, int K, float* cf, cudaStream_t st);
-cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
-                            const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
-                            float* c, int64_t ldc, cudaStream_t st);
 
 // TMA mainloop (k_gemm_tma.cu) for L_low in {32, 64}; SRMRA_GEMM_TMA=0 selects the cp.async mainloop
 static bool use_tma(const srmra_ctx* c) {

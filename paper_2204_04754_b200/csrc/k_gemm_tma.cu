@@ -32,6 +32,9 @@ struct TmaArgs {
     int circ, Ll;   // B from the circulant factor (GEMM1) with L_low = Ll, else dense
     float* c;
     int64_t ldc;
+    double* c64;    // non-null: float64 atomic accumulation into c64 (K split over blockIdx.z, kz k-tiles each)
+    int kz;
+    int sym;        // A == B: only the tiles n0 >= m0 are computed (C symmetric)
 };
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -61,6 +64,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __shared__ uint32_t tmem_slot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    if (g.sym && n0 < m0) return;  // the mirror tile holds the transpose
+    const int kt0 = blockIdx.z * g.kz, nloc = min(g.nk - kt0, g.kz);
 
     if (warp == 1) tc::tmem_alloc<BN * KSPLIT>(&tmem_slot);
     if (tid == 0) {
@@ -75,13 +80,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     tc::fence_after();
     const uint32_t taddr = tmem_slot;
-    const int kper = (g.nk + KSPLIT - 1) / KSPLIT;
+    const int kper = (nloc + KSPLIT - 1) / KSPLIT;
 
     if (warp == 0 && lane == 0) {
         // ---- producer: TMA boxes of tile kt into stage kt % STAGES
-        for (int kt = 0; kt < g.nk; ++kt) {
-            const int st = kt % STAGES;
-            if (kt >= STAGES) tc::mbar_wait(tc::smem_u32(&empty[st]), ((kt / STAGES) - 1) & 1);
+        for (int lt = 0; lt < nloc; ++lt) {
+            const int kt = kt0 + lt, st = lt % STAGES;
+            if (lt >= STAGES) tc::mbar_wait(tc::smem_u32(&empty[st]), ((lt / STAGES) - 1) & 1);
             const uint32_t sb = tc::smem_u32(base + st * STAGE_BYTES), fb = tc::smem_u32(&full[st]);
             mbar_expect_tx(fb, STAGE_BYTES);
             tma_2d(sb, &ta_hi, kt * BK, m0, fb);
@@ -105,19 +110,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer: 3 x 4 tcgen05.mma kind::tf32 per k-tile into split-K block kt / kper
-        for (int kt = 0; kt < g.nk; ++kt) {
-            const int st = kt % STAGES;
-            tc::mbar_wait(tc::smem_u32(&full[st]), (kt / STAGES) & 1);
+        for (int lt = 0; lt < nloc; ++lt) {
+            const int st = lt % STAGES;
+            tc::mbar_wait(tc::smem_u32(&full[st]), (lt / STAGES) & 1);
             tc::fence_after();
             const uint32_t sa = tc::smem_u32(base + st * STAGE_BYTES);
-            const int part = kt / kper;
+            const int part = lt / kper;
             const uint32_t td = taddr + (uint32_t)(part * BN);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
                 const uint32_t o = kk * 32;  // 8 tf32 = 32 B along K inside the 128-B swizzle row
                 const uint64_t ah = sw128_desc(sa + o), al = sw128_desc(sa + TILE_BYTES + o);
                 const uint64_t bh = sw128_desc(sa + 2 * TILE_BYTES + o), bl = sw128_desc(sa + 3 * TILE_BYTES + o);
-                tc::mma_tf32(td, ah, bh, IDESC, ((kt - part * kper) | kk) != 0);
+                tc::mma_tf32(td, ah, bh, IDESC, ((lt - part * kper) | kk) != 0);
                 tc::mma_tf32(td, ah, bl, IDESC, 1u);
                 tc::mma_tf32(td, al, bh, IDESC, 1u);
             }
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::fence_after();
         const int q4 = warp & 3;
         const int row = m0 + q4 * 32 + lane;
-        const int nparts = (g.nk + kper - 1) / kper;
+        const int nparts = (nloc + kper - 1) / kper;
 #pragma unroll 1
         for (int cc = 0; cc < BN; cc += 16) {
             float v[16];
@@ -142,7 +147,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) acc[j] += (double)v[j];
             }
-            if (row < g.M) {
+            if (row < g.M && g.c64) {
+                double* dst = g.c64 + (size_t)row * g.ldc + n0 + cc;
+                for (int j = 0; j < 16; ++j)
+                    if (n0 + cc + j < g.N) atomicAdd(dst + j, acc[j]);
+            } else if (row < g.M) {
                 float* dst = g.c + (size_t)row * g.ldc + n0 + cc;
                 if (n0 + cc + 16 <= g.N) {
 #pragma unroll
@@ -223,10 +232,13 @@ cudaError_t launch_gemm_circ(const float* x32, int L, int K, float* cf, cudaStre
     return cudaGetLastError();
 }
 
-// C[M][N] = A B^T (both K-major, hi / lo tf32 planes), 3xTF32 with float64 split-K combine
+// C[M][N] = A B^T (both K-major, hi / lo tf32 planes), 3xTF32 with float64 split-K combine.
+// c64 != NULL: C is accumulated in float64 with atomics into c64 (zeroed by the caller), the K range split
+// over blockIdx.z in slices of kz k-tiles (shorter float32 TMEM chains, more CTAs); sym: A == B, only the
+// tiles with n0 >= m0 are computed.
 cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
                             const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
-                            float* c, int64_t ldc, cudaStream_t st) {
+                            float* c, int64_t ldc, cudaStream_t st, double* c64, int kz, int sym) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -246,7 +258,10 @@ cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int
     g.Ll = Ll;
     g.c = c;
     g.ldc = ldc;
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    g.c64 = c64;
+    g.kz = (c64 && kz > 0) ? kz : g.nk;
+    g.sym = sym;
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)((g.nk + g.kz - 1) / g.kz));
     k_gemm_tma<<<grid, THREADS, SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, g);
     return cudaGetLastError();
 }

@@ -361,6 +361,18 @@ int sync_iters(srmra_ctx* c) {
 }  // namespace
 
 // ==================================================================== ABI
+namespace srmra {
+// NCCL sum of a device float64 buffer over all ranks, on the context stream (no-op for world 1);
+// the moments call (k_moments.cu) uses it for its raw sums.
+int allreduce_doubles(srmra_ctx* c, double* buf, size_t n) {
+    if (c->opt.world <= 1 || n == 0) return SRMRA_OK;
+    NcclApi& api = nccl();
+    ncclResult_t r = api.AllReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
+    if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    return SRMRA_OK;
+}
+}  // namespace srmra
+
 extern "C" {
 
 void srmra_default_options(srmra_options* o) {
@@ -650,6 +662,17 @@ int srmra_get_joint_rho(srmra_ctx* c, double* out) {
     CK(cudaMemcpyAsync(out, c->d_rhoj, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SRMRA_OK;
+}
+
+int srmra_moments(srmra_ctx* c, double* m1, double* m2) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no observations loaded (the last srmra_load was rejected)");
+    if (!m1 && !m2) return fail(c, SRMRA_ERR_INVALID_ARG, "both outputs NULL");
+    std::string err;
+    const int rc = moments(c, m1, m2, err);
+    if (rc == SRMRA_ERR_CUDA) return fail(c, rc, err);
+    return rc;
 }
 
 int srmra_set_denoiser(srmra_ctx* c, srmra_denoiser_fn fn, void* user) {

@@ -130,6 +130,12 @@ cudaError_t launch_pack(srmra_ctx* c);          // colsum (+ Bhat) -> packed b |
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
 cudaError_t launch_x32_from_x64(srmra_ctx* c);   // after a denoiser hook changed x
 cudaError_t launch_shift_corr(srmra_ctx* c, const double* xref_dev, double* corr_dev);  // NEXT-4
+int moments(srmra_ctx* c, double* m1, double* m2, std::string& err);  // NEXT-2 (k_moments.cu)
+// TMA 3xTF32 tcgen05 GEMM C = A B^T (k_gemm_tma.cu); c64 / kz / sym: see there
+cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
+                            const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
+                            float* c, int64_t ldc, cudaStream_t st, double* c64 = nullptr, int kz = 0, int sym = 0);
+int allreduce_doubles(srmra_ctx* c, double* buf, size_t n);           // NCCL sum, no-op for world 1
 // ---------------------------------------------------------------- path kernels
 cudaError_t launch_direct_em(srmra_ctx* c);     // k_direct.cu
 bool direct_supported(int L, int Ll, int K);
