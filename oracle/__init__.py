@@ -233,6 +233,56 @@ def analytic_moments(x, rho1, rho2, K, sigma, rho=None):
     return M1, M2
 
 
+def mom_lambda(L_high: int, sigma: float) -> float:
+    """lambda = 1 / (L_high^2 (1 + sigma^2)) of eq:LS_SR."""
+    return 1.0 / (L_high * L_high * (1.0 + sigma * sigma))
+
+
+def shifted_templates(x, K):
+    """V [L_high^2][L_low^2]: row s = s1 L_high + s2 is vec(P R_s x) (Eq. (2)), i.e. the
+    columns of P C_x."""
+    x = _f64(x)
+    L = x.shape[0]
+    V = np.empty((L * L, (L // K) ** 2))
+    for s1 in range(L):
+        for s2 in range(L):
+            V[s1 * L + s2] = np.roll(x, (s1, s2), axis=(0, 1))[::K, ::K].reshape(-1)
+    return V
+
+
+def mom_objective(x, rho1, rho2, K, sigma, M1hat, M2hat):
+    """The least-squares moment objective eq:LS_SR at theta = (x, rho1 rho2^T):
+        f = || P C_x D_rho C_x^T P^T + sigma^2 I - M2hat ||_F^2 + lambda || P C_x rho - M1hat ||_2^2,
+    lambda = mom_lambda(L_high, sigma), and its gradient (derived here, not printed in the paper; pinned by
+    finite differences): with V = shifted_templates(x), E = M2(theta) - M2hat, e = M1(theta) - M1hat,
+        df/drho[s] = 2 v_s^T E v_s + 2 lambda e^T v_s                      (joint rho, s = s1 L + s2)
+        df/dx      = sum_s rho[s] R_s^T P^T (4 E v_s + 2 lambda e)         (E symmetric)
+        df/drho1[s1] = sum_s2 df/drho[s1, s2] rho2[s2],  df/drho2[s2] = sum_s1 df/drho[s1, s2] rho1[s1].
+    Returns (f, grad_x [L][L], grad_rho1 [L], grad_rho2 [L], grad_rho [L][L])."""
+    x = _f64(x)
+    L = x.shape[0]
+    Ll = L // K
+    rho = np.outer(_f64(rho1), _f64(rho2))
+    r = rho.reshape(-1)
+    V = shifted_templates(x, K)
+    M1 = V.T @ r
+    M2 = V.T @ (r[:, None] * V) + sigma ** 2 * np.eye(Ll * Ll)
+    E = M2 - _f64(M2hat)
+    e = M1 - _f64(M1hat).reshape(-1)
+    lam = mom_lambda(L, sigma)
+    f = float((E * E).sum() + lam * (e * e).sum())
+    G = V @ E                                                   # row s: E v_s
+    grho = (2.0 * (G * V).sum(1) + 2.0 * lam * (V @ e)).reshape(L, L)
+    gx = np.zeros((L, L))
+    for s1 in range(L):
+        for s2 in range(L):
+            z = r[s1 * L + s2] * (4.0 * G[s1 * L + s2] + 2.0 * lam * e)
+            up = np.zeros((L, L))
+            up[::K, ::K] = z.reshape(Ll, Ll)                    # P^T z
+            gx += np.roll(up, (-s1, -s2), axis=(0, 1))           # R_s^T = R_{-s}
+    return f, gx, grho @ _f64(rho2), grho.T @ _f64(rho1), grho
+
+
 def posterior(yi, L_low, K, sigma, x, rho1, rho2):
     """(w [L][L], log-likelihood term) of one observation."""
     lib = _load()

@@ -530,3 +530,60 @@ def test_moments_law_of_large_numbers(oracle_mod):
         errs.append(np.abs(M2 - A2).max())
         assert np.abs(M1 - A1).max() <= 6.0 / np.sqrt(N)
     assert errs[1] < errs[0] / 2.0   # 16x the observations: ~4x smaller
+
+
+# ---------------------------------------------------------------- NEXT-2: the moment objective eq:LS_SR
+@pytest.mark.parametrize("L,K", [(8, 2), (6, 3)])
+def test_mom_gradient_matches_finite_differences(oracle_mod, L, K):
+    """The oracle's gradient of eq:LS_SR (derived, not printed in the paper) against central differences of
+    its objective in every coordinate of x, rho1, rho2 (the objective is a polynomial: h = 1e-5 leaves
+    O(h^2) truncation)."""
+    rng = np.random.default_rng(L * 10 + K)
+    Ll, sigma, h = L // K, 0.4, 1e-5
+    x = rng.standard_normal((L, L))
+    r1, r2 = rng.dirichlet(np.ones(L)), rng.dirichlet(np.ones(L))
+    Y = rng.standard_normal((40, Ll * Ll))
+    M1, M2 = Y.mean(0), Y.T @ Y / 40
+    f, gx, g1, g2, _ = oracle_mod.mom_objective(x, r1, r2, K, sigma, M1, M2)
+
+    def fd(fun, a):
+        out = np.zeros_like(a)
+        for idx in np.ndindex(a.shape):
+            ap, am = a.copy(), a.copy()
+            ap[idx] += h
+            am[idx] -= h
+            out[idx] = (fun(ap) - fun(am)) / (2 * h)
+        return out
+    nx = fd(lambda a: oracle_mod.mom_objective(a, r1, r2, K, sigma, M1, M2)[0], x)
+    n1 = fd(lambda a: oracle_mod.mom_objective(x, a, r2, K, sigma, M1, M2)[0], r1)
+    n2 = fd(lambda a: oracle_mod.mom_objective(x, r1, a, K, sigma, M1, M2)[0], r2)
+    for g, n in ((gx, nx), (g1, n1), (g2, n2)):
+        np.testing.assert_allclose(g, n, rtol=1e-6, atol=1e-6 * np.abs(n).max())
+
+
+def test_mom_objective_definition_zero_and_invariance(oracle_mod):
+    """f is the squared distance of PAPER.md:215-218 with lambda = 1/(L^2(1+sigma^2)): it
+    equals the dense-matrix value, vanishes with zero gradient at the truth given the perfect moments
+    (N -> infinity, as in the paper's Fig. 2 experiment), and is invariant under x -> R_u x,
+    rho -> R_{-u} rho (the translation symmetry of the model)."""
+    L, K, sigma = 8, 2, 0.25
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((L, L))
+    r1, r2 = rng.dirichlet(np.ones(L)), rng.dirichlet(np.ones(L))
+    assert oracle_mod.mom_lambda(64, 0.5) == 1.0 / (64 * 64 * 1.25)
+    A1, A2 = oracle_mod.analytic_moments(x, r1, r2, K, sigma)
+    f, gx, g1, g2, grho = oracle_mod.mom_objective(x, r1, r2, K, sigma, A1, A2)
+    assert abs(f) <= 1e-24 and np.abs(gx).max() <= 1e-12 and np.abs(grho).max() <= 1e-12
+    Y = rng.standard_normal((30, 16))
+    M1, M2 = Y.mean(0), Y.T @ Y / 30
+    C = np.stack([R_matrix(L, (a, b)) @ x.reshape(-1) for a in range(L) for b in range(L)], axis=1)
+    P = P_matrix(L, K)
+    rho = np.outer(r1, r2).reshape(-1)
+    dense = (np.linalg.norm(P @ C @ np.diag(rho) @ C.T @ P.T + sigma ** 2 * P @ P.T - M2) ** 2
+             + np.linalg.norm(P @ C @ rho - M1) ** 2 / (L * L * (1 + sigma ** 2)))
+    f = oracle_mod.mom_objective(x, r1, r2, K, sigma, M1, M2)[0]
+    np.testing.assert_allclose(f, dense, rtol=1e-12)
+    u = (3, 5)
+    fs = oracle_mod.mom_objective(np.roll(x, u, axis=(0, 1)), np.roll(r1, -u[0]), np.roll(r2, -u[1]), K, sigma,
+                                  M1, M2)[0]
+    np.testing.assert_allclose(fs, f, rtol=1e-12)
