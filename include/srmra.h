@@ -165,6 +165,44 @@ SRMRA_API int srmra_relative_error(srmra_ctx* ctx, const float* x_true, double* 
 SRMRA_API int srmra_moments(srmra_ctx* ctx, double* m1, double* m2);
 
 /*
+ * NEXT-2, Algorithm 1 (projected method of moments).  L_low <= 64 (else UNSUPPORTED).
+ *
+ * srmra_mom_set_moments: the data term of eq:LS_SR.  m1 / m2 both NULL: the empirical moments of the
+ * loaded observations (srmra_moments' computation, kept on the device); both non-NULL: caller moments,
+ * host float64 m1 [L_low^2], m2 [L_low^2][L_low^2] (e.g. the perfect moments of the paper's Fig. 2
+ * experiment), copied; the symmetric part of m2 is used.  Transforms them once to the Fourier domain
+ * (F M2 F^H, F the L_low x L_low 2-D DFT; O(L_low^5) float64).  Allocates 2 L_low^4 complex doubles.
+ * Errors: INVALID_ARG (exactly one NULL, non-finite), STATE (rejected load with NULL moments),
+ * UNSUPPORTED, CUDA, NCCL.  Synchronises.
+ */
+SRMRA_API int srmra_mom_set_moments(srmra_ctx* ctx, const double* m1, const double* m2);
+
+/*
+ * The objective eq:LS_SR at theta = (x, rho1 rho2^T), sigma the context's:
+ *     f = || P C_x D_rho C_x^T P^T + sigma^2 I - M2 ||_F^2 + lambda || P C_x rho - M1 ||_2^2,
+ *     lambda = 1 / (L_high^2 (1 + sigma^2)),
+ * and its gradient with respect to x [L_high][L_high], rho1 [L_high], rho2 [L_high] (float64, host;
+ * outputs may be NULL).  Evaluated in the Fourier domain without forming C_x:
+ * O(L_high^4) float64 work.  theta is not checked (any real values).  Errors: INVALID_ARG (NULL theta),
+ * STATE (no moments set), CUDA.  Synchronises.
+ */
+SRMRA_API int srmra_mom_objective(srmra_ctx* ctx, const double* x, const double* rho1, const double* rho2,
+                                  double* f, double* grad_x, double* grad_rho1, double* grad_rho2);
+
+/*
+ * Algorithm 1 from the context's current estimate (x, rho1, rho2): up to max_steps L-BFGS steps
+ * (memory 10, Armijo backtracking) on eq:LS_SR over (x, a1, a2), rho_j = softmax(a_j); after every F-th
+ * step (F = 0: never) the projection x <- D(x, sigma_j) (built-in stand-in or the srmra_set_denoiser
+ * hook; sigma_j = 2^(-(j-1)/10), eq:decaying_function) and a memory reset.  Stops early when
+ * ||grad||_inf <= gtol or the line search finds no decrease.  The result becomes the context's estimate
+ * (srmra_get_estimate; EM iterations may follow; a joint prior is dropped); *f_out the final objective,
+ * *steps_out the steps taken (either may be NULL).  Errors: INVALID_ARG (max_steps < 0, F < 0,
+ * gtol < 0 or NaN), STATE (no moments set), NUMERIC (non-finite objective / hook failure), CUDA.
+ */
+SRMRA_API int srmra_mom_run(srmra_ctx* ctx, int32_t max_steps, int32_t F, double gtol, double* f_out,
+                            int32_t* steps_out);
+
+/*
  * Synchronise the stream and copy the current estimate to caller-owned host buffers (any may be
  * NULL): x_out float32 [L_high][L_high], rho1_out / rho2_out float64 [L_high], *loglik_out the
  * log-likelihood at the INPUT of the last iteration (NaN if none ran), *iters_done the number of

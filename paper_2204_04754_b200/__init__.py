@@ -35,7 +35,8 @@ ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_it
                "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
                "srmra_last_error", "srmra_run", "srmra_set_denoiser", "srmra_relative_error",
-               "srmra_set_joint_rho", "srmra_get_joint_rho", "srmra_moments")
+               "srmra_set_joint_rho", "srmra_get_joint_rho", "srmra_moments",
+               "srmra_mom_set_moments", "srmra_mom_objective", "srmra_mom_run")
 
 
 class SrmraError(RuntimeError):
@@ -90,6 +91,9 @@ def _load():
         "srmra_set_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
         "srmra_get_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
         "srmra_moments": (ctypes.c_int, [_ctxp, _dp, _dp]),
+        "srmra_mom_set_moments": (ctypes.c_int, [_ctxp, _dp, _dp]),
+        "srmra_mom_objective": (ctypes.c_int, [_ctxp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+        "srmra_mom_run": (ctypes.c_int, [_ctxp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _dp, _ip]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -187,6 +191,41 @@ def srmra_moments(ctx, L_low: int):
     m2 = np.empty((d, d))
     _check(_lib.srmra_moments(ctx, _ptr(m1, _dp), _ptr(m2, _dp)), ctx)
     return m1, m2
+
+
+def srmra_mom_set_moments(ctx, m1=None, m2=None):
+    """Data term of eq:LS_SR: the loaded observations' empirical moments (None, None) or given ones."""
+    if (m1 is None) != (m2 is None):
+        raise ValueError("m1 and m2: both or neither")
+    if m1 is None:
+        _check(_lib.srmra_mom_set_moments(ctx, None, None), ctx)
+    else:
+        a = np.ascontiguousarray(m1, dtype=np.float64)
+        b = np.ascontiguousarray(m2, dtype=np.float64)
+        _check(_lib.srmra_mom_set_moments(ctx, _ptr(a, _dp), _ptr(b, _dp)), ctx)
+
+
+def srmra_mom_objective(ctx, x, rho1, rho2):
+    """(f, grad_x, grad_rho1, grad_rho2) of eq:LS_SR."""
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    r1 = np.ascontiguousarray(rho1, dtype=np.float64)
+    r2 = np.ascontiguousarray(rho2, dtype=np.float64)
+    L = r1.shape[0]
+    f = ctypes.c_double()
+    gx = np.empty((L, L))
+    g1 = np.empty(L)
+    g2 = np.empty(L)
+    _check(_lib.srmra_mom_objective(ctx, _ptr(xx, _dp), _ptr(r1, _dp), _ptr(r2, _dp), ctypes.byref(f),
+                                    _ptr(gx, _dp), _ptr(g1, _dp), _ptr(g2, _dp)), ctx)
+    return f.value, gx, g1, g2
+
+
+def srmra_mom_run(ctx, max_steps: int, F: int = 5, gtol: float = 0.0):
+    """Algorithm 1 from the context's estimate: (final objective, steps taken)."""
+    f = ctypes.c_double()
+    st = ctypes.c_int32()
+    _check(_lib.srmra_mom_run(ctx, int(max_steps), int(F), float(gtol), ctypes.byref(f), ctypes.byref(st)), ctx)
+    return f.value, st.value
 
 
 def snr(x_true, sigma: float) -> float:
@@ -328,6 +367,15 @@ class Context:
 
     def moments(self):
         return srmra_moments(self.handle, self.L_low)
+
+    def mom_set_moments(self, m1=None, m2=None):
+        srmra_mom_set_moments(self.handle, m1, m2)
+
+    def mom_objective(self, x, rho1, rho2):
+        return srmra_mom_objective(self.handle, x, rho1, rho2)
+
+    def mom_run(self, max_steps, F=5, gtol=0.0):
+        return srmra_mom_run(self.handle, max_steps, F, gtol)
 
     def get_estimate(self):
         return srmra_get_estimate(self.handle, self.L_high)

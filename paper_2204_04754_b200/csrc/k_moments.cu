@@ -7,7 +7,7 @@
 // With world > 1 the float64 sums are all-reduced over NCCL before the division by the global N.
 #include <math.h>
 
-#include <vector>
+#include <algorithm>
 
 #include "srmra_internal.cuh"
 #include "tcgen05.cuh"
@@ -65,16 +65,20 @@ __global__ void k_mom_out(const double* __restrict__ C, int ldc, int Ll2, double
 
 using namespace momk;
 
-// Sums over this rank's observations, all-reduced, divided by the global N (see srmra.h).
-int moments(srmra_ctx* c, double* m1, double* m2, std::string& err) {
+__global__ void k_mom_scale(double* __restrict__ out, int64_t total, double inv) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] *= inv;
+}
+
+// The moments over all ranks on the device: out[0 .. Ll2) = M1, out[Ll2 ..) = M2 (row-major), float64.
+// Enqueued on the context stream (temporaries stream-ordered); returns a CUDA or NCCL error code.
+int moments_dev(srmra_ctx* c, double* out, std::string& err) {
     const int Ll2 = c->Ll2, R = (Ll2 + 1 + 15) / 16 * 16;  // + the all-ones row; 16-aligned rows
-    const int64_t n = c->n_local, ldw = ((n + 7) / 8) * 8 > 0 ? ((n + 7) / 8) * 8 : 8;
+    const int64_t n = c->n_local, ldw = std::max<int64_t>(8, (n + 7) / 8 * 8);
     const size_t nout = (size_t)Ll2 + (size_t)Ll2 * Ll2;
     float* yt = nullptr;
     double* C = nullptr;
-    double* out = nullptr;
-    cudaError_t e = cudaMallocAsync(&out, sizeof(double) * nout, c->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(out, 0, sizeof(double) * nout, c->stream);
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * nout, c->stream);
     if (e == cudaSuccess && n > 0) {
         e = cudaMallocAsync(&yt, sizeof(float) * 2 * (size_t)R * ldw, c->stream);
         if (e == cudaSuccess) e = cudaMallocAsync(&C, sizeof(double) * (size_t)R * R, c->stream);
@@ -90,31 +94,52 @@ int moments(srmra_ctx* c, double* m1, double* m2, std::string& err) {
             e = launch_gemm_tma(yt, yt + (size_t)R * ldw, R, ldw, yt, yt + (size_t)R * ldw, R, ldw, R, ldw, 0, c->Ll,
                                 nullptr, R, c->stream, C, MOM_KZ, 1);
         if (e == cudaSuccess) {
-            const int64_t total = (int64_t)nout;
-            k_mom_out<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, c->stream>>>(C, R, Ll2, out);
+            k_mom_out<<<(unsigned)std::min<int64_t>(((int64_t)nout + 255) / 256, 4096), 256, 0, c->stream>>>(C, R, Ll2, out);
             e = cudaGetLastError();
         }
     }
-    int rc = SRMRA_OK;
-    if (e == cudaSuccess) rc = allreduce_doubles(c, out, nout);
-    std::vector<double> h(nout);
-    if (e == cudaSuccess && rc == SRMRA_OK) e = cudaMemcpyAsync(h.data(), out, sizeof(double) * nout, cudaMemcpyDeviceToHost, c->stream);
     if (yt) cudaFreeAsync(yt, c->stream);
     if (C) cudaFreeAsync(C, c->stream);
-    if (out) cudaFreeAsync(out, c->stream);
-    const cudaError_t es = cudaStreamSynchronize(c->stream);
-    if (e == cudaSuccess) e = es;
+    if (e != cudaSuccess) {
+        err = std::string("moments: ") + cudaGetErrorString(e);
+        return SRMRA_ERR_CUDA;
+    }
+    const int rc = allreduce_doubles(c, out, nout);
+    if (rc != SRMRA_OK) return rc;
+    const double inv = c->n_global > 0 ? 1.0 / (double)c->n_global : 0.0;
+    k_mom_scale<<<(unsigned)std::min<int64_t>(((int64_t)nout + 255) / 256, 4096), 256, 0, c->stream>>>(out, (int64_t)nout, inv);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        err = std::string("moments: ") + cudaGetErrorString(e);
+        return SRMRA_ERR_CUDA;
+    }
+    return SRMRA_OK;
+}
+
+// srmra_moments: the moments copied to caller-owned host buffers (see srmra.h).
+int moments(srmra_ctx* c, double* m1, double* m2, std::string& err) {
+    const int Ll2 = c->Ll2;
+    const size_t nout = (size_t)Ll2 + (size_t)Ll2 * Ll2;
+    double* out = nullptr;
+    cudaError_t e = cudaMallocAsync(&out, sizeof(double) * nout, c->stream);
     if (e != cudaSuccess) {
         err = std::string("srmra_moments: ") + cudaGetErrorString(e);
         return SRMRA_ERR_CUDA;
     }
-    if (rc != SRMRA_OK) return rc;
-    const double inv = c->n_global > 0 ? 1.0 / (double)c->n_global : 0.0;
-    if (m1)
-        for (int a = 0; a < Ll2; ++a) m1[a] = h[a] * inv;
-    if (m2)
-        for (size_t f = 0; f < (size_t)Ll2 * Ll2; ++f) m2[f] = h[Ll2 + f] * inv;
-    return SRMRA_OK;
+    int rc = moments_dev(c, out, err);
+    if (rc == SRMRA_OK) {
+        if (m1) e = cudaMemcpyAsync(m1, out, sizeof(double) * Ll2, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess && m2)
+            e = cudaMemcpyAsync(m2, out + Ll2, sizeof(double) * Ll2 * Ll2, cudaMemcpyDeviceToHost, c->stream);
+    }
+    cudaFreeAsync(out, c->stream);
+    const cudaError_t es = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = es;
+    if (rc == SRMRA_OK && e != cudaSuccess) {
+        err = std::string("srmra_moments: ") + cudaGetErrorString(e);
+        rc = SRMRA_ERR_CUDA;
+    }
+    return rc;
 }
 
 }  // namespace srmra

@@ -675,6 +675,55 @@ int srmra_moments(srmra_ctx* c, double* m1, double* m2) {
     return rc;
 }
 
+static int mom_fail(srmra_ctx* c, int rc, const std::string& err) {
+    if (rc == SRMRA_OK || rc == SRMRA_ERR_NCCL) return rc;  // NCCL failures were recorded by allreduce_doubles
+    return fail(c, rc, err);
+}
+
+int srmra_mom_set_moments(srmra_ctx* c, const double* m1, const double* m2) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if ((m1 == nullptr) != (m2 == nullptr)) return fail(c, SRMRA_ERR_INVALID_ARG, "m1 and m2: both or neither");
+    if (!m1 && c->needs_load) return fail(c, SRMRA_ERR_STATE, "no observations loaded (the last srmra_load was rejected)");
+    if (!mom_supported(c)) return fail(c, SRMRA_ERR_UNSUPPORTED, "moment objective compiled for L_low <= 64");
+    if (m1) {
+        for (int a = 0; a < c->Ll2; ++a)
+            if (!isfinite(m1[a])) return fail(c, SRMRA_ERR_INVALID_ARG, "m1 not finite");
+        for (size_t a = 0; a < (size_t)c->Ll2 * c->Ll2; ++a)
+            if (!isfinite(m2[a])) return fail(c, SRMRA_ERR_INVALID_ARG, "m2 not finite");
+    }
+    std::string err;
+    return mom_fail(c, mom_set(c, m1, m2, err), err);
+}
+
+int srmra_mom_objective(srmra_ctx* c, const double* x, const double* rho1, const double* rho2, double* f,
+                        double* grad_x, double* grad_rho1, double* grad_rho2) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (!x || !rho1 || !rho2) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL theta");
+    if (!mom_ready(c)) return fail(c, SRMRA_ERR_STATE, "no moments set (srmra_mom_set_moments)");
+    std::string err;
+    return mom_fail(c, mom_objective(c, x, rho1, rho2, f, grad_x, grad_rho1, grad_rho2, err), err);
+}
+
+int srmra_mom_run(srmra_ctx* c, int32_t max_steps, int32_t F, double gtol, double* f_out, int32_t* steps_out) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (max_steps < 0 || F < 0 || !(gtol >= 0.0)) return fail(c, SRMRA_ERR_INVALID_ARG, "max_steps < 0, F < 0 or gtol < 0");
+    if (!mom_ready(c)) return fail(c, SRMRA_ERR_STATE, "no moments set (srmra_mom_set_moments)");
+    int rc;
+    if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
+    std::string err;
+    int steps = 0;
+    rc = mom_run(c, max_steps, F, gtol, f_out, &steps, err);
+    if (steps_out) *steps_out = steps;
+    if (rc != SRMRA_OK) return mom_fail(c, rc, err);
+    c->joint = false;  // the estimate is (x, rho1, rho2) again
+    if ((rc = refresh_after_denoise(c)) != SRMRA_OK) return rc;  // EM can continue from the MoM estimate
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
+
 int srmra_set_denoiser(srmra_ctx* c, srmra_denoiser_fn fn, void* user) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
@@ -857,6 +906,7 @@ void srmra_free(srmra_ctx* c) {
     if (c->d_run) cudaFree(c->d_run);
     if (c->d_emt) cudaFree(c->d_emt);
     if (c->d_rhoj) cudaFree(c->d_rhoj);
+    mom_free(c);
     if (c->d_lrj) cudaFree(c->d_lrj);
     if (c->d_rtol) cudaFree(c->d_rtol);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

@@ -24,6 +24,8 @@ struct IterParams {
     double* f64;
 };
 
+struct MomState;  // NEXT-2 moment-objective state (k_mom_obj.cu)
+
 struct PackLayout {  // packed statistics  b | class_mass | marg1 | marg2 | LL
     int64_t b, cmass, m1, m2, ll, total;
 };
@@ -110,6 +112,9 @@ struct srmra_ctx {
     float* g_cf = nullptr;    // [2][KK Ll Ll][Ll] circulant factor of the polyphase components (TMA mainloop)
     int64_t g_ldw = 0;        // n rounded up to a multiple of 4
 
+    // NEXT-2: method of moments (k_mom_obj.cu), allocated by srmra_mom_set_moments
+    srmra::MomState* mom = nullptr;
+
     // multi-GPU
     void* nccl_comm = nullptr;
 
@@ -131,6 +136,14 @@ cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
 cudaError_t launch_x32_from_x64(srmra_ctx* c);   // after a denoiser hook changed x
 cudaError_t launch_shift_corr(srmra_ctx* c, const double* xref_dev, double* corr_dev);  // NEXT-4
 int moments(srmra_ctx* c, double* m1, double* m2, std::string& err);  // NEXT-2 (k_moments.cu)
+int moments_dev(srmra_ctx* c, double* out_dev, std::string& err);     // same, left on the device
+bool mom_supported(const srmra_ctx* c);                                // k_mom_obj.cu: L_low <= 64
+void mom_free(srmra_ctx* c);
+bool mom_ready(const srmra_ctx* c);                                    // moments set
+int mom_set(srmra_ctx* c, const double* m1, const double* m2, std::string& err);
+int mom_objective(srmra_ctx* c, const double* x, const double* r1, const double* r2, double* f, double* gx,
+                  double* g1, double* g2, std::string& err);
+int mom_run(srmra_ctx* c, int max_steps, int F, double gtol, double* f_out, int* steps_out, std::string& err);
 // TMA 3xTF32 tcgen05 GEMM C = A B^T (k_gemm_tma.cu); c64 / kz / sym: see there
 cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
                             const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
