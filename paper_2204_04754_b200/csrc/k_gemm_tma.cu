@@ -15,6 +15,8 @@
 #include <cuda.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "srmra_internal.cuh"
 #include "tcgen05.cuh"
 
@@ -170,6 +172,131 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 1) tc::tmem_dealloc<BN * KSPLIT>(taddr);
 }
 
+// ---------------------------------------------------------------- float64-accumulating variant (NEXT-2)
+// C (float64) += A B^T with the float32 TMEM chains kept short: the MMA warp rotates over the 4 TMEM blocks
+// of 128 columns, one block per chunk of CH k-tiles (CH x 4 x 3 = 48 MMA accumulations for CH = 4), and 8
+// epilogue warps (2 per TMEM lane quadrant, 64 columns each) drain every finished chunk into float64
+// registers while the MMA fills the next blocks.  A CTA covers kz k-tiles (blockIdx.z slice); slices are
+// combined with float64 atomics (plain stores when there is one slice).  sym: only tiles n0 >= m0.
+constexpr int CH = 4, ACC_THREADS = 320;
+
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
+struct Acc64Args {
+    int M, N, nk, kz, sym;
+    double* c;
+    int64_t ldc;
+};
+
+__global__ void __launch_bounds__(ACC_THREADS, 1)
+    k_gemm_tma_acc64(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+                     const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo, Acc64Args g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t full[STAGES], empty[STAGES], cfull[KSPLIT], cempty[KSPLIT];
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    if (g.sym && n0 < m0) return;
+    const int kt0 = blockIdx.z * g.kz, nloc = min(g.nk - kt0, g.kz);
+    const int nch = (nloc + CH - 1) / CH;
+
+    if (warp == 1) tc::tmem_alloc<BN * KSPLIT>(&tmem_slot);
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(tc::smem_u32(&full[s]), 1);
+            tc::mbar_init(tc::smem_u32(&empty[s]), 1);
+        }
+        for (int p = 0; p < KSPLIT; ++p) {
+            tc::mbar_init(tc::smem_u32(&cfull[p]), 1);
+            tc::mbar_init(tc::smem_u32(&cempty[p]), 8);  // one arrival per epilogue warp
+        }
+        tc::fence_mbar_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t taddr = tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        for (int lt = 0; lt < nloc; ++lt) {
+            const int kt = kt0 + lt, st = lt % STAGES;
+            if (lt >= STAGES) tc::mbar_wait(tc::smem_u32(&empty[st]), ((lt / STAGES) - 1) & 1);
+            const uint32_t sb = tc::smem_u32(base + st * STAGE_BYTES), fb = tc::smem_u32(&full[st]);
+            mbar_expect_tx(fb, STAGE_BYTES);
+            tma_2d(sb, &ta_hi, kt * BK, m0, fb);
+            tma_2d(sb + TILE_BYTES, &ta_lo, kt * BK, m0, fb);
+            tma_2d(sb + 2 * TILE_BYTES, &tb_hi, kt * BK, n0, fb);
+            tma_2d(sb + 3 * TILE_BYTES, &tb_lo, kt * BK, n0, fb);
+        }
+    } else if (warp == 1 && lane == 0) {
+        for (int lt = 0; lt < nloc; ++lt) {
+            const int ch = lt / CH, part = ch % KSPLIT;
+            if (lt % CH == 0 && ch >= KSPLIT) {  // the epilogue has drained this block's previous chunk
+                tc::mbar_wait(tc::smem_u32(&cempty[part]), ((ch / KSPLIT) - 1) & 1);
+                tc::fence_after();
+            }
+            const int st = lt % STAGES;
+            tc::mbar_wait(tc::smem_u32(&full[st]), (lt / STAGES) & 1);
+            tc::fence_after();
+            const uint32_t sa = tc::smem_u32(base + st * STAGE_BYTES);
+            const uint32_t td = taddr + (uint32_t)(part * BN);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint32_t o = kk * 32;
+                const uint64_t ah = sw128_desc(sa + o), al = sw128_desc(sa + TILE_BYTES + o);
+                const uint64_t bh = sw128_desc(sa + 2 * TILE_BYTES + o), bl = sw128_desc(sa + 3 * TILE_BYTES + o);
+                tc::mma_tf32(td, ah, bh, IDESC, ((lt % CH) | kk) != 0);
+                tc::mma_tf32(td, ah, bl, IDESC, 1u);
+                tc::mma_tf32(td, al, bh, IDESC, 1u);
+            }
+            tc::commit(tc::smem_u32(&empty[st]));
+            if (lt % CH == CH - 1 || lt == nloc - 1) tc::commit(tc::smem_u32(&cfull[part]));
+        }
+    } else if (warp >= 2) {
+        const int q4 = warp & 3, half = (warp - 2) >> 2;  // lane quadrant, column half
+        double acc[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+        for (int ch = 0; ch < nch; ++ch) {
+            const int part = ch % KSPLIT;
+            tc::mbar_wait(tc::smem_u32(&cfull[part]), (ch / KSPLIT) & 1);
+            tc::fence_after();
+            const uint32_t ta = taddr + ((uint32_t)(q4 * 32) << 16) + part * BN + half * 64;
+#pragma unroll
+            for (int cc = 0; cc < 64; cc += 32) {
+                float va[16], vb[16];
+                tc::tmem_ld16x2(ta + cc, va, ta + cc + 16, vb);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    acc[cc + j] += (double)va[j];
+                    acc[cc + 16 + j] += (double)vb[j];
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tc::smem_u32(&cempty[part]));
+        }
+        const int row = m0 + q4 * 32 + lane;
+        if (row < g.M) {
+            double* dst = g.c + (size_t)row * g.ldc + n0 + half * 64;
+            const int lim = g.N - (n0 + half * 64);
+            const bool single = gridDim.z == 1;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+                if (j < lim) {
+                    if (single) dst[j] = acc[j];
+                    else atomicAdd(dst + j, acc[j]);
+                }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc<BN * KSPLIT>(taddr);
+}
+
 // circulant factor of the polyphase components: cf[h][(r Ll + rho) Ll + t2][n2] = x_r[rho][(n2 - t2) mod Ll],
 // tf32 hi (h = 0) / lo (h = 1), x_r[m1][m2] = x[(K m1 - r1) mod L][(K m2 - r2) mod L]
 __global__ void k_gemm_circ(const float* __restrict__ x32, int L, int K, float* __restrict__ cf) {
@@ -221,6 +348,39 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// C (float64, zeroed by the caller when the K range is sliced) = A B^T, K sliced in kz k-tiles over
+// blockIdx.z (kz <= 0: chosen so that about 2 waves of CTAs cover the SMs), sym as above
+cudaError_t launch_gemm_tma_acc64(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
+                                  const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, double* c,
+                                  int64_t ldc, int sym, int num_sms, cudaStream_t st, int* zslices) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_acc64, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+    bool ok = make_map(&ta_hi, a_hi, M, Kdim, lda, BM) && make_map(&ta_lo, a_lo, M, Kdim, lda, BM) &&
+              make_map(&tb_hi, b_hi, nb_rows, Kdim, ldb, BN) && make_map(&tb_lo, b_lo, nb_rows, Kdim, ldb, BN);
+    if (!ok) return cudaErrorInvalidValue;
+    Acc64Args g;
+    g.M = (int)M;
+    g.N = N;
+    g.nk = (int)((Kdim + BK - 1) / BK);
+    g.sym = sym;
+    g.c = c;
+    g.ldc = ldc;
+    const int tm = (int)((M + BM - 1) / BM), tn = (N + BN - 1) / BN;
+    const int tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
+    const int want = std::max(1, (2 * num_sms + tiles - 1) / tiles);  // z slices for ~2 waves
+    g.kz = std::max(CH, (g.nk + want - 1) / want);
+    const int z = (g.nk + g.kz - 1) / g.kz;
+    if (zslices) *zslices = z;
+    dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)z);
+    k_gemm_tma_acc64<<<grid, ACC_THREADS, SMEM_BYTES, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, g);
+    return cudaGetLastError();
 }
 
 bool gemm_tma_supported(int Ll) { return (Ll == 32 || Ll == 64) && encode_fn() != nullptr; }

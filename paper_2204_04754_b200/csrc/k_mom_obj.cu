@@ -34,7 +34,7 @@ struct MomState {
     double2* et = nullptr;  // [Ll2][Ll2] Etilde
     double2* e1 = nullptr;  // [Ll2] etilde
     double2* xh = nullptr;  // [L2]
-    double2* rh = nullptr;  // [L2]
+    double2* rh = nullptr;  // [2L] 1-D spectra of rho1 | rho2 (allocated [L2])
     double2* ax = nullptr;  // [L2]
     double2* gr = nullptr;  // [L2]
     double2* tmp = nullptr; // [L2] DFT scratch
@@ -105,36 +105,99 @@ __global__ void k_dft_axis(const double2* __restrict__ in, double2* __restrict__
     }
 }
 
+// 2-D transforms of the [L][L] spectra: one block per line (row: line_stride L, elem_stride 1; column: 1, L),
+// the line and the twiddles staged in shared memory
+__global__ void k_dft_line(const double2* __restrict__ in, double2* __restrict__ out, int n, int64_t line_stride,
+                           int64_t elem_stride, int sgn, const double2* __restrict__ tw, int step) {
+    extern __shared__ double2 sl[];  // line [n] | twiddles [n]
+    double2* tws = sl + n;
+    const double2* src = in + (int64_t)blockIdx.x * line_stride;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        sl[j] = src[(int64_t)j * elem_stride];
+        double2 w = tw[j * step];
+        if (sgn > 0) w.y = -w.y;
+        tws[j] = w;
+    }
+    __syncthreads();
+    double2* dst = out + (int64_t)blockIdx.x * line_stride;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        int idx = 0;
+        for (int j = 0; j < n; ++j) {
+            acc = cadd(acc, cmul(sl[j], tws[idx]));
+            idx += k;
+            if (idx >= n) idx -= n;
+        }
+        dst[(int64_t)k * elem_stride] = acc;
+    }
+}
+
 __global__ void k_sub_diag(double2* t2, int n, double v) {
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) t2[(int64_t)a * n + a].x -= v;
 }
 
-// rhohat[u1][u2] = rhohat1[u1] rhohat2[u2] (D_rho = diag vec(rho1 rho2^T))
-__global__ void k_rhohat(const double* __restrict__ r1, const double* __restrict__ r2, int L,
-                         const double2* __restrict__ tw, double2* __restrict__ rh) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < L * L; e += gridDim.x * blockDim.x) {
-        const int u1 = e / L, u2 = e - u1 * L;
-        double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
-        int i1 = 0, i2 = 0;
+// rhohat = rhohat1 (x) rhohat2 (D_rho = diag vec(rho1 rho2^T)): the kernels below take the two
+// 1-D spectra rh[0 .. L) | rh[L .. 2L) and form rhohat[d1][d2] = rh1[d1] rh2[d2] on the fly
+__global__ void k_rhohat(const double* __restrict__ r, int L, const double2* __restrict__ tw, double2* __restrict__ rh) {
+    extern __shared__ double2 st[];  // twiddles [L] | rho_j [L] (as .x)
+    const int j = blockIdx.x;        // rho1 | rho2
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        st[i] = tw[i];
+        st[L + i].x = r[j * L + i];
+    }
+    __syncthreads();
+    for (int u = threadIdx.x; u < L; u += blockDim.x) {
+        double2 a = make_double2(0.0, 0.0);
+        int idx = 0;
         for (int s = 0; s < L; ++s) {
-            const double2 w1 = tw[i1], w2 = tw[i2];
-            a.x += r1[s] * w1.x; a.y += r1[s] * w1.y;
-            b.x += r2[s] * w2.x; b.y += r2[s] * w2.y;
-            i1 += u1; if (i1 >= L) i1 -= L;
-            i2 += u2; if (i2 >= L) i2 -= L;
+            const double2 w = st[idx];
+            const double v = st[L + s].x;
+            a.x += v * w.x;
+            a.y += v * w.y;
+            idx += u;
+            if (idx >= L) idx -= L;
         }
-        rh[e] = cmul(a, b);
+        rh[j * L + u] = a;
     }
 }
 
-// Etilde[k][k'] (one block per k) and etilde[k]; |.|^2 partials per block
-__global__ void k_mom_E(const double2* __restrict__ xh, const double2* __restrict__ rh, const double2* __restrict__ t2,
-                        const double2* __restrict__ t1, int L, int Ll, int K, double2* __restrict__ et,
-                        double2* __restrict__ e1, double* __restrict__ fpart) {
-    extern __shared__ double2 xs[];  // [K^2] xhat[k + Ll m]
+constexpr int MC = 16;  // frequencies u = ubar + Ll m handled per pass (accumulators per thread)
+
+// block-wide sum of n complex accumulators (blockDim = 256); results in out[0 .. n) of shared memory
+__device__ __forceinline__ void block_csum_n(double2* acc, int n, double2* sred /*[8][MC]*/, double2* out) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int m = 0; m < n; ++m) {
+        double2 v = acc[m];
+        v.x = warp_sum(v.x);
+        v.y = warp_sum(v.y);
+        if (lane == 0) sred[w * MC + m] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < n) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int j = 0; j < 8; ++j) t = cadd(t, sred[j * MC + threadIdx.x]);
+        out[threadIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+// Etilde[k][k'] (one block per k, threads over k') and etilde[k]; |.|^2 partials per block.
+//   sum_{m, m'} xhat[u] conj(xhat[u']) rh1[u1 - u1'] rh2[u2 - u2'], inner sum over m2 first.
+// KT = K <= 4: u1 - u1' = k1 - k1' + Ll (m1 - m1') takes 2K - 1 values, so the prior factors are gathered
+// once per k' and the K^4 sum is done as two K^3 contractions.
+template <int KT>
+__global__ void __launch_bounds__(256) k_mom_E(const double2* __restrict__ xh, const double2* __restrict__ rh,
+                                               const double2* __restrict__ t2, const double2* __restrict__ t1, int L,
+                                               int Ll, int K, double2* __restrict__ et, double2* __restrict__ e1,
+                                               double* __restrict__ fpart) {
+    extern __shared__ double2 sm[];  // rh1 [L] | rh2 [L] | xs [K^2]
     __shared__ double red[32];
+    double2* r1s = sm;
+    double2* r2s = sm + L;
+    double2* xs = sm + 2 * L;
     const int Ll2 = Ll * Ll, KK = K * K;
     const int k = blockIdx.x, k1 = k / Ll, k2 = k - k1 * Ll;
+    for (int j = threadIdx.x; j < 2 * L; j += blockDim.x) sm[j] = rh[j];
     for (int m = threadIdx.x; m < KK; m += blockDim.x) xs[m] = xh[(k1 + Ll * (m / K)) * L + k2 + Ll * (m % K)];
     __syncthreads();
     const double invK4 = 1.0 / ((double)KK * KK);
@@ -142,14 +205,56 @@ __global__ void k_mom_E(const double2* __restrict__ xh, const double2* __restric
     for (int kp = threadIdx.x; kp < Ll2; kp += blockDim.x) {
         const int kp1 = kp / Ll, kp2 = kp - kp1 * Ll;
         double2 acc = make_double2(0.0, 0.0);
-        for (int mp = 0; mp < KK; ++mp) {
-            const int up1 = kp1 + Ll * (mp / K), up2 = kp2 + Ll * (mp % K);
-            double2 in = make_double2(0.0, 0.0);
-            for (int m = 0; m < KK; ++m) {
-                const int d1 = imod(k1 + Ll * (m / K) - up1, L), d2 = imod(k2 + Ll * (m % K) - up2, L);
-                in = cadd(in, cmul(xs[m], rh[d1 * L + d2]));
+        if constexpr (KT > 0) {
+            double2 A1[2 * KT - 1], A2[2 * KT - 1], B[KT][KT];
+#pragma unroll
+            for (int dl = 0; dl < 2 * KT - 1; ++dl) {
+                int d1 = k1 - kp1 + Ll * (dl - (KT - 1)), d2 = k2 - kp2 + Ll * (dl - (KT - 1));
+                d1 += d1 < 0 ? L : 0;
+                d1 -= d1 >= L ? L : 0;
+                d2 += d2 < 0 ? L : 0;
+                d2 -= d2 >= L ? L : 0;
+                A1[dl] = r1s[d1];
+                A2[dl] = r2s[d2];
             }
-            acc = cadd(acc, cmulc(in, xh[up1 * L + up2]));
+#pragma unroll
+            for (int m1 = 0; m1 < KT; ++m1)
+#pragma unroll
+                for (int mp2 = 0; mp2 < KT; ++mp2) {
+                    double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int m2 = 0; m2 < KT; ++m2) t = cadd(t, cmul(xs[m1 * KT + m2], A2[m2 - mp2 + KT - 1]));
+                    B[m1][mp2] = t;
+                }
+#pragma unroll
+            for (int mp1 = 0; mp1 < KT; ++mp1)
+#pragma unroll
+                for (int mp2 = 0; mp2 < KT; ++mp2) {
+                    double2 in = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int m1 = 0; m1 < KT; ++m1) in = cadd(in, cmul(A1[m1 - mp1 + KT - 1], B[m1][mp2]));
+                    acc = cadd(acc, cmulc(in, xh[(kp1 + Ll * mp1) * L + kp2 + Ll * mp2]));
+                }
+        } else {
+            for (int mp1 = 0; mp1 < K; ++mp1) {
+                const int up1 = kp1 + Ll * mp1;
+                for (int mp2 = 0; mp2 < K; ++mp2) {
+                    const int up2 = kp2 + Ll * mp2;
+                    double2 in = make_double2(0.0, 0.0);
+                    for (int m1 = 0; m1 < K; ++m1) {
+                        int d1 = k1 + Ll * m1 - up1;
+                        d1 += d1 < 0 ? L : 0;
+                        double2 row = make_double2(0.0, 0.0);
+                        for (int m2 = 0; m2 < K; ++m2) {
+                            int d2 = k2 + Ll * m2 - up2;
+                            d2 += d2 < 0 ? L : 0;
+                            row = cadd(row, cmul(xs[m1 * K + m2], r2s[d2]));
+                        }
+                        in = cadd(in, cmul(row, r1s[d1]));
+                    }
+                    acc = cadd(acc, cmulc(in, xh[up1 * L + up2]));
+                }
+            }
         }
         const double2 t = t2[(int64_t)k * Ll2 + kp];
         const double2 E = make_double2(acc.x * invK4 - t.x, acc.y * invK4 - t.y);
@@ -160,73 +265,165 @@ __global__ void k_mom_E(const double2* __restrict__ xh, const double2* __restric
     if (threadIdx.x == 0) {
         fpart[k] = part;
         double2 m1 = make_double2(0.0, 0.0);
-        for (int m = 0; m < KK; ++m) m1 = cadd(m1, cmul(xs[m], rh[(k1 + Ll * (m / K)) * L + k2 + Ll * (m % K)]));
+        for (int m = 0; m < KK; ++m)
+            m1 = cadd(m1, cmul(xs[m], cmul(r1s[k1 + Ll * (m / K)], r2s[k2 + Ll * (m % K)])));
         const double2 e = make_double2(m1.x / KK - t1[k].x, m1.y / KK - t1[k].y);
         e1[k] = e;
         fpart[Ll2 + k] = e.x * e.x + e.y * e.y;
     }
 }
 
-// Ax[u] for the K^2 frequencies u = ubar + Ll m of one block (row ubar of Etilde staged in shared memory)
-__global__ void k_mom_A(const double2* __restrict__ xh, const double2* __restrict__ rh, const double2* __restrict__ et,
-                        const double2* __restrict__ e1, int L, int Ll, int K, double c2, double c1, double2* __restrict__ ax) {
-    extern __shared__ double2 erow[];  // [Ll2]
-    __shared__ double red[32];
-    const int Ll2 = Ll * Ll, KK = K * K, L2 = L * L;
+// Ax[u] for the K^2 frequencies u = ubar + Ll m of one block: conj(row ubar of Etilde) and the 1-D prior
+// spectra staged in shared memory; each term h = conj(Etilde[ubar, ubar']) conj(xhat[u']) is formed once,
+// multiplied by the K values rh1[u1 - u1'] (m1) and then by the K values rh2[u2 - u2'] (m2) into the K^2
+// accumulators.  KT = K for K <= 4 (fully unrolled); KT = 0: any K, MC frequencies per pass.
+template <int KT>
+__global__ void __launch_bounds__(256) k_mom_A(const double2* __restrict__ xh, const double2* __restrict__ rh,
+                                               const double2* __restrict__ et, const double2* __restrict__ e1, int L,
+                                               int Ll, int K, double c2, double c1, double2* __restrict__ ax) {
+    extern __shared__ double2 sm[];  // erow [Ll2] | rh1 [L] | rh2 [L]
+    __shared__ double2 sred[8 * MC], sout[MC];
+    const int Ll2 = Ll * Ll, KK = K * K;
+    double2* erow = sm;
+    double2* r1s = sm + Ll2;
+    double2* r2s = r1s + L;
     const int ub = blockIdx.x, ub1 = ub / Ll, ub2 = ub - ub1 * Ll;
-    for (int j = threadIdx.x; j < Ll2; j += blockDim.x) erow[j] = et[(int64_t)ub * Ll2 + j];
+    for (int j = threadIdx.x; j < Ll2; j += blockDim.x) erow[j] = conj2(et[(int64_t)ub * Ll2 + j]);
+    for (int j = threadIdx.x; j < 2 * L; j += blockDim.x) r1s[j] = rh[j];
     __syncthreads();
-    for (int m = 0; m < KK; ++m) {
-        const int u1 = ub1 + Ll * (m / K), u2 = ub2 + Ll * (m % K);
-        double2 acc = make_double2(0.0, 0.0);
-        for (int up = threadIdx.x; up < L2; up += blockDim.x) {
-            const int up1 = up / L, up2 = up - up1 * L;
-            const double2 ec = conj2(erow[(up1 % Ll) * Ll + up2 % Ll]);
-            const double2 r = rh[imod(u1 - up1, L) * L + imod(u2 - up2, L)];
-            acc = cadd(acc, cmulc(cmul(ec, r), xh[up]));
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int m0 = 0; m0 < KK; m0 += MC) {
+        const int nm = KT ? KT * KT : min(MC, KK - m0);
+        double2 acc[MC];
+        int o1[MC], o2[MC];
+#pragma unroll
+        for (int m = 0; m < MC; ++m) {
+            acc[m] = make_double2(0.0, 0.0);
+            const int mm = m0 + m;
+            o1[m] = ub1 + Ll * (mm / K);  // u1 of accumulator m (KT: o1 indexed by m1 only)
+            o2[m] = ub2 + Ll * (mm % K);
         }
-        acc = block_csum(acc, red);
-        if (threadIdx.x == 0) {
-            const double2 t = cmul(conj2(e1[ub]), rh[u1 * L + u2]);
-            ax[u1 * L + u2] = make_double2(c2 * acc.x + c1 * t.x, c2 * acc.y + c1 * t.y);
+        for (int up1 = ty; up1 < L; up1 += 8) {
+            const double2* erow1 = erow + (up1 % Ll) * Ll;
+            int ub2p = tx % Ll;
+            for (int up2 = tx; up2 < L; up2 += 32) {
+                const double2 h = cmulc(erow1[ub2p], xh[up1 * L + up2]);
+                ub2p += 32;
+                while (ub2p >= Ll) ub2p -= Ll;
+                if constexpr (KT > 0) {
+                    double2 r2[KT];
+#pragma unroll
+                    for (int m2 = 0; m2 < KT; ++m2) {
+                        int d2 = ub2 + Ll * m2 - up2;
+                        d2 += d2 < 0 ? L : 0;
+                        r2[m2] = r2s[d2];
+                    }
+#pragma unroll
+                    for (int m1 = 0; m1 < KT; ++m1) {
+                        int d1 = ub1 + Ll * m1 - up1;
+                        d1 += d1 < 0 ? L : 0;
+                        const double2 hr = cmul(h, r1s[d1]);
+#pragma unroll
+                        for (int m2 = 0; m2 < KT; ++m2) acc[m1 * KT + m2] = cadd(acc[m1 * KT + m2], cmul(hr, r2[m2]));
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < MC; ++m) {
+                        if (m < nm) {
+                            int d1 = o1[m] - up1, d2 = o2[m] - up2;
+                            d1 += d1 < 0 ? L : 0;
+                            d2 += d2 < 0 ? L : 0;
+                            acc[m] = cadd(acc[m], cmul(cmul(h, r1s[d1]), r2s[d2]));
+                        }
+                    }
+                }
+            }
+        }
+        block_csum_n(acc, nm, sred, sout);
+        if (threadIdx.x < nm) {
+            const int mm = m0 + threadIdx.x, m1 = mm / K, m2 = mm - m1 * K;
+            const int u1 = ub1 + Ll * m1, u2 = ub2 + Ll * m2;
+            const double2 t = cmul(conj2(e1[ub]), cmul(r1s[u1], r2s[u2]));
+            const double2 a = sout[threadIdx.x];
+            ax[u1 * L + u2] = make_double2(c2 * a.x + c1 * t.x, c2 * a.y + c1 * t.y);
         }
     }
 }
 
-// Gr[v] for the K^2 frequencies v = vbar + Ll m of one block (the diagonal Etilde[j, j - vbar] staged)
-__global__ void k_mom_G(const double2* __restrict__ xh, const double2* __restrict__ et, const double2* __restrict__ e1,
-                        int L, int Ll, int K, double c2, double c1, double2* __restrict__ gr) {
+// Gr[v] for the K^2 frequencies v = vbar + Ll m of one block (the diagonal Etilde[j, j - vbar] staged);
+// each term h = Etilde[ubar, ubar - vbar] conj(xhat[u]) is formed once for all K^2 shifts v
+template <int KT>
+__global__ void __launch_bounds__(256) k_mom_G(const double2* __restrict__ xh, const double2* __restrict__ et,
+                                               const double2* __restrict__ e1, int L, int Ll, int K, double c2,
+                                               double c1, double2* __restrict__ gr) {
     extern __shared__ double2 ediag[];  // [Ll2]
-    __shared__ double red[32];
-    const int Ll2 = Ll * Ll, KK = K * K, L2 = L * L;
+    __shared__ double2 sred[8 * MC], sout[MC];
+    const int Ll2 = Ll * Ll, KK = K * K;
     const int vb = blockIdx.x, vb1 = vb / Ll, vb2 = vb - vb1 * Ll;
     for (int j = threadIdx.x; j < Ll2; j += blockDim.x) {
         const int j1 = j / Ll, j2 = j - j1 * Ll;
         ediag[j] = et[(int64_t)j * Ll2 + imod(j1 - vb1, Ll) * Ll + imod(j2 - vb2, Ll)];
     }
     __syncthreads();
-    for (int m = 0; m < KK; ++m) {
-        const int v1 = vb1 + Ll * (m / K), v2 = vb2 + Ll * (m % K);
-        double2 acc = make_double2(0.0, 0.0);
-        for (int u = threadIdx.x; u < L2; u += blockDim.x) {
-            const int u1 = u / L, u2 = u - u1 * L;
-            const double2 e = ediag[(u1 % Ll) * Ll + u2 % Ll];
-            const double2 xm = xh[imod(u1 - v1, L) * L + imod(u2 - v2, L)];
-            acc = cadd(acc, cmul(cmulc(e, xh[u]), xm));
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int m0 = 0; m0 < KK; m0 += MC) {
+        const int nm = KT ? KT * KT : min(MC, KK - m0);
+        double2 acc[MC];
+        int o1[MC], o2[MC];
+#pragma unroll
+        for (int m = 0; m < MC; ++m) {
+            acc[m] = make_double2(0.0, 0.0);
+            const int mm = m0 + m;
+            o1[m] = vb1 + Ll * (mm / K);
+            o2[m] = vb2 + Ll * (mm % K);
         }
-        acc = block_csum(acc, red);
-        if (threadIdx.x == 0) {
+        for (int u1 = ty; u1 < L; u1 += 8) {
+            const double2* ed1 = ediag + (u1 % Ll) * Ll;
+            int ub2 = tx % Ll;
+            for (int u2 = tx; u2 < L; u2 += 32) {
+                const double2 h = cmulc(ed1[ub2], xh[u1 * L + u2]);
+                ub2 += 32;
+                while (ub2 >= Ll) ub2 -= Ll;
+                if constexpr (KT > 0) {
+#pragma unroll
+                    for (int m1 = 0; m1 < KT; ++m1) {
+                        int w1 = u1 - vb1 - Ll * m1;
+                        w1 += w1 < 0 ? L : 0;
+                        const double2* xrow = xh + w1 * L;
+#pragma unroll
+                        for (int m2 = 0; m2 < KT; ++m2) {
+                            int w2 = u2 - vb2 - Ll * m2;
+                            w2 += w2 < 0 ? L : 0;
+                            acc[m1 * KT + m2] = cadd(acc[m1 * KT + m2], cmul(h, xrow[w2]));
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < MC; ++m) {
+                        if (m < nm) {
+                            int w1 = u1 - o1[m], w2 = u2 - o2[m];
+                            w1 += w1 < 0 ? L : 0;
+                            w2 += w2 < 0 ? L : 0;
+                            acc[m] = cadd(acc[m], cmul(h, xh[w1 * L + w2]));
+                        }
+                    }
+                }
+            }
+        }
+        block_csum_n(acc, nm, sred, sout);
+        if (threadIdx.x < nm) {
+            const int mm = m0 + threadIdx.x, m1 = mm / K, m2 = mm - m1 * K;
+            const int v1 = vb1 + Ll * m1, v2 = vb2 + Ll * m2;
             const double2 t = cmulc(e1[vb], xh[v1 * L + v2]);
-            gr[v1 * L + v2] = make_double2(c2 * acc.x + c1 * t.x, c2 * acc.y + c1 * t.y);
+            const double2 a = sout[threadIdx.x];
+            gr[v1 * L + v2] = make_double2(c2 * a.x + c1 * t.x, c2 * a.y + c1 * t.y);
         }
     }
 }
 
-// f, grad x = Re(DFT(Ax)), grad rho (joint) = Re(IDFT(Gr)), grad rho1 / rho2 (one block)
-__global__ void k_mom_finish(const double* __restrict__ fpart, int Ll2, double lam, const double2* __restrict__ gxc,
-                             const double2* __restrict__ grc, const double* __restrict__ theta, int L, double* __restrict__ out) {
+// f (one block)
+__global__ void k_mom_fsum(const double* __restrict__ fpart, int Ll2, double lam, double* __restrict__ out) {
     __shared__ double red[32];
-    const int L2 = L * L;
     double a = 0.0, b = 0.0;
     for (int k = threadIdx.x; k < Ll2; k += blockDim.x) {
         a += fpart[k];
@@ -236,25 +433,33 @@ __global__ void k_mom_finish(const double* __restrict__ fpart, int Ll2, double l
     __syncthreads();
     b = block_sum(b, red);
     if (threadIdx.x == 0) out[0] = a / ((double)Ll2 * Ll2) + lam * b / (double)Ll2;
+}
+
+// grad x = Re(DFT(Ax)), grad rho (joint) = Re(IDFT(Gr)) row s; grad rho1[s], grad rho2[s] (block s)
+__global__ void k_mom_grad(const double2* __restrict__ gxc, const double2* __restrict__ grc,
+                           const double* __restrict__ theta, int L, double* __restrict__ out) {
+    __shared__ double red[32];
+    const int L2 = L * L, s = blockIdx.x;
     double* gx = out + 1;
     double* g1 = gx + L2;
     double* g2 = g1 + L;
     double* gj = g2 + L;
-    for (int p = threadIdx.x; p < L2; p += blockDim.x) {
-        gx[p] = gxc[p].x;
-        gj[p] = grc[p].x;
-    }
-    __syncthreads();
     const double* r1 = theta + L2;
     const double* r2 = r1 + L;
-    for (int s = threadIdx.x; s < L; s += blockDim.x) {
-        double s1 = 0.0, s2 = 0.0;
-        for (int t = 0; t < L; ++t) {
-            s1 += gj[s * L + t] * r2[t];
-            s2 += gj[t * L + s] * r1[t];
-        }
-        g1[s] = s1;
-        g2[s] = s2;
+    double a = 0.0, b = 0.0;
+    for (int t = threadIdx.x; t < L; t += blockDim.x) {
+        gx[s * L + t] = gxc[s * L + t].x;
+        const double v = grc[s * L + t].x;
+        gj[s * L + t] = v;
+        a += v * r2[t];
+        b += grc[t * L + s].x * r1[t];
+    }
+    a = block_sum(a, red);
+    __syncthreads();
+    b = block_sum(b, red);
+    if (threadIdx.x == 0) {
+        g1[s] = a;
+        g2[s] = b;
     }
 }
 
@@ -324,8 +529,10 @@ static cudaError_t mom_alloc(srmra_ctx* c) {
 static cudaError_t dft2(srmra_ctx* c, double2* a, double2* scratch, int n, int sgn) {
     MomState* m = c->mom;
     const int step = m->L / n;
-    k_dft_axis<<<grid_for((int64_t)n * n), 256, 0, c->stream>>>(a, scratch, 1, n, n, sgn, m->tw, step);
-    k_dft_axis<<<grid_for((int64_t)n * n), 256, 0, c->stream>>>(scratch, a, n, n, 1, sgn, m->tw, step);
+    const int th = std::min(n, 256);
+    const size_t sh = sizeof(double2) * 2 * n;
+    k_dft_line<<<n, th, sh, c->stream>>>(a, scratch, n, n, 1, sgn, m->tw, step);         // rows
+    k_dft_line<<<n, th, sh, c->stream>>>(scratch, a, n, 1, n, sgn, m->tw, step);         // columns
     return cudaGetLastError();
 }
 
@@ -388,22 +595,41 @@ static cudaError_t mom_eval_dev(srmra_ctx* c) {
     const double c1 = 2.0 * m->lambda / ((double)Ll2 * K * K);
     k_real_to_c<<<grid_for(L2), 256, 0, c->stream>>>(m->theta, m->xh, L2);
     MCK(dft2(c, m->xh, m->tmp, L, -1));
-    k_rhohat<<<grid_for(L2), 256, 0, c->stream>>>(m->theta + L2, m->theta + L2 + L, L, m->tw, m->rh);
-    k_mom_E<<<Ll2, 256, sizeof(double2) * K * K, c->stream>>>(m->xh, m->rh, m->t2, m->t1, L, Ll, K, m->et, m->e1, m->fpart);
-    k_mom_A<<<Ll2, 256, sizeof(double2) * Ll2, c->stream>>>(m->xh, m->rh, m->et, m->e1, L, Ll, K, 4.0 / L4, c1, m->ax);
-    k_mom_G<<<Ll2, 256, sizeof(double2) * Ll2, c->stream>>>(m->xh, m->et, m->e1, L, Ll, K, 2.0 / L4, c1, m->gr);
+    k_rhohat<<<2, std::min(L, 256), sizeof(double2) * 2 * L, c->stream>>>(m->theta + L2, L, m->tw, m->rh);
+    const size_t sa = sizeof(double2) * (Ll2 + 2 * L), sg = sizeof(double2) * Ll2;
+#define MOM_AG(KT)                                                                                                 \
+    k_mom_E<KT><<<Ll2, 256, sizeof(double2) * (2 * L + K * K), c->stream>>>(m->xh, m->rh, m->t2, m->t1, L, Ll, K,   \
+                                                                          m->et, m->e1, m->fpart);              \
+    k_mom_A<KT><<<Ll2, 256, sa, c->stream>>>(m->xh, m->rh, m->et, m->e1, L, Ll, K, 4.0 / L4, c1, m->ax);        \
+    k_mom_G<KT><<<Ll2, 256, sg, c->stream>>>(m->xh, m->et, m->e1, L, Ll, K, 2.0 / L4, c1, m->gr)
+    switch (K) {
+        case 1: MOM_AG(1); break;
+        case 2: MOM_AG(2); break;
+        case 3: MOM_AG(3); break;
+        case 4: MOM_AG(4); break;
+        default: MOM_AG(0); break;
+    }
+#undef MOM_AG
     MCK(dft2(c, m->ax, m->tmp, L, -1));
     MCK(dft2(c, m->gr, m->tmp, L, +1));
-    k_mom_finish<<<1, 1024, 0, c->stream>>>(m->fpart, Ll2, m->lambda, m->ax, m->gr, m->theta, L, m->out);
+    k_mom_fsum<<<1, 256, 0, c->stream>>>(m->fpart, Ll2, m->lambda, m->out);
+    k_mom_grad<<<L, std::min(L, 128), 0, c->stream>>>(m->ax, m->gr, m->theta, L, m->out);
     return cudaGetLastError();
 }
 
 static bool attrs_set = false;
 static cudaError_t mom_attrs(int Ll2) {
     if (attrs_set) return cudaSuccess;
-    const int bytes = (int)sizeof(double2) * 64 * 64;
-    MCK(cudaFuncSetAttribute(k_mom_A, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MCK(cudaFuncSetAttribute(k_mom_G, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int bytes = (int)sizeof(double2) * (64 * 64 + 2 * 4096);  // Ll <= 64; L <= 4096
+#define MOM_ATTR(KT)                                                                             \
+    MCK(cudaFuncSetAttribute(k_mom_A<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
+    MCK(cudaFuncSetAttribute(k_mom_G<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
+    MOM_ATTR(0);
+    MOM_ATTR(1);
+    MOM_ATTR(2);
+    MOM_ATTR(3);
+    MOM_ATTR(4);
+#undef MOM_ATTR
     (void)Ll2;
     attrs_set = true;
     return cudaSuccess;

@@ -17,7 +17,6 @@ namespace srmra {
 
 namespace momk {
 
-constexpr int MOM_KZ = 16;
 
 // yt[h][k][i] (h = tf32 hi / lo): y_i[k] for k < Ll2, 1 for k = Ll2 (i < n), 0 otherwise; ldw >= n
 __global__ void k_mom_yt(const float* __restrict__ y, int64_t n, int Ll2, int R, int64_t ldw, float* __restrict__ yt) {
@@ -89,10 +88,10 @@ int moments_dev(srmra_ctx* c, double* out, std::string& err) {
             e = cudaGetLastError();
         }
         if (e == cudaSuccess)
-            // K sliced over blockIdx.z in 16 k-tiles (4 per TMEM split-K block: float32 chains of 48 MMA
-            // accumulations), slices combined with float64 atomics; symmetric: upper tiles only
-            e = launch_gemm_tma(yt, yt + (size_t)R * ldw, R, ldw, yt, yt + (size_t)R * ldw, R, ldw, R, ldw, 0, c->Ll,
-                                nullptr, R, c->stream, C, MOM_KZ, 1);
+            // float64-accumulating tensor-core SYRK: float32 TMEM chains of 48 MMA accumulations drained into
+            // float64 registers; the K range sliced over ~2 waves of CTAs (float64 atomics); upper tiles only
+            e = launch_gemm_tma_acc64(yt, yt + (size_t)R * ldw, R, ldw, yt, yt + (size_t)R * ldw, R, ldw, R, ldw, C, R, 1,
+                                      c->num_sms, c->stream);
         if (e == cudaSuccess) {
             k_mom_out<<<(unsigned)std::min<int64_t>(((int64_t)nout + 255) / 256, 4096), 256, 0, c->stream>>>(C, R, Ll2, out);
             e = cudaGetLastError();

@@ -444,6 +444,13 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     c->opt = opt;
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;
+    {  // stream-ordered temporaries (moments, evaluation) are reused across calls instead of returned to the OS
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     c->L = L_high; c->Ll = L_low; c->K = K; c->KK = K * K;
     c->L2 = L_high * L_high; c->Ll2 = L_low * L_low; c->Lh = L_low / 2 + 1;
     c->n_local = n_local;

@@ -148,6 +148,10 @@ int mom_run(srmra_ctx* c, int max_steps, int F, double gtol, double* f_out, int*
 cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
                             const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
                             float* c, int64_t ldc, cudaStream_t st, double* c64 = nullptr, int kz = 0, int sym = 0);
+// same product accumulated in float64 (TMEM chunks drained into registers; k_gemm_tma.cu)
+cudaError_t launch_gemm_tma_acc64(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
+                                  const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, double* c,
+                                  int64_t ldc, int sym, int num_sms, cudaStream_t st, int* zslices = nullptr);
 int allreduce_doubles(srmra_ctx* c, double* buf, size_t n);           // NCCL sum, no-op for world 1
 // ---------------------------------------------------------------- path kernels
 cudaError_t launch_direct_em(srmra_ctx* c);     // k_direct.cu
