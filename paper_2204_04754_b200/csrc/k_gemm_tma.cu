@@ -374,8 +374,16 @@ cudaError_t launch_gemm_tma_acc64(const float* a_hi, const float* a_lo, int64_t 
     g.ldc = ldc;
     const int tm = (int)((M + BM - 1) / BM), tn = (N + BN - 1) / BN;
     const int tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
-    const int want = std::max(1, (2 * num_sms + tiles - 1) / tiles);  // z slices for ~2 waves
-    g.kz = std::max(CH, (g.nk + want - 1) / want);
+    // z slices: at least ~2 waves of CTAs; among up to 4x that many, the count whose last wave is fullest
+    const int want = std::max(1, (2 * num_sms + tiles - 1) / tiles);
+    int zb = want;
+    double eb = 0.0;
+    for (int zz = want; zz <= 4 * want && zz <= std::max(1, g.nk / CH); ++zz) {
+        const double ctas = (double)tiles * zz, waves = ceil(ctas / num_sms);
+        const double eff = ctas / (waves * num_sms);
+        if (eff > eb + 1e-9) { eb = eff; zb = zz; }
+    }
+    g.kz = std::max(CH, (g.nk + zb - 1) / zb);
     const int z = (g.nk + g.kz - 1) / g.kz;
     if (zslices) *zslices = z;
     dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)z);
