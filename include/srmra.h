@@ -82,7 +82,9 @@ SRMRA_API void srmra_default_options(srmra_options* opt);
 
 /*
  * Create a context for this rank's shard of the observations and stage theta_0.
- *   y       host, float32 [n_local][L_low][L_low]: observations y_i of this rank (copied).
+ *   y       host, float32 [n_local][L_low][L_low]: observations y_i of this rank (copied); or NULL:
+ *           no observations yet — the context returns STATE from the iteration / moment calls until
+ *           srmra_load or srmra_generate supplies them.
  *   n_local number of observations on this rank (>= 0; the global N is the sum over ranks).
  *   L_high, L_low, K   image side, observation side, K = L_high / L_low (must hold exactly).
  *   sigma   noise standard deviation (> 0, finite), known.
@@ -102,6 +104,31 @@ SRMRA_API int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32
  * before the next srmra_em_iter (which returns STATE until then). */
 SRMRA_API int srmra_load(srmra_ctx* ctx, const float* y, const float* x0, const double* rho1_0,
                const double* rho2_0);
+
+/*
+ * NEXT-4 device data generator: like srmra_load, but the n_local observations are drawn on the GPU from
+ * the model of PAPER.md:37-38 (eq:model_1), y_j[n1, n2] = x[(n1 K - s^1) mod L_high, (n2 K - s^2) mod
+ * L_high] + sigma z, for the global observation indices j = first_index .. first_index + n_local - 1
+ * (ranks pass their offset, so the union over ranks equals the one-rank data set), sigma the context's.
+ * Counter-based: Philox4x32-10 with key (seed mod 2^32, seed >> 32).  Shifts: counter (j mod 2^32,
+ * j >> 32, 0, 0) -> words (u0, u1); s^1 = min{k : (u0 + 0.5) 2^-32 < C1[k]}, C1 the sequential float64
+ * partial sums of rho1_true as given (clamped to the last k with positive mass), s^2 likewise from u1
+ * and rho2_true.  Noise: counter (j mod 2^32, j >> 32, 1 + b, 0) -> (r0..r3), V = ((r >> 9) + 0.5) 2^-23 (exact in float32),
+ * Box-Muller z = sqrt(-2 ln V0) (cos, sin)(2 pi V1), sqrt(-2 ln V2) (cos, sin)(2 pi V3) for pixels
+ * 4b .. 4b+3 (row-major), evaluated in float32 (logf, sqrtf, sincospif).  synth/philox.py is the
+ * reference.  x_true: host float32 [L_high][L_high]; rho*_true, rho*_0: host float64 [L_high] (>= 0,
+ * sum 1 within 1e-6); x0 / rho*_0 the initial estimate as in srmra_load; shifts_out: host int32
+ * [n_local][2] (s^1, s^2) or NULL.  Resets the iteration counter and trace.  Synchronises.
+ * Errors: INVALID_ARG (NULL, first_index < 0, non-finite, bad pmf), STATE, CUDA.
+ */
+SRMRA_API int srmra_generate(srmra_ctx* ctx, const float* x_true, const double* rho1_true, const double* rho2_true,
+                             uint64_t seed, int64_t first_index, const float* x0, const double* rho1_0,
+                             const double* rho2_0, int32_t* shifts_out);
+
+/* Test hook: copy observations first .. first + count - 1 of this rank (float32 [count][L_low][L_low],
+ * caller-owned host buffer) as the device holds them (e.g. after srmra_generate).  Synchronises.
+ * Errors: INVALID_ARG (range outside [0, n_local), NULL), STATE, CUDA. */
+SRMRA_API int srmra_get_observations(srmra_ctx* ctx, int64_t first, int64_t count, float* y_out);
 
 /* Enqueue n_iters >= 0 EM iterations on the context stream; asynchronous (no host sync).
  * With world > 1 each iteration performs one NCCL all-reduce of the sufficient statistics. */

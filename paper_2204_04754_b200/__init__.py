@@ -36,7 +36,7 @@ ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_it
                "srmra_nccl_unique_id", "srmra_free",
                "srmra_last_error", "srmra_run", "srmra_set_denoiser", "srmra_relative_error",
                "srmra_set_joint_rho", "srmra_get_joint_rho", "srmra_moments",
-               "srmra_mom_set_moments", "srmra_mom_objective", "srmra_mom_run")
+               "srmra_mom_set_moments", "srmra_mom_objective", "srmra_mom_run", "srmra_generate", "srmra_get_observations")
 
 
 class SrmraError(RuntimeError):
@@ -91,6 +91,8 @@ def _load():
         "srmra_set_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
         "srmra_get_joint_rho": (ctypes.c_int, [_ctxp, _dp]),
         "srmra_moments": (ctypes.c_int, [_ctxp, _dp, _dp]),
+        "srmra_get_observations": (ctypes.c_int, [_ctxp, ctypes.c_int64, ctypes.c_int64, _fp]),
+        "srmra_generate": (ctypes.c_int, [_ctxp, _fp, _dp, _dp, ctypes.c_uint64, ctypes.c_int64, _fp, _dp, _dp, _ip]),
         "srmra_mom_set_moments": (ctypes.c_int, [_ctxp, _dp, _dp]),
         "srmra_mom_objective": (ctypes.c_int, [_ctxp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
         "srmra_mom_run": (ctypes.c_int, [_ctxp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _dp, _ip]),
@@ -129,14 +131,22 @@ def srmra_nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, opt: srmra_options | None = None):
-    """Returns the opaque context handle (int).  y: float32 [n][L_low][L_low] host array."""
-    y = np.ascontiguousarray(y, dtype=np.float32)
+def srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, opt: srmra_options | None = None,
+               n_local: int | None = None):
+    """Returns the opaque context handle (int).  y: float32 [n][L_low][L_low] host array, or None with
+    n_local given (observations to come from srmra_generate / srmra_load)."""
+    if y is None:
+        if n_local is None:
+            raise ValueError("y is None: pass n_local")
+        yp, n = None, int(n_local)
+    else:
+        y = np.ascontiguousarray(y, dtype=np.float32)
+        yp, n = _ptr(y, _fp), int(y.shape[0])
     x0 = np.ascontiguousarray(x0, dtype=np.float32)
     r1 = np.ascontiguousarray(rho1_0, dtype=np.float64)
     r2 = np.ascontiguousarray(rho2_0, dtype=np.float64)
     h = _ctxp()
-    rc = _lib.srmra_init(ctypes.byref(h), _ptr(y, _fp), int(y.shape[0]), int(L_high), int(L_low), int(K),
+    rc = _lib.srmra_init(ctypes.byref(h), yp, n, int(L_high), int(L_low), int(K),
                          float(sigma), _ptr(x0, _fp), _ptr(r1, _dp), _ptr(r2, _dp),
                          ctypes.byref(opt) if opt is not None else None)
     _check(rc, None)
@@ -148,6 +158,29 @@ def srmra_load(ctx, y, x0, rho1_0, rho2_0):
     _check(_lib.srmra_load(ctx, _ptr(y, _fp), _ptr(np.ascontiguousarray(x0, dtype=np.float32), _fp),
                            _ptr(np.ascontiguousarray(rho1_0, dtype=np.float64), _dp),
                            _ptr(np.ascontiguousarray(rho2_0, dtype=np.float64), _dp)), ctx)
+
+
+def srmra_generate(ctx, x_true, rho1_true, rho2_true, seed: int, first_index: int, x0, rho1_0, rho2_0,
+                   n_local: int, want_shifts: bool = False):
+    """Device-generated observations (NEXT-4; synth/philox.py is the reference) + theta_0, like srmra_load.
+    Returns the shifts (int32 [n_local][2]) if want_shifts."""
+    xt = np.ascontiguousarray(x_true, dtype=np.float32)
+    t1 = np.ascontiguousarray(rho1_true, dtype=np.float64)
+    t2 = np.ascontiguousarray(rho2_true, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0, dtype=np.float32)
+    r1 = np.ascontiguousarray(rho1_0, dtype=np.float64)
+    r2 = np.ascontiguousarray(rho2_0, dtype=np.float64)
+    sh = np.empty((n_local, 2), dtype=np.int32) if want_shifts else None
+    _check(_lib.srmra_generate(ctx, _ptr(xt, _fp), _ptr(t1, _dp), _ptr(t2, _dp), ctypes.c_uint64(int(seed) & (2 ** 64 - 1)),
+                               int(first_index), _ptr(x0, _fp), _ptr(r1, _dp), _ptr(r2, _dp),
+                               _ptr(sh, _ip) if sh is not None else None), ctx)
+    return sh
+
+
+def srmra_get_observations(ctx, first: int, count: int, L_low: int):
+    out = np.empty((count, L_low, L_low), dtype=np.float32)
+    _check(_lib.srmra_get_observations(ctx, int(first), int(count), _ptr(out, _fp)), ctx)
+    return out
 
 
 def srmra_em_iter(ctx, n_iters: int = 1):
@@ -312,7 +345,8 @@ class Context:
 
     def __init__(self, y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, path="auto", proj_every=1,
                  floor_tau=-1.0, device=-1, rank=0, world=1, nccl_id: bytes | None = None, stream=None,
-                 trace_cap=4096):
+                 trace_cap=4096, n_local: int | None = None):
+        """y None: n_local observations to come from generate() / load()."""
         o = srmra_default_options()
         o.path = PATH_IDS[path] if isinstance(path, str) else int(path)
         o.proj_every = int(proj_every)
@@ -326,12 +360,21 @@ class Context:
         o.stream = stream
         o.trace_cap = int(trace_cap)
         self.L_high, self.L_low, self.K = int(L_high), int(L_low), int(K)
-        self.n_local = int(np.asarray(y).shape[0])
-        self.handle = srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, o)
+        self.n_local = int(np.asarray(y).shape[0]) if y is not None else int(n_local)
+        self.handle = srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, o, n_local=self.n_local)
 
     @property
     def path(self) -> str:
         return PATH_NAMES[srmra_get_path(self.handle)]
+
+    def generate(self, x_true, rho1_true, rho2_true, seed, x0, rho1_0, rho2_0, first_index=0, want_shifts=False):
+        """Observations drawn on the device (counter-based; synth/philox.py is the reference) + theta_0."""
+        return srmra_generate(self.handle, x_true, rho1_true, rho2_true, seed, first_index, x0, rho1_0, rho2_0,
+                              self.n_local, want_shifts)
+
+    def observations(self, first=0, count=None):
+        count = self.n_local - first if count is None else count
+        return srmra_get_observations(self.handle, first, count, self.L_low)
 
     def load(self, y, x0, rho1_0, rho2_0):
         """Replace the observations (same n_local as at init: srmra_load takes no size) and theta."""

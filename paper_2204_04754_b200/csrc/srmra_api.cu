@@ -118,15 +118,18 @@ int choose_path(int requested, int L, int Ll, int K) {
     return -1;
 }
 
-// Upload y and theta_0 (host) and run the per-observation init kernels.
+// Upload y and theta_0 (host) and run the per-observation init kernels.  ysrc: Y_HOST = host y,
+// Y_DEVICE = y already in d_y (srmra_generate), Y_NONE = no observations yet (srmra_init with y NULL:
+// d_y zeroed, the context needs srmra_load / srmra_generate before iterating).
+enum { Y_HOST = 0, Y_DEVICE = 1, Y_NONE = 2 };
 int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<double>& r1,
-           const std::vector<double>& r2) {
+           const std::vector<double>& r2, int ysrc = Y_HOST) {
     const size_t ny = (size_t)c->n_local * c->Ll2;
     // pinned caller buffers give an asynchronous DMA; pageable ones are staged by the driver.  FFT path:
     // y goes over in ~4 MB chunks on the copy stream and each chunk's init kernels (||y_i||^2, Yhat_i)
     // run on the context stream as soon as it has landed, overlapping the transfer
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));  // before k_ynorm may set bit 1
-    const bool chunked = c->path == SRMRA_PATH_FFT && c->copy_stream && ny;
+    const bool chunked = ysrc == Y_HOST && c->path == SRMRA_PATH_FFT && c->copy_stream && ny;
     if (chunked) {
         const int64_t per = std::max<int64_t>(1, (int64_t)(4 << 20) / (int64_t)(sizeof(float) * c->Ll2));
         for (int64_t o = 0; o < c->n_local; o += per) {
@@ -138,8 +141,10 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
             CK(launch_init_obs(c, o, m));
             CK(launch_fft_init(c, o, m));
         }
-    } else if (ny) {
+    } else if (ny && ysrc == Y_HOST) {
         CK(cudaMemcpyAsync(c->d_y, y, sizeof(float) * ny, cudaMemcpyHostToDevice, c->stream));
+    } else if (ny && ysrc == Y_NONE) {
+        CK(cudaMemsetAsync(c->d_y, 0, sizeof(float) * ny, c->stream));
     }
     std::vector<double> x64(c->L2), rho(2 * c->L);
     for (int k = 0; k < c->L2; ++k) x64[k] = (double)x0[k];
@@ -167,7 +172,7 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
         CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
         return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
     }
-    c->needs_load = false;
+    c->needs_load = ysrc == Y_NONE && c->n_local > 0;
     return SRMRA_OK;
 }
 
@@ -415,7 +420,7 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
         return fail(c, SRMRA_ERR_INVALID_ARG, "sizes must be positive (n_local >= 0)");
     if ((int64_t)K * L_low != L_high) return fail(c, SRMRA_ERR_INVALID_ARG, "K * L_low != L_high");
     if (!(sigma > 0) || !isfinite(sigma)) return fail(c, SRMRA_ERR_INVALID_ARG, "sigma must be finite and > 0");
-    if (!x0 || !rho1_0 || !rho2_0 || (n_local > 0 && !y)) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
+    if (!x0 || !rho1_0 || !rho2_0) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(c, SRMRA_ERR_INVALID_ARG, "bad rank/world");
     if (opt.world > 1 && !opt.nccl_id) return fail(c, SRMRA_ERR_INVALID_ARG, "world > 1 needs nccl_id");
     if (opt.proj_every < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "proj_every < 0");
@@ -559,7 +564,7 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     }
     c->tau = opt.floor_tau >= 0 ? opt.floor_tau : 1e-12 * (double)c->n_global;
 
-    if ((rc = upload(c, y, x0, r1, r2)) != SRMRA_OK) return bail(rc);
+    if ((rc = upload(c, y, x0, r1, r2, y ? Y_HOST : Y_NONE)) != SRMRA_OK) return bail(rc);
     *out = c;
     return SRMRA_OK;
 }
@@ -575,12 +580,65 @@ int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1
     return upload(c, y, x0, r1, r2);
 }
 
+int srmra_generate(srmra_ctx* c, const float* x_true, const double* rho1_true, const double* rho2_true, uint64_t seed,
+                   int64_t first_index, const float* x0, const double* rho1_0, const double* rho2_0,
+                   int32_t* shifts_out) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (!x_true || !rho1_true || !rho2_true || !x0 || !rho1_0 || !rho2_0)
+        return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
+    if (first_index < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "first_index < 0");
+    if (!all_finite_f(x_true, (size_t)c->L2) || !all_finite_f(x0, (size_t)c->L2))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "x_true / x0 not finite");
+    std::vector<double> t1, t2, r1, r2;
+    if (check_rho(rho1_true, c->L, t1) || check_rho(rho2_true, c->L, t2) || check_rho(rho1_0, c->L, r1) ||
+        check_rho(rho2_0, c->L, r2))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "rho must be >= 0, finite and sum to 1 (within 1e-6)");
+    // inverse-CDF tables: sequential float64 partial sums of the caller's pmfs (as given, not renormalised)
+    std::vector<double> cdf(2 * c->L);
+    int last[2] = {0, 0};
+    for (int a = 0; a < 2; ++a) {
+        const double* r = a ? rho2_true : rho1_true;
+        double s = 0.0;
+        for (int k = 0; k < c->L; ++k) {
+            s += r[k];
+            cdf[a * c->L + k] = s;
+            if (r[k] > 0) last[a] = k;
+        }
+    }
+    const size_t bytes = sizeof(float) * c->L2 + sizeof(double) * 2 * c->L + sizeof(int) * 2 * (size_t)c->n_local;
+    unsigned char* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, bytes, c->stream));
+    double* d_cdf = reinterpret_cast<double*>(tmp);
+    float* d_x = reinterpret_cast<float*>(tmp + sizeof(double) * 2 * c->L);
+    int* d_sh = reinterpret_cast<int*>(tmp + sizeof(double) * 2 * c->L + sizeof(float) * c->L2);
+    cudaError_t e = cudaMemcpyAsync(d_cdf, cdf.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_x, x_true, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = launch_generate(c, d_x, d_cdf, last[0], last[1], seed, first_index, shifts_out ? d_sh : nullptr);
+    if (e == cudaSuccess && shifts_out && c->n_local > 0)
+        e = cudaMemcpyAsync(shifts_out, d_sh, sizeof(int) * 2 * (size_t)c->n_local, cudaMemcpyDeviceToHost, c->stream);
+    cudaFreeAsync(tmp, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);  // host tables go out of scope
+    if (e != cudaSuccess) return cuda_fail(c, e, "srmra_generate");
+    return upload(c, nullptr, x0, r1, r2, Y_DEVICE);
+}
+
+int srmra_get_observations(srmra_ctx* c, int64_t first, int64_t count, float* y_out) {
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (first < 0 || count < 0 || first + count > c->n_local || (count > 0 && !y_out))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "range outside [0, n_local) or NULL output");
+    if (count == 0) return SRMRA_OK;
+    CK(cudaMemcpyAsync(y_out, c->d_y + first * c->Ll2, sizeof(float) * count * c->Ll2, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SRMRA_OK;
+}
 
 int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
-    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "the last srmra_load was rejected; load valid data first");
+    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no valid observations (srmra_init with y NULL, or a rejected srmra_load): srmra_load / srmra_generate first");
     return iterate(c, n_iters, 0.0);
 }
 
@@ -588,7 +646,7 @@ int srmra_run(srmra_ctx* c, int32_t max_iters, double rel_tol) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (max_iters < 0 || !(rel_tol == rel_tol)) return fail(c, SRMRA_ERR_INVALID_ARG, "max_iters < 0 or rel_tol NaN");
-    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "the last srmra_load was rejected; load valid data first");
+    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no valid observations (srmra_init with y NULL, or a rejected srmra_load): srmra_load / srmra_generate first");
     int rc;
     if ((rc = sync_iters(c)) != SRMRA_OK) return rc;  // the run's first iteration index
     c->n_proj = 0;
@@ -674,7 +732,7 @@ int srmra_get_joint_rho(srmra_ctx* c, double* out) {
 int srmra_moments(srmra_ctx* c, double* m1, double* m2) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
-    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no observations loaded (the last srmra_load was rejected)");
+    if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no valid observations (srmra_init with y NULL, or a rejected srmra_load)");
     if (!m1 && !m2) return fail(c, SRMRA_ERR_INVALID_ARG, "both outputs NULL");
     std::string err;
     const int rc = moments(c, m1, m2, err);
@@ -691,7 +749,7 @@ int srmra_mom_set_moments(srmra_ctx* c, const double* m1, const double* m2) {
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if ((m1 == nullptr) != (m2 == nullptr)) return fail(c, SRMRA_ERR_INVALID_ARG, "m1 and m2: both or neither");
-    if (!m1 && c->needs_load) return fail(c, SRMRA_ERR_STATE, "no observations loaded (the last srmra_load was rejected)");
+    if (!m1 && c->needs_load) return fail(c, SRMRA_ERR_STATE, "no valid observations (srmra_init with y NULL, or a rejected srmra_load)");
     if (!mom_supported(c)) return fail(c, SRMRA_ERR_UNSUPPORTED, "moment objective compiled for L_low <= 64");
     if (m1) {
         for (int a = 0; a < c->Ll2; ++a)

@@ -135,6 +135,8 @@ cudaError_t launch_pack(srmra_ctx* c);          // colsum (+ Bhat) -> packed b |
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project);
 cudaError_t launch_x32_from_x64(srmra_ctx* c);   // after a denoiser hook changed x
 cudaError_t launch_shift_corr(srmra_ctx* c, const double* xref_dev, double* corr_dev);  // NEXT-4
+cudaError_t launch_generate(srmra_ctx* c, const float* x_dev, const double* cdf_dev, int last1, int last2,
+                            uint64_t seed, int64_t first, int* shifts_dev);  // NEXT-4 (k_synth.cu)
 int moments(srmra_ctx* c, double* m1, double* m2, std::string& err);  // NEXT-2 (k_moments.cu)
 int moments_dev(srmra_ctx* c, double* out_dev, std::string& err);     // same, left on the device
 bool mom_supported(const srmra_ctx* c);                                // k_mom_obj.cu: L_low <= 64
