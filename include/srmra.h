@@ -137,9 +137,10 @@ SRMRA_API int srmra_em_iter(srmra_ctx* ctx, int32_t n_iters);
 /* NEXT-3: a joint (non-separable) shift prior rho[s1 L_high + s2] (host, float64, [L_high][L_high],
  * >= 0, summing to 1 within 1e-6; copied) replaces (rho1, rho2) in eq:weights_EM, and the M-step
  * becomes eq:rho_EM as written: rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'};
- * srmra_get_estimate then reports its marginals.  GEMM and direct paths only (the FFT kernels
- * accumulate the marginals, not every shift's posterior mass): UNSUPPORTED elsewhere.  A later
- * srmra_load returns the context to a separable prior. */
+ * srmra_get_estimate then reports its marginals.  All paths except the FFT path at L_low = 128
+ * (UNSUPPORTED there); on the FFT path the E/M kernel is re-planned with a per-CTA accumulator of every
+ * shift's posterior mass (possibly fewer thread groups per SM).  Synchronises.  A later srmra_load /
+ * srmra_generate / srmra_mom_run returns the context to a separable prior. */
 SRMRA_API int srmra_set_joint_rho(srmra_ctx* ctx, const double* rho);
 /* Copy the current joint prior [L_high][L_high] (STATE if none is set).  Synchronises. */
 SRMRA_API int srmra_get_joint_rho(srmra_ctx* ctx, double* out);

@@ -86,6 +86,8 @@ struct EmArgs {
     unsigned long long* emt;  // [cap][2] first-CTA start / last-CTA end of this launch (globaltimer), slot *iter
     const int* iter;          // device iteration counter (slot index)
     int emt_cap;
+    const float2* ljp;        // JOINT: log2 joint prior per pair [NP][LL n2][LL n1] = (class 2q, class 2q+1)
+    float* jpart;             // JOINT: per-CTA posterior mass per shift [gridDim.x][KK][LL t1][LL t2]
 };
 
 template <int LL>
@@ -130,6 +132,13 @@ __host__ __device__ inline size_t par_bytes(int KK) {
 template <int LL>
 __host__ __device__ inline size_t smem_bytes(int KK, int groups, int ystride) {
     return group_smem<LL>(KK, ystride) * groups + par_bytes<LL>(KK);
+}
+
+// JOINT (NEXT-3, eq:rho_EM as written): one per-CTA accumulator of the posterior mass of every shift,
+// JA [KK][LL][LL + 1] float (rows padded: the row threads of a warp add at the same n2 conflict-free)
+template <int LL>
+__host__ __device__ inline size_t joint_bytes(int KK) {
+    return ((size_t)KK * LL * (LL + 1) * sizeof(float) + 15) & ~(size_t)15;
 }
 
 // TACC (L_low >= 32): the M-step accumulators U_q / V_q (and the Yhat values of pass 0) live in tensor memory instead of the group's
@@ -225,7 +234,7 @@ __host__ __device__ inline size_t xs_bytes(int KK) {
     return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (LL / 2 + 1);
 }
 
-template <int LL, bool PAIRS, bool XS, bool TACC>
+template <int LL, bool PAIRS, bool XS, bool TACC, bool JOINT>
 __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArgs a) {
     using G = Geo<LL>;
     constexpr int LH = G::LH, WS = G::WS, M = LL - 1;
@@ -281,6 +290,11 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     if (TACC) tc::fence_after();
     const size_t per_g = TACC ? group_smem_t<LL>(KK, a.ystride) : group_smem<LL>(KK, a.ystride);
     const int PB = part_bins(KK, LL);
+    float* JA = reinterpret_cast<float*>(gbase + per_g * a.groups);  // JOINT accumulator (after the groups)
+    if (JOINT) {
+        for (int k = threadIdx.x; k < KK * LL * (LL + 1); k += blockDim.x) JA[k] = 0.f;
+        __syncthreads();
+    }
     float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [2][ystride]
     float2* Wk = Yb + 2 * a.ystride;                                    // [NP][LL][WS]
     // TACC: zc | yc | red after Wk, the partial staged over Yb (at the end); else Acc [PB] | red
@@ -325,8 +339,9 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     float2* Vq = Uq + (size_t)LL * LH;
     const int ra2 = ra % K, rb2 = rb % K;
     // logit bias (log2 units) of this thread's row n1 = idx, per class
-    const float biasA = line_ok ? lr1[ra / K + K * idx] + beta[ra] : 0.f;
-    const float biasB = (line_ok && has_b) ? lr1[rb / K + K * idx] + beta[rb] : 0.f;
+    // (JOINT: the class bias only; the whole log prior comes from the per-shift table ljp)
+    const float biasA = line_ok ? (JOINT ? 0.f : lr1[ra / K + K * idx]) + beta[ra] : 0.f;
+    const float biasB = (line_ok && has_b) ? (JOINT ? 0.f : lr1[rb / K + K * idx]) + beta[rb] : 0.f;
 
     // per-thread accumulators over this group's observations
     float rsumA = 0.f, rsumB = 0.f;     // row sums of w (class ra / rb, row idx)
@@ -489,7 +504,9 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
 #pragma unroll
                     for (int n2 = 0; n2 < LL; ++n2) {
                         float2 b2;
-                        if constexpr (LL >= 2) {
+                        if constexpr (JOINT) {
+                            b2 = __ldg(a.ljp + ((size_t)q * LL + n2) * LL + idx);
+                        } else {
                             const float4 l4 = lq[n2 >> 1];
                             b2 = (n2 & 1) ? make_float2(l4.z, l4.w) : make_float2(l4.x, l4.y);
                         }
@@ -521,6 +538,15 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     rsumB = fmaf(zb, f, rsumB);
 #pragma unroll
                     for (int n2 = 0; n2 < LL; ++n2) v[n2] = make_float2(v[n2].x * f, v[n2].y * f);
+                    if constexpr (JOINT) {  // posterior mass of the shifts (ra | rb, t1 = idx, t2 = n2)
+                        float* ja = JA + ((size_t)ra * LL + idx) * (LL + 1);
+                        float* jb = JA + ((size_t)rb * LL + idx) * (LL + 1);
+#pragma unroll
+                        for (int n2 = 0; n2 < LL; ++n2) {
+                            atomicAdd(ja + n2, v[n2].x);
+                            if (has_b) atomicAdd(jb + n2, v[n2].y);
+                        }
+                    }
                 }
             }
             if (pass == 0) {
@@ -594,6 +620,13 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
         }
         dst[k] = s;
     }
+    if (JOINT) {
+        float* jd = a.jpart + (size_t)blockIdx.x * KK * LL * LL;
+        for (int k = threadIdx.x; k < KK * LL * LL; k += blockDim.x) {
+            const int row = k / LL, c = k - row * LL;
+            jd[k] = JA[row * (LL + 1) + c];
+        }
+    }
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int gg = 0; gg < a.groups; ++gg) {
@@ -641,20 +674,21 @@ bool fft_supported(int L, int Ll, int K) {
     return true;
 }
 
-template <int LL, bool TACC>
+template <int LL, bool TACC, bool JOINT>
 static auto em_kernel(int KK, bool xs) {
-    return (KK % 2 == 0) ? (xs ? k_fft_em<LL, true, true, TACC> : k_fft_em<LL, true, false, TACC>)
-                         : (xs ? k_fft_em<LL, false, true, TACC> : k_fft_em<LL, false, false, TACC>);
+    return (KK % 2 == 0) ? (xs ? k_fft_em<LL, true, true, TACC, JOINT> : k_fft_em<LL, true, false, TACC, JOINT>)
+                         : (xs ? k_fft_em<LL, false, true, TACC, JOINT> : k_fft_em<LL, false, false, TACC, JOINT>);
 }
 
-template <int LL, bool TACC>
+template <int LL, bool TACC, bool JOINT>
 static cudaError_t plan_em_tt(srmra_ctx* c) {
     const int KK = c->KK;
     const int GT = group_threads<LL>(KK);
     const int ys = ystride_of(LL);
     constexpr int MAXT = max_cta_threads<LL, TACC>();
     if (GT > MAXT) return cudaErrorInvalidConfiguration;
-    auto gsm = [&](int g) { return (TACC ? group_smem_t<LL>(KK, ys) : group_smem<LL>(KK, ys)) * g + par_bytes<LL>(KK); };
+    const size_t jb = JOINT ? joint_bytes<LL>(KK) : 0;
+    auto gsm = [&](int g) { return (TACC ? group_smem_t<LL>(KK, ys) : group_smem<LL>(KK, ys)) * g + par_bytes<LL>(KK) + jb; };
     int groups = MAXT / GT;
     if (groups > 15) groups = 15;
     const char* eg = getenv("SRMRA_FFT_GROUPS");  // tuning override
@@ -675,7 +709,7 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     if (need < groups) groups = (int)(need < 1 ? 1 : need);
     const size_t smem = gsm(groups) + (xs ? xsb : 0);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    auto kern = em_kernel<LL, TACC>(KK, xs);
+    auto kern = em_kernel<LL, TACC, JOINT>(KK, xs);
     c->fft_xs = xs;
     c->fft_tacc = TACC;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -696,24 +730,30 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     int64_t grid = (int64_t)c->num_sms * per_sm;
     const int64_t max_grid = (c->n_local + groups - 1) / groups;
     if (grid > max_grid) grid = max_grid;
+    if (c->fft_part_cap > 0 && grid > c->fft_part_cap) grid = c->fft_part_cap;  // partial buffers of the first plan
     if (grid < 1) grid = 1;
     c->fft_grid = (int)grid;
+    c->fft_joint = JOINT;
     c->fft_groups = groups;
     c->fft_threads = GT * groups;
     c->fft_smem = smem;
     return cudaSuccess;
 }
 
-template <int LL>
-static cudaError_t plan_em_t(srmra_ctx* c) {
+template <int LL, bool JOINT>
+static cudaError_t plan_em_tj(srmra_ctx* c) {
     // tensor-memory accumulators where the staged partial fits (L_low >= 32); SRMRA_FFT_TACC=0 disables
     const char* et = getenv("SRMRA_FFT_TACC");
     const bool tacc_ok = LL >= 32 && tacc_fits<LL>(c->KK, ystride_of(LL)) && !(et && atoi(et) == 0);
     if constexpr (LL >= 32) {
-        if (tacc_ok && plan_em_tt<LL, true>(c) == cudaSuccess) return cudaSuccess;
+        if (tacc_ok && plan_em_tt<LL, true, JOINT>(c) == cudaSuccess) return cudaSuccess;
         cudaGetLastError();
     }
-    return plan_em_tt<LL, false>(c);
+    return plan_em_tt<LL, false, JOINT>(c);
+}
+template <int LL>
+static cudaError_t plan_em_t(srmra_ctx* c) {
+    return c->fft_joint ? plan_em_tj<LL, true>(c) : plan_em_tj<LL, false>(c);
 }
 
 template <int LL>
@@ -741,14 +781,20 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     a.emt = c->d_emt;
     a.iter = c->d_iter;
     a.emt_cap = c->opt.trace_cap;
+    a.ljp = c->d_ljp;
+    a.jpart = c->d_jpart;
+#define SRMRA_EM_LAUNCH(T, J)                                                                                        \
+    em_kernel<LL, T, J>(c->KK, c->fft_xs)<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a); \
+    return cudaGetLastError()
     if constexpr (LL >= 32) {
         if (c->fft_tacc) {
-            em_kernel<LL, true>(c->KK, c->fft_xs)<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
-            return cudaGetLastError();
+            if (c->fft_joint) { SRMRA_EM_LAUNCH(true, true); }
+            SRMRA_EM_LAUNCH(true, false);
         }
     }
-    em_kernel<LL, false>(c->KK, c->fft_xs)<<<(unsigned)c->fft_grid, c->fft_threads, c->fft_smem, c->stream>>>(a);
-    return cudaGetLastError();
+    if (c->fft_joint) { SRMRA_EM_LAUNCH(false, true); }
+    SRMRA_EM_LAUNCH(false, false);
+#undef SRMRA_EM_LAUNCH
 }
 
 int fft_partial_bins(int KK, int Ll) { return part_bins(KK, Ll); }
@@ -769,10 +815,30 @@ size_t fft_part_float2(const srmra_ctx* c) { return (size_t)c->fft_grid * fft_pa
         default: return cudaErrorInvalidValue;   \
     }
 
+static cudaError_t fft_plan_ll(srmra_ctx* c) { SRMRA_LL_DISPATCH(plan_em_t, c) }
+
 cudaError_t fft_plan(srmra_ctx* c) {
     if (c->Ll == 128) return fft128_plan(c);
-    SRMRA_LL_DISPATCH(plan_em_t, c)
+    const cudaError_t e = fft_plan_ll(c);
+    if (e == cudaSuccess && c->fft_part_cap == 0) c->fft_part_cap = c->fft_grid;
+    return e;
 }
+
+// NEXT-3 on the FFT path (L_low <= 64): re-plan the E/M kernel with / without the joint-prior accumulator
+// (fewer groups may fit; the grid stays within the partial buffers of the first plan)
+cudaError_t fft_plan_joint(srmra_ctx* c, bool joint) {
+    if (c->Ll == 128) return cudaErrorNotSupported;
+    const bool old = c->fft_joint;
+    c->fft_joint = joint;
+    const cudaError_t e = fft_plan_ll(c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c->fft_joint = old;
+        fft_plan_ll(c);
+    }
+    return e;
+}
+size_t fft_joint_bins(int KK, int Ll) { return (size_t)KK * Ll * Ll; }
 
 cudaError_t launch_fft_em(srmra_ctx* c) {
     if (c->n_local == 0) return cudaSuccess;

@@ -26,6 +26,7 @@ namespace cg = cooperative_groups;
 namespace srmra {
 
 int fft_partial_bins(int KK, int Ll);
+size_t fft_joint_bins(int KK, int Ll);
 
 namespace ffttail {
 using namespace dft64;
@@ -57,6 +58,12 @@ struct TailArgs {
     int* run;                 // srmra_run control: [0] stop flag (set here on convergence), [1] first t of the run
     const double* rtol;       // convergence tolerance of the run (0: none)
     int proj_every;           // F of Algorithm 2 (project after t when (t+1) % F == 0; 0 = never)
+    // NEXT-3 joint prior (eq:rho_EM as written): per-CTA posterior mass per shift -> jacc -> rho'[s]
+    int joint, JB;            // JB = KK Ll^2 bins [r][t1][t2]
+    const float* jpart;       // [nparts][JB]
+    double* jacc;             // [JB]
+    double* rhoj;             // [L][L]
+    float2* ljp;              // [NP][Ll n2][Ll n1] log2 rho of (class 2q, class 2q+1)
 };
 
 __device__ inline void grid_sync() { cg::this_grid().sync(); }
@@ -96,6 +103,29 @@ __device__ void phase_reduce(const TailArgs& a) {
             a.acc[2 * k + 1] = ty;
         }
         __syncthreads();
+    }
+    if (a.joint) {  // joint prior: the per-shift posterior mass, same fixed-order scheme (real bins)
+        __shared__ double redj[kSlices][33];
+        for (int base = blockIdx.x * 32; base < a.JB; base += gridDim.x * 32) {
+            const int k = base + b;
+            double sx[4] = {0, 0, 0, 0};
+            if (k < a.JB) {
+                int c = sl;
+                for (; c + 3 * kSlices < a.nparts; c += 4 * kSlices) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) sx[u] += __ldcg(a.jpart + (size_t)(c + u * kSlices) * a.JB + k);
+                }
+                for (; c < a.nparts; c += kSlices) sx[0] += __ldcg(a.jpart + (size_t)c * a.JB + k);
+            }
+            redj[sl][b] = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+            __syncthreads();
+            if (sl == 0 && k < a.JB) {
+                double tx = 0.0;
+                for (int j = 0; j < kSlices; ++j) tx += redj[j][b];
+                a.jacc[k] = tx;
+            }
+            __syncthreads();
+        }
     }
     if (blockIdx.x == 0 && sl == 1) {  // LL partials: strided lanes then a fixed-order shuffle tree
         double s = 0.0;
@@ -206,7 +236,36 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                 a.pack[a.off_m1 + s] = a1;
                 a.pack[a.off_m2 + s] = a2 * invL;
             }
-            if (update) {
+            if (update && a.joint) {
+                // eq:rho_EM as written: rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'} (zero prior mass stays
+                // zero); the reported marginals are its row / column sums
+                __syncthreads();
+                double tot = 0.0;
+                for (int s = threadIdx.x; s < L * L; s += blockDim.x) {
+                    const int s1 = s / L, s2 = s - s1 * L;
+                    const int jb = ((s1 % K) * K + s2 % K) * Ll * Ll + (s1 / K) * Ll + s2 / K;
+                    tot += a.rhoj[s] == 0.0 ? 0.0 : fmax(__ldcg(a.jacc + jb), 0.0);
+                }
+                tot = block_sum(tot, red);
+                __syncthreads();
+                if (tot > 0.0) {
+                    for (int s = threadIdx.x; s < L * L; s += blockDim.x) {
+                        const int s1 = s / L, s2 = s - s1 * L;
+                        const int jb = ((s1 % K) * K + s2 % K) * Ll * Ll + (s1 / K) * Ll + s2 / K;
+                        a.rhoj[s] = a.rhoj[s] == 0.0 ? 0.0 : fmax(__ldcg(a.jacc + jb), 0.0) / tot;
+                    }
+                }
+                __syncthreads();
+                for (int k = threadIdx.x; k < L; k += blockDim.x) {
+                    double r1 = 0.0, r2 = 0.0;
+                    for (int j = 0; j < L; ++j) {
+                        r1 += a.rhoj[(size_t)k * L + j];
+                        r2 += a.rhoj[(size_t)j * L + k];
+                    }
+                    a.rho[k] = r1;
+                    a.rho[L + k] = r2;
+                }
+            } else if (update) {
                 // eq:rho_EM marginals; zero prior mass stays exactly zero; per-axis normalisation
                 __syncthreads();  // this block's marginal writes visible to the block
                 double m1s = 0.0, m2s = 0.0;
@@ -223,17 +282,17 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                         a.rho[L + k] = a.rho[L + k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m2 + k], 0.0) / m2s;
                     }
                 }
-                if (threadIdx.x == 0) {
-                    const double ll = a.pack[a.off_ll];
-                    if (a.t < a.trace_cap) a.trace[a.t] = ll;
-                    bad |= !isfinite(ll);
-                    // Algorithm 2 stopping rule (srmra_run): |LL_t - LL_{t-1}| <= rtol |LL_t| for t >= run start + 1;
-                    // the remaining enqueued iterations of the run become no-ops
-                    const double rt = *a.rtol;
-                    if (rt > 0.0 && a.t - a.run[1] >= 1 && a.t - 1 < a.trace_cap &&
-                        fabs(ll - a.trace[a.t - 1]) <= rt * fabs(ll))
-                        a.run[0] = 1;
-                }
+            }
+            if (update && threadIdx.x == 0) {
+                const double ll = a.pack[a.off_ll];
+                if (a.t < a.trace_cap) a.trace[a.t] = ll;
+                bad |= !isfinite(ll);
+                // Algorithm 2 stopping rule (srmra_run): |LL_t - LL_{t-1}| <= rtol |LL_t| for t >= run start + 1;
+                // the remaining enqueued iterations of the run become no-ops
+                const double rt = *a.rtol;
+                if (rt > 0.0 && a.t - a.run[1] >= 1 && a.t - 1 < a.trace_cap &&
+                    fabs(ll - a.trace[a.t - 1]) <= rt * fabs(ll))
+                    a.run[0] = 1;
             }
         }
     }
@@ -334,6 +393,21 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                 const double p1 = __ldcg(a.rho + k), p2 = __ldcg(a.rho + L + k);
                 a.par32[k] = p1 > 0.0 ? (float)log2(p1) : -INFINITY;
                 a.par32[L + k] = p2 > 0.0 ? (float)log2(p2) : -INFINITY;
+            }
+            if (a.joint) {  // per-shift log2 prior, pair-interleaved [q][n2][n1] (the E/M kernel's JOINT table)
+                const int NPq = (KK + 1) / 2;
+                for (int e = threadIdx.x; e < NPq * Ll * Ll; e += blockDim.x) {
+                    const int qq = e / (Ll * Ll), rem = e - qq * Ll * Ll, n2 = rem / Ll, n1 = rem - n2 * Ll;
+                    float lv[2] = {0.f, 0.f};
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = 2 * qq + h;
+                        if (r >= KK) break;
+                        const int s1 = r / K + K * n1, s2 = r % K + K * n2;
+                        const double pv = __ldcg(a.rhoj + (size_t)s1 * L + s2);
+                        lv[h] = pv > 0.0 ? (float)log2(pv) : -INFINITY;
+                    }
+                    a.ljp[e] = make_float2(lv[0], lv[1]);
+                }
             }
         }
     }
@@ -438,6 +512,12 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     a.xhat = c->d_xhat;
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
+    a.joint = c->fft_joint ? 1 : 0;
+    a.JB = (int)fft_joint_bins(c->KK, Ll);
+    a.jpart = c->d_jpart;
+    a.jacc = c->d_jacc;
+    a.rhoj = c->d_rhoj;
+    a.ljp = c->d_ljp;
     a.nchunk = Ll >= 8 ? Ll / 8 : 1;
     a.wq = (Lh + a.nchunk - 1) / a.nchunk;
     a.nchunk_q = (Lh + a.wq - 1) / a.wq;

@@ -118,6 +118,28 @@ int choose_path(int requested, int L, int Ll, int K) {
     return -1;
 }
 
+// The captured FFT iteration bakes in the E/M kernel instantiation: drop it when that changes.
+void drop_graphs(srmra_ctx* c) {
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->graph_prof) cudaGraphExecDestroy(c->graph_prof);
+    if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
+    c->graph = nullptr;
+    c->graph_prof = nullptr;
+    c->graph_prof_src = nullptr;
+    for (int k = 0; k < 4; ++k) c->prof_nodes[k] = nullptr;
+    c->graph_failed = false;
+}
+
+// FFT path: switch the E/M kernel between the separable and the joint-prior variant (NEXT-3)
+int fft_joint_mode(srmra_ctx* c, bool on) {
+    if (c->path != SRMRA_PATH_FFT || c->fft_joint == on) return SRMRA_OK;
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graphs(c);
+    const cudaError_t e = fft_plan_joint(c, on);
+    if (e != cudaSuccess) return fail(c, SRMRA_ERR_UNSUPPORTED, std::string("FFT joint-prior plan: ") + cudaGetErrorString(e));
+    return SRMRA_OK;
+}
+
 // Upload y and theta_0 (host) and run the per-observation init kernels.  ysrc: Y_HOST = host y,
 // Y_DEVICE = y already in d_y (srmra_generate), Y_NONE = no observations yet (srmra_init with y NULL:
 // d_y zeroed, the context needs srmra_load / srmra_generate before iterating).
@@ -154,6 +176,10 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
     c->joint = false;  // (rho1, rho2): a separable prior again
+    {
+        const int rcj = fft_joint_mode(c, false);
+        if (rcj != SRMRA_OK) return rcj;
+    }
     CK(cudaMemsetAsync(c->d_run, 0, 2 * sizeof(int), c->stream));
     CK(cudaMemsetAsync(c->d_rtol, 0, sizeof(double), c->stream));
     c->n_proj = 0;
@@ -186,6 +212,11 @@ int allreduce_stats(srmra_ctx* c) {
     const size_t n = c->path == SRMRA_PATH_FFT ? fft_bhat_doubles(c->KK, c->Ll) : (size_t)c->pk.total;
     ncclResult_t r = api.AllReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
     if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    if (c->path == SRMRA_PATH_FFT && c->fft_joint) {  // + the per-shift posterior mass of the joint prior
+        r = api.AllReduce(c->d_jacc, c->d_jacc, fft_joint_bins(c->KK, c->Ll), ncclFloat64, ncclSum,
+                          (ncclComm_t)c->nccl_comm, c->stream);
+        if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+    }
     return SRMRA_OK;
 }
 
@@ -692,8 +723,8 @@ int srmra_relative_error(srmra_ctx* c, const float* x_true, double* err_out, int
 int srmra_set_joint_rho(srmra_ctx* c, const double* rho) {
     if (!c || !rho) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
-    if (c->path != SRMRA_PATH_GEMM && c->path != SRMRA_PATH_DIRECT)
-        return fail(c, SRMRA_ERR_UNSUPPORTED, "joint shift prior: GEMM and direct paths only (init with path = gemm | direct)");
+    if (c->path == SRMRA_PATH_FFT && c->Ll > 64)
+        return fail(c, SRMRA_ERR_UNSUPPORTED, "joint shift prior on the FFT path: L_low <= 64 (init with path = gemm | direct)");
     std::vector<double> r(rho, rho + c->L2);
     double s = 0.0;
     for (double v : r) {
@@ -713,9 +744,23 @@ int srmra_set_joint_rho(srmra_ctx* c, const double* rho) {
         CK(cudaMalloc(&c->d_rhoj, sizeof(double) * c->L2));
         CK(cudaMalloc(&c->d_lrj, sizeof(float) * c->L2));
     }
+    if (c->path == SRMRA_PATH_FFT && !c->d_ljp) {
+        CK(cudaMalloc(&c->d_ljp, sizeof(float2) * ((c->KK + 1) / 2) * (size_t)c->Ll * c->Ll));
+        CK(cudaMalloc(&c->d_jpart, sizeof(float) * (size_t)std::max(1, c->fft_part_cap) * fft_joint_bins(c->KK, c->Ll)));
+        CK(cudaMalloc(&c->d_jacc, sizeof(double) * fft_joint_bins(c->KK, c->Ll)));
+    }
     CK(cudaMemcpyAsync(c->d_rhoj, r.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_rho, marg.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (c->path == SRMRA_PATH_FFT) {
+        int rc;
+        if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
+        if ((rc = fft_joint_mode(c, true)) != SRMRA_OK) return rc;
+        c->joint = true;
+        CK(launch_fft_tail(c, TAIL_PREP, c->iters_done, 0));  // the per-shift log2 prior table of the E/M kernel
+        CK(cudaStreamSynchronize(c->stream));
+        return SRMRA_OK;
+    }
     c->joint = true;
     return SRMRA_OK;
 }
@@ -784,6 +829,7 @@ int srmra_mom_run(srmra_ctx* c, int32_t max_steps, int32_t F, double gtol, doubl
     if (steps_out) *steps_out = steps;
     if (rc != SRMRA_OK) return mom_fail(c, rc, err);
     c->joint = false;  // the estimate is (x, rho1, rho2) again
+    if ((rc = fft_joint_mode(c, false)) != SRMRA_OK) return rc;
     if ((rc = refresh_after_denoise(c)) != SRMRA_OK) return rc;  // EM can continue from the MoM estimate
     CK(cudaStreamSynchronize(c->stream));
     return SRMRA_OK;
@@ -971,6 +1017,9 @@ void srmra_free(srmra_ctx* c) {
     if (c->d_run) cudaFree(c->d_run);
     if (c->d_emt) cudaFree(c->d_emt);
     if (c->d_rhoj) cudaFree(c->d_rhoj);
+    if (c->d_ljp) cudaFree(c->d_ljp);
+    if (c->d_jpart) cudaFree(c->d_jpart);
+    if (c->d_jacc) cudaFree(c->d_jacc);
     mom_free(c);
     if (c->d_lrj) cudaFree(c->d_lrj);
     if (c->d_rtol) cudaFree(c->d_rtol);

@@ -76,6 +76,11 @@ struct srmra_ctx {
     int fft_grid = 0, fft_groups = 0, fft_threads = 0;
     bool fft_xs = false;        // Xhat staged in shared memory by the E/M kernel
     bool fft_tacc = false;      // E/M kernel keeps the M-step accumulators in tensor memory
+    bool fft_joint = false;     // E/M kernel planned with the joint-prior accumulator (NEXT-3)
+    int fft_part_cap = 0;       // CTAs the partial buffers were sized for (first plan)
+    float2* d_ljp = nullptr;    // NEXT-3, FFT path: log2 joint prior per class pair [NP][Ll n2][Ll n1]
+    float* d_jpart = nullptr;   // NEXT-3, FFT path: per-CTA posterior mass per shift [fft_part_cap][KK Ll^2]
+    double* d_jacc = nullptr;   // NEXT-3, FFT path: its fixed-order float64 sum [KK Ll^2]
     int fft_tmem_cols = 0;      // tensor-memory columns per CTA (fft_tacc)
     size_t fft_smem = 0;
     double* d_pack = nullptr;   // packed statistics, see PackLayout
@@ -175,6 +180,8 @@ int fft_launches_per_iter(const srmra_ctx* c);
 size_t fft_bhat_doubles(int KK, int Ll);  // Bhat [KK][Ll][Lh] complex + mass lines [KK][Ll+Lh] complex
 size_t fft_yhat_stride(int Ll);           // float2 per observation in d_yhat (16-byte multiple)
 cudaError_t fft_plan(srmra_ctx* c);       // grid / groups / smem of the E/M kernel for this shard
+cudaError_t fft_plan_joint(srmra_ctx* c, bool joint);  // re-plan with / without the joint-prior accumulator
+size_t fft_joint_bins(int KK, int Ll);
 size_t fft_part_float2(const srmra_ctx* c);
 size_t fft_xhat_float2(int KK, int Ll);   // pair-interleaved Xhat
 

@@ -1,5 +1,5 @@
-"""NEXT-3: the joint (non-separable) shift prior — eq:rho_EM as written — on the GEMM
-and direct paths against the oracle's joint iteration, element by element (tolerances of
+"""NEXT-3: the joint (non-separable) shift prior — eq:rho_EM as written — on the FFT
+(L_low <= 64), GEMM and direct paths against the oracle's joint iteration, element by element (tolerances of
 tests/test_gpu_parity.py; the joint prior uses the rho bound of reading R10)."""
 import numpy as np
 import pytest
@@ -26,7 +26,7 @@ def joint_prior(L, seed, zeros=0):
 
 
 CASES = [("c0", None, 0), ("rand8K2", (8, 2, 33, 0.3, 2), 5), ("rand4K4", (4, 4, 31, 0.25, 4), 3),
-         ("c1", 400, 0)]
+         ("c1", 400, 0), ("c3", 300, 0)]
 
 
 @pytest.mark.parametrize("name,spec,zeros", CASES, ids=[c[0] for c in CASES])
@@ -41,14 +41,16 @@ def test_joint_prior_iterations_vs_oracle(srm, oracle_mod, name, spec, zeros):
     # three chained iterations on the small shapes; one at the c1 geometry, where each of the 4096 joint
     # entries comes from 400 observations with no marginal averaging (chained, the direct path's fp32
     # sums reach 2e-4 by the third iteration)
-    iters = 1 if name == "c1" else 3
+    iters = 1 if name in ("c1", "c3") else 3
     x, rho = p.x0.astype(np.float64), pr
     trace = []
     for _ in range(iters):
         r = oracle_mod.em_iter_joint(p.y, p.L_low, p.K, p.sigma, x, rho, project=True)
         trace.append(r.loglik)
         x, rho = r.x, r.rho
-    for path in ("gemm", "direct"):
+    # c3 geometry (16 classes, 16384 joint entries from 300 observations): the FFT path only — the GEMM
+    # path's 3xTF32 scores put its smallest per-shift masses at 1.5e-4 of max rho there (bound 1e-4)
+    for path in (("fft",) if name == "c3" else ("fft", "gemm", "direct")):
         try:
             ctx = srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path)
         except srm.SrmraError:
@@ -68,34 +70,48 @@ def test_joint_prior_iterations_vs_oracle(srm, oracle_mod, name, spec, zeros):
         assert np.all(rg.reshape(-1)[pr.reshape(-1) == 0] == 0.0)   # zero prior mass stays zero
 
 
-def test_joint_prior_rejected_on_fft_path_and_reset_by_load(srm):
+def test_joint_prior_limits_and_reset_by_load(srm):
+    """FFT path at L_low = 128 (configs[4]) is rejected; srmra_load returns every path to the separable
+    prior (and the FFT path to its separable E/M kernel)."""
+    q = synth.make_config("c4", N=4)
+    with srm.Context(q.y, q.L_high, q.L_low, q.K, q.sigma, q.x0, q.rho1_0, q.rho2_0, path="fft") as ctx:
+        with pytest.raises(srm.SrmraError) as ei:
+            ctx.set_joint_rho(joint_prior(q.L_high, 1))
+        assert ei.value.code == srm.SRMRA_ERR_UNSUPPORTED
     p = synth.make_config("c0")
     L = p.L_high
-    with srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path="fft") as ctx:
-        with pytest.raises(srm.SrmraError) as ei:
+    for path in ("fft", "gemm"):
+        with srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path) as ctx:
+            ctx.em_iter(1)
+            ref = ctx.get_estimate()
             ctx.set_joint_rho(joint_prior(L, 1))
-        assert ei.value.code == srm.SRMRA_ERR_UNSUPPORTED
-    with srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path="gemm") as ctx:
-        ctx.set_joint_rho(joint_prior(L, 1))
-        ctx.load(p.y, p.x0, p.rho1_0, p.rho2_0)
-        with pytest.raises(srm.SrmraError) as ei:
-            ctx.joint_rho()
-        assert ei.value.code == srm.SRMRA_ERR_STATE
+            ctx.em_iter(2)
+            ctx.load(p.y, p.x0, p.rho1_0, p.rho2_0)
+            with pytest.raises(srm.SrmraError) as ei:
+                ctx.joint_rho()
+            assert ei.value.code == srm.SRMRA_ERR_STATE
+            ctx.em_iter(1)
+            again = ctx.get_estimate()
+        np.testing.assert_array_equal(again[0], ref[0])   # the separable iteration, bit for bit
+        np.testing.assert_array_equal(again[1], ref[1])
 
 
 def test_product_joint_prior_equals_separable(srm):
     """rho = rho1 rho2^T through the joint machinery gives the separable iteration (GPU vs GPU) — for one
     iteration: the joint update of the next prior is no longer a product."""
-    p = synth.make_config("c0")
-    L = p.L_high
-    outs = []
-    for joint in (False, True):
-        with srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path="gemm") as ctx:
-            if joint:
-                ctx.set_joint_rho(np.outer(p.rho1_0, p.rho2_0))
-            ctx.em_iter(1)
-            outs.append(ctx.get_estimate())
-    (xa, a1, a2, lla, _), (xb, b1, b2, llb, _) = outs
-    np.testing.assert_allclose(xb, xa, atol=1e-5 * np.abs(xa).max())
-    np.testing.assert_allclose(b1, a1, atol=1e-6)
-    assert abs(llb - lla) <= 1e-7 * abs(lla)
+    for name in ("c0", "c1"):
+        p = synth.make_config(name, N=2000 if name == "c1" else None)
+        L = p.L_high
+        for path in ("fft", "gemm"):
+            outs = []
+            for joint in (False, True):
+                with srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path) as ctx:
+                    if joint:
+                        ctx.set_joint_rho(np.outer(p.rho1_0, p.rho2_0))
+                    ctx.em_iter(1)
+                    outs.append(ctx.get_estimate())
+            (xa, a1, a2, lla, _), (xb, b1, b2, llb, _) = outs
+            np.testing.assert_allclose(xb, xa, atol=1e-5 * np.abs(xa).max())
+            np.testing.assert_allclose(b1, a1, atol=1e-6)
+            np.testing.assert_allclose(b2, a2, atol=1e-6)
+            assert abs(llb - lla) <= 1e-7 * abs(lla), (name, path)
