@@ -153,12 +153,9 @@ __global__ void k_finalize(const double* __restrict__ pack, int64_t off_cm, int6
 
 cudaError_t launch_finalize(srmra_ctx* c, int t, int project) {
     const size_t sm = c->L2 <= 16384 ? sizeof(double) * c->L2 : 0;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    cudaError_t e = attr.run([] { return cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 8); });
+    if (e != cudaSuccess) return e;
     k_finalize<<<1, 1024, sm, c->stream>>>(c->d_pack, c->pk.cmass, c->pk.m1, c->pk.m2, c->pk.ll, c->L, c->K,
                                           c->tau, project, c->d_x64, c->d_x32, c->d_rho, c->d_xtmp,
                                           c->d_trace, t, c->opt.trace_cap, c->d_flag, c->d_colsum,

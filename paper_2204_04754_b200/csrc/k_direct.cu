@@ -137,12 +137,9 @@ k_direct_em(const float* __restrict__ y, const double* __restrict__ ynorm, int64
 cudaError_t launch_direct_em(srmra_ctx* c) {
     if (c->n_local == 0) return cudaSuccess;
     const size_t smem = sizeof(float) * (4 * (size_t)c->L2 + c->Ll2 + 2 * c->L + c->KK);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_direct_em, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static PerDeviceOnce attr;
+    cudaError_t ea = attr.run([] { return cudaFuncSetAttribute(k_direct_em, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); });
+    if (ea != cudaSuccess) return ea;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_direct_em, kDirectThreads, smem);
     if (per_sm < 1) per_sm = 1;

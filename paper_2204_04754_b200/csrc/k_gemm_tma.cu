@@ -355,12 +355,9 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
 cudaError_t launch_gemm_tma_acc64(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
                                   const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, double* c,
                                   int64_t ldc, int sym, int num_sms, cudaStream_t st, int* zslices) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tma_acc64, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    cudaError_t ea = attr.run([] { return cudaFuncSetAttribute(k_gemm_tma_acc64, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); });
+    if (ea != cudaSuccess) return ea;
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     bool ok = make_map(&ta_hi, a_hi, M, Kdim, lda, BM) && make_map(&ta_lo, a_lo, M, Kdim, lda, BM) &&
               make_map(&tb_hi, b_hi, nb_rows, Kdim, ldb, BN) && make_map(&tb_lo, b_lo, nb_rows, Kdim, ldb, BN);
@@ -407,12 +404,9 @@ cudaError_t launch_gemm_circ(const float* x32, int L, int K, float* cf, cudaStre
 cudaError_t launch_gemm_tma(const float* a_hi, const float* a_lo, int64_t M, int64_t lda, const float* b_hi,
                             const float* b_lo, int64_t nb_rows, int64_t ldb, int N, int64_t Kdim, int circ, int Ll,
                             float* c, int64_t ldc, cudaStream_t st, double* c64, int kz, int sym) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    cudaError_t ea = attr.run([] { return cudaFuncSetAttribute(k_gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); });
+    if (ea != cudaSuccess) return ea;
     CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
     bool ok = make_map(&ta_hi, a_hi, M, Kdim, lda, BM) && make_map(&ta_lo, a_lo, M, Kdim, lda, BM);
     if (circ) ok = ok && make_map(&tb_hi, b_hi, nb_rows, Ll, Ll, Ll) && make_map(&tb_lo, b_lo, nb_rows, Ll, Ll, Ll);

@@ -617,9 +617,8 @@ static cudaError_t mom_eval_dev(srmra_ctx* c) {
     return cudaGetLastError();
 }
 
-static bool attrs_set = false;
-static cudaError_t mom_attrs(int Ll2) {
-    if (attrs_set) return cudaSuccess;
+static PerDeviceOnce mom_attr_once;
+static cudaError_t mom_attrs_set() {
     const int bytes = (int)sizeof(double2) * (64 * 64 + 2 * 4096);  // Ll <= 64; L <= 4096
 #define MOM_ATTR(KT)                                                                             \
     MCK(cudaFuncSetAttribute(k_mom_A<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
@@ -630,10 +629,9 @@ static cudaError_t mom_attrs(int Ll2) {
     MOM_ATTR(3);
     MOM_ATTR(4);
 #undef MOM_ATTR
-    (void)Ll2;
-    attrs_set = true;
     return cudaSuccess;
 }
+static cudaError_t mom_attrs(int) { return mom_attr_once.run(mom_attrs_set); }
 
 // srmra_mom_objective: theta from host (x | rho1 | rho2), outputs to host (any NULL)
 int mom_objective(srmra_ctx* c, const double* x, const double* r1, const double* r2, double* f, double* gx,

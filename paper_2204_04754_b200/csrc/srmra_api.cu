@@ -409,6 +409,22 @@ int allreduce_doubles(srmra_ctx* c, double* buf, size_t n) {
 }
 }  // namespace srmra
 
+namespace {
+// Every call on a context runs on the context's device and restores the caller's current device
+// (a process may hold contexts on several GPUs).
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(const srmra_ctx* c) {
+        int cur = -1;
+        if (c && cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess)
+            prev = cur;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
 extern "C" {
 
 void srmra_default_options(srmra_options* o) {
@@ -601,6 +617,7 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
 }
 
 int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1_0, const double* rho2_0) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (!x0 || !rho1_0 || !rho2_0 || (c->n_local > 0 && !y)) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
@@ -614,6 +631,7 @@ int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1
 int srmra_generate(srmra_ctx* c, const float* x_true, const double* rho1_true, const double* rho2_true, uint64_t seed,
                    int64_t first_index, const float* x0, const double* rho1_0, const double* rho2_0,
                    int32_t* shifts_out) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (!x_true || !rho1_true || !rho2_true || !x0 || !rho1_0 || !rho2_0)
@@ -655,6 +673,7 @@ int srmra_generate(srmra_ctx* c, const float* x_true, const double* rho1_true, c
 }
 
 int srmra_get_observations(srmra_ctx* c, int64_t first, int64_t count, float* y_out) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (first < 0 || count < 0 || first + count > c->n_local || (count > 0 && !y_out))
@@ -666,6 +685,7 @@ int srmra_get_observations(srmra_ctx* c, int64_t first, int64_t count, float* y_
 }
 
 int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
@@ -674,6 +694,7 @@ int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
 }
 
 int srmra_run(srmra_ctx* c, int32_t max_iters, double rel_tol) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (max_iters < 0 || !(rel_tol == rel_tol)) return fail(c, SRMRA_ERR_INVALID_ARG, "max_iters < 0 or rel_tol NaN");
@@ -685,6 +706,7 @@ int srmra_run(srmra_ctx* c, int32_t max_iters, double rel_tol) {
 }
 
 int srmra_relative_error(srmra_ctx* c, const float* x_true, double* err_out, int32_t* s1_out, int32_t* s2_out) {
+    DevGuard dg_(c);
     if (!c || !x_true) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
     std::vector<double> xr(c->L2), corr(c->L2), xh(c->L2);
@@ -721,6 +743,7 @@ int srmra_relative_error(srmra_ctx* c, const float* x_true, double* err_out, int
 }
 
 int srmra_set_joint_rho(srmra_ctx* c, const double* rho) {
+    DevGuard dg_(c);
     if (!c || !rho) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
     if (c->path == SRMRA_PATH_FFT && c->Ll > 64)
@@ -766,6 +789,7 @@ int srmra_set_joint_rho(srmra_ctx* c, const double* rho) {
 }
 
 int srmra_get_joint_rho(srmra_ctx* c, double* out) {
+    DevGuard dg_(c);
     if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
     if (!c->joint) return fail(c, SRMRA_ERR_STATE, "no joint shift prior set (srmra_set_joint_rho)");
@@ -775,6 +799,7 @@ int srmra_get_joint_rho(srmra_ctx* c, double* out) {
 }
 
 int srmra_moments(srmra_ctx* c, double* m1, double* m2) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no valid observations (srmra_init with y NULL, or a rejected srmra_load)");
@@ -791,6 +816,7 @@ static int mom_fail(srmra_ctx* c, int rc, const std::string& err) {
 }
 
 int srmra_mom_set_moments(srmra_ctx* c, const double* m1, const double* m2) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if ((m1 == nullptr) != (m2 == nullptr)) return fail(c, SRMRA_ERR_INVALID_ARG, "m1 and m2: both or neither");
@@ -808,6 +834,7 @@ int srmra_mom_set_moments(srmra_ctx* c, const double* m1, const double* m2) {
 
 int srmra_mom_objective(srmra_ctx* c, const double* x, const double* rho1, const double* rho2, double* f,
                         double* grad_x, double* grad_rho1, double* grad_rho2) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (!x || !rho1 || !rho2) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL theta");
@@ -817,6 +844,7 @@ int srmra_mom_objective(srmra_ctx* c, const double* x, const double* rho1, const
 }
 
 int srmra_mom_run(srmra_ctx* c, int32_t max_steps, int32_t F, double gtol, double* f_out, int32_t* steps_out) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (max_steps < 0 || F < 0 || !(gtol >= 0.0)) return fail(c, SRMRA_ERR_INVALID_ARG, "max_steps < 0, F < 0 or gtol < 0");
@@ -844,6 +872,7 @@ int srmra_set_denoiser(srmra_ctx* c, srmra_denoiser_fn fn, void* user) {
 }
 
 int srmra_profile(srmra_ctx* c, int32_t enable) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     CK(cudaStreamSynchronize(c->stream));
@@ -864,6 +893,7 @@ int srmra_profile(srmra_ctx* c, int32_t enable) {
 }
 
 int srmra_profile_read(srmra_ctx* c, double* em_ms, double* iter_ms, int32_t* n_iters) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     CK(cudaStreamSynchronize(c->stream));
@@ -908,6 +938,7 @@ int srmra_profile_read(srmra_ctx* c, double* em_ms, double* iter_ms, int32_t* n_
 
 int srmra_get_estimate(srmra_ctx* c, float* x_out, double* rho1_out, double* rho2_out, double* loglik_out,
                        int32_t* iters_done) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (x_out) CK(cudaMemcpyAsync(x_out, c->d_x32, sizeof(float) * c->L2, cudaMemcpyDeviceToHost, c->stream));
@@ -929,6 +960,7 @@ int srmra_get_estimate(srmra_ctx* c, float* x_out, double* rho1_out, double* rho
 }
 
 int srmra_get_loglik_trace(srmra_ctx* c, double* out, int32_t cap, int32_t* n) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     int rc;
@@ -942,6 +974,7 @@ int srmra_get_loglik_trace(srmra_ctx* c, double* out, int32_t cap, int32_t* n) {
 }
 
 int srmra_get_stats(srmra_ctx* c, double* b, double* cmass, double* m1, double* m2) {
+    DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
     if (b) CK(cudaMemcpyAsync(b, c->d_pack + c->pk.b, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream));
@@ -953,6 +986,7 @@ int srmra_get_stats(srmra_ctx* c, double* b, double* cmass, double* m1, double* 
 }
 
 int srmra_get_obs_loglik(srmra_ctx* c, double* out) {
+    DevGuard dg_(c);
     if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
     if (c->n_local) CK(cudaMemcpyAsync(out, c->d_llobs, sizeof(double) * c->n_local, cudaMemcpyDeviceToHost, c->stream));
@@ -961,6 +995,7 @@ int srmra_get_obs_loglik(srmra_ctx* c, double* out) {
 }
 
 int srmra_local_stats(srmra_ctx* c, double* out) {
+    DevGuard dg_(c);
     if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
     const bool prof = c->prof;
@@ -977,6 +1012,7 @@ int srmra_local_stats(srmra_ctx* c, double* out) {
 int srmra_get_path(const srmra_ctx* c) { return c ? c->path : SRMRA_ERR_INVALID_ARG; }
 
 int srmra_debug_timestamps(srmra_ctx* c, uint64_t* out8) {
+    DevGuard dg_(c);
     if (!c || !out8) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (!c->d_stamps) return fail(c, SRMRA_ERR_STATE, "set SRMRA_TAIL_STAMPS before srmra_init");
     CK(cudaMemcpyAsync(out8, c->d_stamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -996,6 +1032,7 @@ int srmra_launches_per_iter(const srmra_ctx* c) {
 }
 
 void srmra_free(srmra_ctx* c) {
+    DevGuard dg_(c);
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->nccl_comm) {

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -184,6 +185,21 @@ cudaError_t fft_plan_joint(srmra_ctx* c, bool joint);  // re-plan with / without
 size_t fft_joint_bins(int KK, int Ll);
 size_t fft_part_float2(const srmra_ctx* c);
 size_t fft_xhat_float2(int KK, int Ll);   // pair-interleaved Xhat
+
+// cudaFuncSetAttribute is per device: run a setup functor once per device ordinal (retried after a failure)
+struct PerDeviceOnce {
+    std::atomic<unsigned long long> mask{0};
+    template <class F>
+    cudaError_t run(F f) {
+        int d = 0;
+        cudaGetDevice(&d);
+        const unsigned long long bit = 1ull << (d & 63);
+        if (mask.load() & bit) return cudaSuccess;
+        const cudaError_t e = f();
+        if (e == cudaSuccess) mask.fetch_or(bit);
+        return e;
+    }
+};
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ int imod(int a, int m) {
