@@ -69,6 +69,7 @@ struct TailArgs {
 __device__ inline void grid_sync() { cg::this_grid().sync(); }
 
 // ---- phase R: bins in rounds of 32, kSlices threads per bin, 4 independent chains per thread
+template <bool JOINT>
 __device__ void phase_reduce(const TailArgs& a) {
     __shared__ double2 red[kSlices][33];
     const int b = threadIdx.x & 31, sl = threadIdx.x >> 5;
@@ -104,7 +105,7 @@ __device__ void phase_reduce(const TailArgs& a) {
         }
         __syncthreads();
     }
-    if (a.joint) {  // joint prior: the per-shift posterior mass, same fixed-order scheme (real bins)
+    if constexpr (JOINT) {  // joint prior: the per-shift posterior mass, same fixed-order scheme (real bins)
         __shared__ double redj[kSlices][33];
         for (int base = blockIdx.x * 32; base < a.JB; base += gridDim.x * 32) {
             const int k = base + b;
@@ -137,6 +138,7 @@ __device__ void phase_reduce(const TailArgs& a) {
 
 // ---- phase F: item (r, ch) -> rows [ch R, ch R + R) of b_r (and x' there when `update`);
 //      item KK*nchunk -> mass, marginals, LL (and rho', the LL trace when `update`)
+template <bool JOINT>
 __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
     __shared__ double red[32];
     __shared__ double cm_s;
@@ -236,7 +238,7 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                 a.pack[a.off_m1 + s] = a1;
                 a.pack[a.off_m2 + s] = a2 * invL;
             }
-            if (update && a.joint) {
+            if (JOINT && update) {
                 // eq:rho_EM as written: rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'} (zero prior mass stays
                 // zero); the reported marginals are its row / column sums
                 __syncthreads();
@@ -302,6 +304,7 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
 // ---- phase Q: Xhat of the new x (items (r, ch): columns k2 in chunk ch of class r) and the logit bias
 // (last item).  Each item stages x_r (float64), transforms its k2 columns along n2 for every row, then
 // along n1: no work is repeated across items and the shared memory stays below 227 KB at L_low = 128.
+template <bool JOINT>
 __device__ void phase_prep(const TailArgs& a, double* sm) {
     const int L = a.L, K = a.K, Ll = L / K, Lh = Ll / 2 + 1, KK = K * K, M = Ll - 1;
     const int Wq = a.wq, nck = a.nchunk_q;
@@ -394,7 +397,7 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                 a.par32[k] = p1 > 0.0 ? (float)log2(p1) : -INFINITY;
                 a.par32[L + k] = p2 > 0.0 ? (float)log2(p2) : -INFINITY;
             }
-            if (a.joint) {  // per-shift log2 prior, pair-interleaved [q][n2][n1] (the E/M kernel's JOINT table)
+            if constexpr (JOINT) {  // per-shift log2 prior, pair-interleaved [q][n2][n1] (the E/M kernel's JOINT table)
                 const int NPq = (KK + 1) / 2;
                 for (int e = threadIdx.x; e < NPq * Ll * Ll; e += blockDim.x) {
                     const int qq = e / (Ll * Ll), rem = e - qq * Ll * Ll, n2 = rem / Ll, n1 = rem - n2 * Ll;
@@ -421,6 +424,7 @@ __device__ inline void stamp(const TailArgs& a, int k) {
     }
 }
 
+template <bool JOINT>
 __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     extern __shared__ double sm[];
     if (*reinterpret_cast<volatile int*>(a.run)) return;  // a converged srmra_run: nothing left to do
@@ -436,19 +440,19 @@ __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
         atomicMin(a.stamps + 6, t0);
     }
     if (a.mode & TAIL_REDUCE) {
-        phase_reduce(a);
+        phase_reduce<JOINT>(a);
         synced = false;
     }
     if (a.mode & TAIL_FOLD) {
         if (!synced) grid_sync();
         stamp(a, 1);
-        phase_fold(a, sm, (a.mode & TAIL_FINALIZE) != 0);
+        phase_fold<JOINT>(a, sm, (a.mode & TAIL_FINALIZE) != 0);
         synced = false;
     }
     if (a.mode & TAIL_PREP) {
         if (!synced) grid_sync();
         stamp(a, 4);
-        phase_prep(a, sm);
+        phase_prep<JOINT>(a, sm);
     }
     if (a.stamps) {
         __syncthreads();
@@ -527,10 +531,13 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     if (sm_marg > sm_fold) sm_fold = sm_marg;
     size_t sm_prep = sizeof(double) * (2 * Ll + (size_t)Ll * Ll) + sizeof(double2) * (size_t)Ll * a.wq;
     const size_t sm = sm_fold > sm_prep ? sm_fold : sm_prep;
-    cudaError_t e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // the joint-prior work is a separate instantiation: the separable tail's code stays as small as before
+    // (after an L2 flush its instructions are fetched from HBM)
+    auto kern = c->fft_joint ? k_fft_tail<true> : k_fft_tail<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // same L1 / shared-memory split as the E/M kernel before it: no carve-out reconfiguration between them
-    e = cudaFuncSetAttribute(k_fft_tail, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     const int grid = fft_tail_grid(c);
     cudaLaunchConfig_t cfg = {};
@@ -543,7 +550,7 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_fft_tail, a);
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 }  // namespace srmra
