@@ -227,14 +227,20 @@ __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, f
 
 // PAIRS = true when K^2 is even (every complex transform carries two classes); for odd K^2 the
 // imaginary half of the last pair is empty.
-// XS = true: the pair-interleaved Xhat of this iteration is staged once per CTA in shared memory
+// XS = 1: the pair-interleaved Xhat of this iteration is staged once per CTA in shared memory
 // (ahead of the group areas) instead of being read through L1 in the E-step product.
+// XS = 2: staged instead as the E-step product's coefficients: for a stored bin o of the pair (a, b) and
+// the sign g = +1 (column k2 < LH, stored bin) or -1 (k2 >= LH, Hermitian mirror), the conjugated packed
+// product v = conj(Yhat conj(Xhat_a) + i Yhat conj(Xhat_b)) (g = +1; its mirror form for g = -1) is
+//     v.x = Y.x (xa.x + g xb.y) + Y.y (xa.y - g xb.x),   v.y = Y.x (g xa.y - xb.x) + Y.y (-g xa.x - xb.y),
+// so one float4 per (bin, g) turns the two complex products and their combination (10 FP32
+// instructions) into 2 FMUL + 2 FFMA, at twice the staged bytes.
 template <int LL>
-__host__ __device__ inline size_t xs_bytes(int KK) {
-    return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (LL / 2 + 1);
+__host__ __device__ inline size_t xs_bytes(int KK, int xs_mode = 1) {
+    return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (LL / 2 + 1) * (xs_mode == 2 ? 2 : 1);
 }
 
-template <int LL, bool PAIRS, bool XS, bool TACC, bool JOINT>
+template <int LL, bool PAIRS, int XS, bool TACC, bool JOINT>
 __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArgs a) {
     using G = Geo<LL>;
     constexpr int LH = G::LH, WS = G::WS, M = LL - 1;
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     // ---- shared layout: par table | [Xhat (XS)] | group 0 | group 1 | ...
     float* pars = reinterpret_cast<float*>(smem_raw);
     const size_t pb = par_bytes<LL>(KK);
-    const size_t xsb = XS ? xs_bytes<LL>(KK) : 0;
+    const size_t xsb = XS ? xs_bytes<LL>(KK, XS) : 0;
     unsigned char* gbase = smem_raw + pb + xsb;
     for (int k = threadIdx.x; k < 2 * L; k += blockDim.x) pars[k] = __ldg(a.par32 + k);
     // class bias beta_r = (E_min - E_r) log2(e) / (2 sigma^2) from E_r (float64, written by the tail)
@@ -278,10 +284,19 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                                    rB < KK ? __ldg(a.par32 + L + rB % K + K * n2) : 0.f);
         }
     }
-    if (XS) {
+    if (XS == 1) {
         const float4* src = a.xhat;
         float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
         for (int k = threadIdx.x; k < NP * LL * LH; k += blockDim.x) dst[k] = __ldg(src + k);
+    } else if (XS == 2) {  // product coefficients: plane g = +1 (dst[k]) | plane g = -1 (dst[P + k])
+        const float4* src = a.xhat;
+        float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
+        const int P = NP * LL * LH;
+        for (int k = threadIdx.x; k < P; k += blockDim.x) {
+            const float4 x = __ldg(src + k);  // (xa, xb)
+            dst[k] = make_float4(x.x + x.w, x.y - x.z, x.y - x.z, -x.x - x.w);
+            dst[P + k] = make_float4(x.x - x.w, x.y + x.z, -x.y - x.z, x.x - x.w);
+        }
     }
     __shared__ uint32_t tmem_slot;
     if (TACC && threadIdx.x < 32) tc::tmem_alloc_n(&tmem_slot, a.tmem_cols);
@@ -410,10 +425,15 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const int sk1 = flip ? ((LL - k1) & M) : k1;
                             const int o = sk1 * LH + sk2;
                             const float2 yv = Y[o];
-                            const float4 xv = XS ? XP[o] : __ldg(XP + o);
-                            const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
-                            const float2 B = cmul_conj(yv, make_float2(xv.z, xv.w));
-                            v[k1] = make_float2(A.x - sgn * B.y, -sgn * A.y - B.x);
+                            if constexpr (XS == 2) {
+                                const float4 cf = XP[o + (flip ? NP * LL * LH : 0)];
+                                v[k1] = make_float2(fmaf(yv.x, cf.x, yv.y * cf.y), fmaf(yv.x, cf.z, yv.y * cf.w));
+                            } else {
+                                const float4 xv = XS ? XP[o] : __ldg(XP + o);
+                                const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
+                                const float2 B = cmul_conj(yv, make_float2(xv.z, xv.w));
+                                v[k1] = make_float2(A.x - sgn * B.y, -sgn * A.y - B.x);
+                            }
                             ys[2 * e] = yv.x;
                             ys[2 * e + 1] = yv.y;
                         }
@@ -675,9 +695,12 @@ bool fft_supported(int L, int Ll, int K) {
 }
 
 template <int LL, bool TACC, bool JOINT>
-static auto em_kernel(int KK, bool xs) {
-    return (KK % 2 == 0) ? (xs ? k_fft_em<LL, true, true, TACC, JOINT> : k_fft_em<LL, true, false, TACC, JOINT>)
-                         : (xs ? k_fft_em<LL, false, true, TACC, JOINT> : k_fft_em<LL, false, false, TACC, JOINT>);
+static auto em_kernel(int KK, int xs) {
+    if (KK % 2 == 0)
+        return xs == 2 ? k_fft_em<LL, true, 2, TACC, JOINT>
+                       : (xs == 1 ? k_fft_em<LL, true, 1, TACC, JOINT> : k_fft_em<LL, true, 0, TACC, JOINT>);
+    return xs == 2 ? k_fft_em<LL, false, 2, TACC, JOINT>
+                   : (xs == 1 ? k_fft_em<LL, false, 1, TACC, JOINT> : k_fft_em<LL, false, 0, TACC, JOINT>);
 }
 
 template <int LL, bool TACC, bool JOINT>
@@ -693,21 +716,29 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     if (groups > 15) groups = 15;
     const char* eg = getenv("SRMRA_FFT_GROUPS");  // tuning override
     if (eg && atoi(eg) > 0 && atoi(eg) < groups) groups = atoi(eg);
-    // Xhat staged in shared memory unless that costs a group (SRMRA_FFT_XS=0/1 overrides)
-    const size_t xsb = xs_bytes<LL>(KK);
-    int g_plain = groups, g_xs = groups;
+    // Xhat staged in shared memory unless that costs a group (SRMRA_FFT_XS=0/1/2 overrides): as the
+    // product coefficients (mode 2) when they cost no group more than the plain staging (mode 1)
+    const size_t xsb1 = xs_bytes<LL>(KK, 1), xsb2 = xs_bytes<LL>(KK, 2);
+    int g_plain = groups, g_xs = groups, g_xs2 = groups;
     while (g_plain > 1 && gsm(g_plain) > 227 * 1024) --g_plain;
-    while (g_xs > 1 && gsm(g_xs) + xsb > 227 * 1024) --g_xs;
+    while (g_xs > 1 && gsm(g_xs) + xsb1 > 227 * 1024) --g_xs;
+    while (g_xs2 > 1 && gsm(g_xs2) + xsb2 > 227 * 1024) --g_xs2;
     // measured on B200 (tools/em_sweep.py, c1 / c3): Xhat in shared memory with one group fewer beats
     // Xhat through L1 with the extra group (164 vs 177 us at c1), so stage it whenever it fits
-    bool xs = gsm(g_xs) + xsb <= 227 * 1024;
+    int xs = gsm(g_xs) + xsb1 <= 227 * 1024 ? 1 : 0;
+    if (xs && g_xs2 == g_xs && gsm(g_xs2) + xsb2 <= 227 * 1024) xs = 2;
     const char* ex = getenv("SRMRA_FFT_XS");
-    if (ex) xs = atoi(ex) != 0 && gsm(1) + xsb <= 227 * 1024;
-    groups = xs ? g_xs : g_plain;
+    if (ex) {
+        xs = atoi(ex);
+        if (xs < 0 || xs > 2 || gsm(1) + xs_bytes<LL>(KK, xs ? xs : 1) * (xs ? 1 : 0) > 227 * 1024) xs = 0;
+    }
+    const size_t xsb = xs ? xs_bytes<LL>(KK, xs) : 0;
+    groups = xs == 2 ? g_xs2 : (xs == 1 ? g_xs : g_plain);
+    while (groups > 1 && gsm(groups) + xsb > 227 * 1024) --groups;
     // keep enough CTAs for all SMs when N is small
     const int64_t need = (c->n_local + c->num_sms - 1) / c->num_sms;
     if (need < groups) groups = (int)(need < 1 ? 1 : need);
-    const size_t smem = gsm(groups) + (xs ? xsb : 0);
+    const size_t smem = gsm(groups) + xsb;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto kern = em_kernel<LL, TACC, JOINT>(KK, xs);
     c->fft_xs = xs;

@@ -582,7 +582,7 @@ cudaError_t fft128_plan(srmra_ctx* c) {
     c->fft_groups = (c->KK + 1) / 2;
     c->fft_threads = NT;
     c->fft_smem = SMEM;
-    c->fft_xs = false;
+    c->fft_xs = 0;
     return cudaSuccess;
 }
 

@@ -75,7 +75,7 @@ struct srmra_ctx {
     double* d_llpart = nullptr; // fft path: per-CTA log-likelihood partials [fft_grid]
     double* d_tw = nullptr;     // fft path: cos | sin (2 pi j / L_low), j < L_low, float64
     int fft_grid = 0, fft_groups = 0, fft_threads = 0;
-    bool fft_xs = false;        // Xhat staged in shared memory by the E/M kernel
+    int fft_xs = 0;             // Xhat staged in shared memory by the E/M kernel (1) / as product coefficients (2)
     bool fft_tacc = false;      // E/M kernel keeps the M-step accumulators in tensor memory
     bool fft_joint = false;     // E/M kernel planned with the joint-prior accumulator (NEXT-3)
     int fft_part_cap = 0;       // CTAs the partial buffers were sized for (first plan)
