@@ -234,10 +234,11 @@ __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, f
 // product v = conj(Yhat conj(Xhat_a) + i Yhat conj(Xhat_b)) (g = +1; its mirror form for g = -1) is
 //     v.x = Y.x (xa.x + g xb.y) + Y.y (xa.y - g xb.x),   v.y = Y.x (g xa.y - xb.x) + Y.y (-g xa.x - xb.y),
 // so one float4 per (bin, g) turns the two complex products and their combination (10 FP32
-// instructions) into 2 FMUL + 2 FFMA, at twice the staged bytes.
+// instructions) into 2 FMUL + 2 FFMA.  Stored per (k1, k2 < LL) in the order the column threads read
+// them (the mirror resolved at staging), so a warp's load is 32 consecutive float4.
 template <int LL>
 __host__ __device__ inline size_t xs_bytes(int KK, int xs_mode = 1) {
-    return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (LL / 2 + 1) * (xs_mode == 2 ? 2 : 1);
+    return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (xs_mode == 2 ? LL : LL / 2 + 1);
 }
 
 template <int LL, bool PAIRS, int XS, bool TACC, bool JOINT>
@@ -288,14 +289,16 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
         const float4* src = a.xhat;
         float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
         for (int k = threadIdx.x; k < NP * LL * LH; k += blockDim.x) dst[k] = __ldg(src + k);
-    } else if (XS == 2) {  // product coefficients: plane g = +1 (dst[k]) | plane g = -1 (dst[P + k])
+    } else if (XS == 2) {  // product coefficients in the order pass 0 reads them: [q][k1][k2], k2 < LL
         const float4* src = a.xhat;
         float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
-        const int P = NP * LL * LH;
-        for (int k = threadIdx.x; k < P; k += blockDim.x) {
-            const float4 x = __ldg(src + k);  // (xa, xb)
-            dst[k] = make_float4(x.x + x.w, x.y - x.z, x.y - x.z, -x.x - x.w);
-            dst[P + k] = make_float4(x.x - x.w, x.y + x.z, -x.y - x.z, x.x - x.w);
+        for (int k = threadIdx.x; k < NP * LL * LL; k += blockDim.x) {
+            const int qq = k / (LL * LL), rem = k - qq * LL * LL, k1 = rem / LL, k2 = rem - k1 * LL;
+            const bool fl = k2 >= LH;  // Hermitian mirror of a stored bin, g = -1
+            const int o = (fl ? ((LL - k1) & M) : k1) * LH + (fl ? LL - k2 : k2);
+            const float4 x = __ldg(src + (size_t)qq * LL * LH + o);  // (xa, xb)
+            dst[k] = fl ? make_float4(x.x - x.w, x.y + x.z, -x.y - x.z, x.x - x.w)
+                        : make_float4(x.x + x.w, x.y - x.z, x.y - x.z, -x.x - x.w);
         }
     }
     __shared__ uint32_t tmem_slot;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     const int idx = line_ok ? tg - q * LL : 0;
     const int ra = 2 * q, rb = 2 * q + 1;
     const bool has_b = PAIRS || rb < KK;
-    const float4* XP = (XS ? reinterpret_cast<const float4*>(smem_raw + pb) : a.xhat) + (size_t)q * LL * LH;
+    const float4* XP = (XS ? reinterpret_cast<const float4*>(smem_raw + pb) : a.xhat) + (size_t)q * LL * (XS == 2 ? LL : LH);
     float2* Wq = Wk + (size_t)q * LL * WS;
     float2* Uq = Acc + (size_t)(2 * q) * LL * LH;
     float2* Vq = Uq + (size_t)LL * LH;
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const int o = sk1 * LH + sk2;
                             const float2 yv = Y[o];
                             if constexpr (XS == 2) {
-                                const float4 cf = XP[o + (flip ? NP * LL * LH : 0)];
+                                const float4 cf = XP[k1 * LL + idx];  // lane-contiguous: ideal wavefronts
                                 v[k1] = make_float2(fmaf(yv.x, cf.x, yv.y * cf.y), fmaf(yv.x, cf.z, yv.y * cf.w));
                             } else {
                                 const float4 xv = XS ? XP[o] : __ldg(XP + o);
