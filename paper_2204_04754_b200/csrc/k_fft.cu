@@ -726,9 +726,11 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     while (g_plain > 1 && gsm(g_plain) > 227 * 1024) --g_plain;
     while (g_xs > 1 && gsm(g_xs) + xsb1 > 227 * 1024) --g_xs;
     while (g_xs2 > 1 && gsm(g_xs2) + xsb2 > 227 * 1024) --g_xs2;
-    // measured on B200 (tools/em_sweep.py, c1 / c3): Xhat in shared memory with one group fewer beats
-    // Xhat through L1 with the extra group (164 vs 177 us at c1), so stage it whenever it fits
-    int xs = gsm(g_xs) + xsb1 <= 227 * 1024 ? 1 : 0;
+    // measured on B200 (tools/em_sweep.py, tools/path_timing.py): Xhat in shared memory with one group
+    // fewer beat Xhat through L1 with the extra group at c1 (164 vs 177 us, 7 vs 6 groups), but at c2
+    // staging halves the warps (1 group instead of 2) and costs 43 % (1.697 vs 1.184 ms): stage only when
+    // it costs no group, or one group out of four or more
+    int xs = (gsm(g_xs) + xsb1 <= 227 * 1024 && (g_xs == g_plain || (g_xs >= 4 && g_xs + 1 >= g_plain))) ? 1 : 0;
     if (xs && g_xs2 == g_xs && gsm(g_xs2) + xsb2 <= 227 * 1024) xs = 2;
     const char* ex = getenv("SRMRA_FFT_XS");
     if (ex) {
