@@ -153,7 +153,12 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));  // before k_ynorm may set bit 1
     const bool chunked = ysrc == Y_HOST && c->path == SRMRA_PATH_FFT && c->copy_stream && ny;
     if (chunked) {
-        const int64_t per = std::max<int64_t>(1, (int64_t)(4 << 20) / (int64_t)(sizeof(float) * c->Ll2));
+        static const int64_t chunk_bytes = [] {  // ~4 MB per chunk (SRMRA_H2D_CHUNK_MB overrides)
+            const char* e = getenv("SRMRA_H2D_CHUNK_MB");
+            const int64_t mb = e ? atoll(e) : 4;
+            return (mb > 0 ? mb : 4) << 20;
+        }();
+        const int64_t per = std::max<int64_t>(1, chunk_bytes / (int64_t)(sizeof(float) * c->Ll2));
         for (int64_t o = 0; o < c->n_local; o += per) {
             const int64_t m = std::min<int64_t>(per, c->n_local - o);
             CK(cudaMemcpyAsync(c->d_y + o * c->Ll2, y + o * c->Ll2, sizeof(float) * m * c->Ll2,
