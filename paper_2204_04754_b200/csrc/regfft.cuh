@@ -101,5 +101,76 @@ __device__ __forceinline__ void fft(float2 (&v)[N]) {
     for (int i = 0; i < N; ++i) v[i] = t[i];
 }
 
+
+// ------------------------------------------------------------------ register FFT (radix 4)
+// Two radix-2 DIT stages (lengths 2H and 4H) merged into one radix-4 butterfly per quad (B + j, + H, + 2H,
+// + 3H): with b~ = W_4H^{2j} b, c~ = W_4H^j c, d~ = W_4H^{3j} d the outputs are a +- b~ +- (c~ + d~) and
+// a -+ b~ ... (-+ i)(c~ - d~) — 3 twiddle products per quad instead of 4, the same 8 complex additions.
+template <int N, int SIGN, int TK>
+__device__ __forceinline__ float2 twmul(float2 b) {
+    constexpr int T = ((TK % N) + N) % N;
+    if constexpr (T == 0) {
+        return b;
+    } else if constexpr (2 * T == N) {
+        return make_float2(-b.x, -b.y);
+    } else if constexpr (4 * T == N) {
+        if constexpr (SIGN > 0) return make_float2(-b.y, b.x);  // * (+i)
+        else return make_float2(b.y, -b.x);                     // * (-i)
+    } else if constexpr (4 * T == 3 * N) {
+        if constexpr (SIGN > 0) return make_float2(b.y, -b.x);  // * (-i)
+        else return make_float2(-b.y, b.x);                     // * (+i)
+    } else {
+        constexpr float c = (float)cos2pi(T, N);
+        constexpr float s = (float)(SIGN * sin2pi(T, N));
+        return make_float2(fmaf(b.x, c, -b.y * s), fmaf(b.x, s, b.y * c));
+    }
+}
+template <int N, int SIGN, int H, int B, int J>
+__device__ __forceinline__ void bfly4(float2* t) {
+    constexpr int S = N / (4 * H);  // W_4H^k = W_N^{k S}
+    const float2 a = t[B + J];
+    const float2 bt = twmul<N, SIGN, 2 * J * S>(t[B + J + H]);
+    const float2 ct = twmul<N, SIGN, J * S>(t[B + J + 2 * H]);
+    const float2 dt = twmul<N, SIGN, 3 * J * S>(t[B + J + 3 * H]);
+    const float2 p = make_float2(a.x + bt.x, a.y + bt.y), m = make_float2(a.x - bt.x, a.y - bt.y);
+    const float2 cp = make_float2(ct.x + dt.x, ct.y + dt.y), cm = make_float2(ct.x - dt.x, ct.y - dt.y);
+    // the (b', d') pair's twiddle W_4H^{j+H} = W_4H^j W_4H^H, W_4H^H = W_N^{N/4} = -+i:
+    // out[j + H] = m + W_N^{N/4} (c~ - d~), out[j + 3H] = m - W_N^{N/4} (c~ - d~)
+    const float2 q = twmul<N, SIGN, N / 4>(cm);
+    t[B + J] = make_float2(p.x + cp.x, p.y + cp.y);
+    t[B + J + 2 * H] = make_float2(p.x - cp.x, p.y - cp.y);
+    t[B + J + H] = make_float2(m.x + q.x, m.y + q.y);
+    t[B + J + 3 * H] = make_float2(m.x - q.x, m.y - q.y);
+}
+template <int N, int SIGN, int H, int B, int... Js>
+__device__ __forceinline__ void bfly4_block(float2* t, std::integer_sequence<int, Js...>) {
+    (bfly4<N, SIGN, H, B, Js>(t), ...);
+}
+template <int N, int SIGN, int H, int... Bs>
+__device__ __forceinline__ void fft_stage4(float2* t, std::integer_sequence<int, Bs...>) {
+    (bfly4_block<N, SIGN, H, Bs * 4 * H>(t, std::make_integer_sequence<int, H>{}), ...);
+}
+// stages: radix-2 (length 2) when log2 N is odd, then radix-4 stages of quarter sizes H = 2^k
+template <int N, int SIGN, int H>
+__device__ __forceinline__ void fft4_stages(float2* t) {
+    if constexpr (4 * H <= N) {
+        fft_stage4<N, SIGN, H>(t, std::make_integer_sequence<int, N / (4 * H)>{});
+        fft4_stages<N, SIGN, 4 * H>(t);
+    }
+}
+template <int N, int SIGN>
+__device__ __forceinline__ void fft_r4(float2 (&v)[N]) {
+    float2 t[N];
+    bitrev_copy<N>(t, v, std::make_integer_sequence<int, N>{});
+    if constexpr (ilog2(N) % 2 == 1) {
+        fft_stage<N, SIGN, 2>(t, std::make_integer_sequence<int, N / 2>{});
+        fft4_stages<N, SIGN, 2>(t);
+    } else {
+        fft4_stages<N, SIGN, 1>(t);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = t[i];
+}
+
 }  // namespace regfft
 }  // namespace srmra
