@@ -172,5 +172,51 @@ __device__ __forceinline__ void fft_r4(float2 (&v)[N]) {
     for (int i = 0; i < N; ++i) v[i] = t[i];
 }
 
+// ------------------------------------------------------------------ register FFT (split radix)
+// X = DFT_N of x[OFF + ST n]: U = DFT_{N/2} of the even samples, Z / Z' = DFT_{N/4} of the samples 4n + 1 /
+// 4n + 3;  X[k] = U[k] + (W^k Z[k] + W^{3k} Z'[k]),  X[k + N/2] = U[k] - (...),
+// X[k + N/4] = U[k + N/4] + W^{N/4} (W^k Z[k] - W^{3k} Z'[k]),  X[k + 3N/4] = U[k + N/4] - W^{N/4} (...).
+template <int N, int SIGN, int OFF, int ST>
+__device__ __forceinline__ void sr_rec(const float2* x, float2* X);
+template <int N, int SIGN, int K>
+__device__ __forceinline__ void sr_comb(const float2* U, const float2* Z, const float2* Zp, float2* X) {
+    const float2 a = twmul<N, SIGN, K>(Z[K]), b = twmul<N, SIGN, 3 * K>(Zp[K]);
+    const float2 sm = make_float2(a.x + b.x, a.y + b.y);
+    const float2 id = twmul<N, SIGN, N / 4>(make_float2(a.x - b.x, a.y - b.y));
+    const float2 u0 = U[K], u1 = U[K + N / 4];
+    X[K] = make_float2(u0.x + sm.x, u0.y + sm.y);
+    X[K + N / 2] = make_float2(u0.x - sm.x, u0.y - sm.y);
+    X[K + N / 4] = make_float2(u1.x + id.x, u1.y + id.y);
+    X[K + 3 * N / 4] = make_float2(u1.x - id.x, u1.y - id.y);
+}
+template <int N, int SIGN, int... Ks>
+__device__ __forceinline__ void sr_combine(const float2* U, const float2* Z, const float2* Zp, float2* X,
+                                           std::integer_sequence<int, Ks...>) {
+    (sr_comb<N, SIGN, Ks>(U, Z, Zp, X), ...);
+}
+template <int N, int SIGN, int OFF, int ST>
+__device__ __forceinline__ void sr_rec(const float2* x, float2* X) {
+    if constexpr (N == 1) {
+        X[0] = x[OFF];
+    } else if constexpr (N == 2) {
+        const float2 a = x[OFF], b = x[OFF + ST];
+        X[0] = make_float2(a.x + b.x, a.y + b.y);
+        X[1] = make_float2(a.x - b.x, a.y - b.y);
+    } else {
+        float2 U[N / 2], Z[N / 4], Zp[N / 4];
+        sr_rec<N / 2, SIGN, OFF, 2 * ST>(x, U);
+        sr_rec<N / 4, SIGN, OFF + ST, 4 * ST>(x, Z);
+        sr_rec<N / 4, SIGN, OFF + 3 * ST, 4 * ST>(x, Zp);
+        sr_combine<N, SIGN>(U, Z, Zp, X, std::make_integer_sequence<int, N / 4>{});
+    }
+}
+template <int N, int SIGN>
+__device__ __forceinline__ void fft_sr(float2 (&v)[N]) {
+    float2 X[N];
+    sr_rec<N, SIGN, 0, 1>(v, X);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = X[i];
+}
+
 }  // namespace regfft
 }  // namespace srmra

@@ -4,8 +4,10 @@ template <int N> __global__ void kk(float2* p) {
     float2 v[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = p[threadIdx.x * N + i];
-#ifdef R4
+#if defined(R4)
     fft_r4<N, -1>(v);
+#elif defined(SR)
+    fft_sr<N, -1>(v);
 #else
     fft<N, -1>(v);
 #endif
