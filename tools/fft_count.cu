@@ -1,4 +1,8 @@
-#include "../../paper_2204_04754_b200/csrc/regfft.cuh"
+// FP32 instruction counts of the register FFT variants (regfft.cuh) — compile only, no GPU:
+//   for D in "" -DR4 -DSR; do nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//     --expt-relaxed-constexpr $D -cubin -o /tmp/fc.cubin tools/fft_count.cu && cuobjdump -sass /tmp/fc.cubin \
+//     | grep -cE "FADD|FFMA|FMUL"; done
+#include "../paper_2204_04754_b200/csrc/regfft.cuh"
 using namespace srmra::regfft;
 template <int N> __global__ void kk(float2* p) {
     float2 v[N];
