@@ -15,7 +15,7 @@
 // Kernel layout (one persistent CTA per SM slot, G "groups" of threads per CTA, each group owns one
 // observation at a time):  two classes (r, r') are packed into one complex L_low x L_low transform
 // (real part r, imaginary part r').  Each 1-D FFT of length L_low is done by ONE thread entirely in
-// registers (radix-2, compile-time twiddles); the row/column transposes go through a padded shared
+// registers (split radix, compile-time twiddles); the row/column transposes go through a padded shared
 // buffer (row stride L_low + 1 float2: conflict-free for both row and column access).  The scores of
 // the observation never leave registers: softmax (3 group reductions) runs on them, and the row
 // thread immediately starts the forward transform of the posterior.  Yhat_i is prefetched with

@@ -1,4 +1,5 @@
-// regfft.cuh — register-resident radix-2 FFTs with compile-time twiddles, shared by the FFT-path
+// regfft.cuh — register-resident FFTs with compile-time twiddles (radix 2, radix 4 and split radix; the
+// E/M kernels use split radix, the fewest twiddle products), shared by the FFT-path
 // E/M kernels (k_fft.cu: one thread per line, L_low <= 64; k_fft128.cu: a thread pair per line,
 // L_low = 128).  fft<N, SIGN>: in place, natural order in and out, unnormalised,
 // X[k] = sum_n x[n] exp(SIGN 2 pi i n k / N)  (SIGN = -1 forward, +1 inverse).
