@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     for (int r = 0; r < LL; ++r) v[r] = Wq[r * WS + idx];
                 }
                 // pass 2: v holds the posterior row w of the pair (forward transform along n2)
-                fft_sr<LL, -1>(v);  // split radix (fewest twiddle products)
+                fft_sr2<LL, -1>(v);  // split radix, packed FP32x2 arithmetic
                 if (pass == 0) {
 #pragma unroll
                     for (int k1 = 0; k1 < LL; ++k1) Wq[k1 * WS + idx] = v[k1];

@@ -219,5 +219,97 @@ __device__ __forceinline__ void fft_sr(float2 (&v)[N]) {
     for (int i = 0; i < N; ++i) v[i] = X[i];
 }
 
+// ------------------------------------------------------------------ packed FP32x2 arithmetic (sm_100)
+// add / sub / mul / fma .rn.f32x2 on a float2 held in a register pair: one issue slot for both halves
+// (FADD2 / FMUL2 / FFMA2; the pipe throughput per FP32 operation is unchanged, tools/fp32x2_peak.cu), so an
+// issue-bound kernel sheds half of its complex-arithmetic instructions.  Scalars broadcast into a pair
+// (bc) become ".F32" operands in SASS, and the halves of a pair can be swapped as an operand.
+namespace px {
+__device__ __forceinline__ unsigned long long u(float2 v) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+    return r;
+}
+__device__ __forceinline__ float2 f(unsigned long long r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ float2 add(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(u(a)), "l"(u(b)));
+    return f(d);
+}
+__device__ __forceinline__ float2 sub(float2 a, float2 b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(u(a)), "l"(u(b)));
+    return f(d);
+}
+__device__ __forceinline__ float2 mul(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(u(a)), "l"(u(b)));
+    return f(d);
+}
+__device__ __forceinline__ float2 fma(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(u(a)), "l"(u(b)), "l"(u(c)));
+    return f(d);
+}
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+}  // namespace px
+
+// b * W_N^TK (SIGN convention of twmul) in packed form: bx (c, s) + by (-s, c); +-i and -1 as swaps / signs
+template <int N, int SIGN, int TK>
+__device__ __forceinline__ float2 twmul2(float2 b) {
+    constexpr int T = ((TK % N) + N) % N;
+    if constexpr (T == 0 || 2 * T == N || 4 * T == N || 4 * T == 3 * N) {
+        return twmul<N, SIGN, TK>(b);  // trivial: sign flips and swaps fold into the consumer
+    } else {
+        constexpr float c = (float)cos2pi(T, N);
+        constexpr float s = (float)(SIGN * sin2pi(T, N));
+        return px::fma(px::bc(b.y), make_float2(-s, c), px::mul(px::bc(b.x), make_float2(c, s)));
+    }
+}
+template <int N, int SIGN, int K>
+__device__ __forceinline__ void sr2_comb(const float2* U, const float2* Z, const float2* Zp, float2* X) {
+    const float2 a = twmul2<N, SIGN, K>(Z[K]), b = twmul2<N, SIGN, 3 * K>(Zp[K]);
+    const float2 sm = px::add(a, b);
+    const float2 id = twmul<N, SIGN, N / 4>(px::sub(a, b));
+    const float2 u0 = U[K], u1 = U[K + N / 4];
+    X[K] = px::add(u0, sm);
+    X[K + N / 2] = px::sub(u0, sm);
+    X[K + N / 4] = px::add(u1, id);
+    X[K + 3 * N / 4] = px::sub(u1, id);
+}
+template <int N, int SIGN, int... Ks>
+__device__ __forceinline__ void sr2_combine(const float2* U, const float2* Z, const float2* Zp, float2* X,
+                                            std::integer_sequence<int, Ks...>) {
+    (sr2_comb<N, SIGN, Ks>(U, Z, Zp, X), ...);
+}
+template <int N, int SIGN, int OFF, int ST>
+__device__ __forceinline__ void sr2_rec(const float2* x, float2* X) {
+    if constexpr (N == 1) {
+        X[0] = x[OFF];
+    } else if constexpr (N == 2) {
+        const float2 a = x[OFF], b = x[OFF + ST];
+        X[0] = px::add(a, b);
+        X[1] = px::sub(a, b);
+    } else {
+        float2 U[N / 2], Z[N / 4], Zp[N / 4];
+        sr2_rec<N / 2, SIGN, OFF, 2 * ST>(x, U);
+        sr2_rec<N / 4, SIGN, OFF + ST, 4 * ST>(x, Z);
+        sr2_rec<N / 4, SIGN, OFF + 3 * ST, 4 * ST>(x, Zp);
+        sr2_combine<N, SIGN>(U, Z, Zp, X, std::make_integer_sequence<int, N / 4>{});
+    }
+}
+// split radix in packed FP32x2 arithmetic
+template <int N, int SIGN>
+__device__ __forceinline__ void fft_sr2(float2 (&v)[N]) {
+    float2 X[N];
+    sr2_rec<N, SIGN, 0, 1>(v, X);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = X[i];
+}
+
 }  // namespace regfft
 }  // namespace srmra

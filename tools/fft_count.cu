@@ -12,6 +12,8 @@ template <int N> __global__ void kk(float2* p) {
     fft_r4<N, -1>(v);
 #elif defined(SR)
     fft_sr<N, -1>(v);
+#elif defined(SR2)
+    fft_sr2<N, -1>(v);
 #else
     fft<N, -1>(v);
 #endif
