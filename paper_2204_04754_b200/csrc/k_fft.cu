@@ -297,7 +297,8 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
             const bool fl = k2 >= LH;  // Hermitian mirror of a stored bin, g = -1
             const int o = (fl ? ((LL - k1) & M) : k1) * LH + (fl ? LL - k2 : k2);
             const float4 x = __ldg(src + (size_t)qq * LL * LH + o);  // (xa, xb)
-            dst[k] = fl ? make_float4(x.x - x.w, x.y + x.z, -x.y - x.z, x.x - x.w)
+            // stored as (a, c, b, d): v = Y.x (a, c) + Y.y (b, d) in packed FP32x2
+            dst[k] = fl ? make_float4(x.x - x.w, -x.y - x.z, x.y + x.z, x.x - x.w)
                         : make_float4(x.x + x.w, x.y - x.z, x.y - x.z, -x.x - x.w);
         }
     }
@@ -429,8 +430,8 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const int o = sk1 * LH + sk2;
                             const float2 yv = Y[o];
                             if constexpr (XS == 2) {
-                                const float4 cf = XP[k1 * LL + idx];  // lane-contiguous: ideal wavefronts
-                                v[k1] = make_float2(fmaf(yv.x, cf.x, yv.y * cf.y), fmaf(yv.x, cf.z, yv.y * cf.w));
+                                const float4 cf = XP[k1 * LL + idx];  // (a, c, b, d), lane-contiguous: ideal wavefronts
+                                v[k1] = px::fma(px::bc(yv.x), make_float2(cf.x, cf.y), px::mul(px::bc(yv.y), make_float2(cf.z, cf.w)));
                             } else {
                                 const float4 xv = XS ? XP[o] : __ldg(XP + o);
                                 const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 const float sref_t = lmax;
                 // ---- posterior (eq:weights_EM) in log2 units: v2 = (S - sref_t) log2e/sigma^2 + bias
                 float mt = -INFINITY, za = 0.f, zb = 0.f;
+                const float2 biasAB = make_float2(biasA, biasB);
                 if (line_ok) {
                     const float4* lq = reinterpret_cast<const float4*>(smem_raw + par_off_lrp<LL>(KK)) + q * (LL / 2);
 #pragma unroll
@@ -533,21 +535,25 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const float4 l4 = lq[n2 >> 1];
                             b2 = (n2 & 1) ? make_float2(l4.z, l4.w) : make_float2(l4.x, l4.y);
                         }
-                        const float va = fmaf(v[n2].x - sref_t, a.c2, biasA + b2.x);
-                        const float vb = has_b ? fmaf(v[n2].y - sref_t, a.c2, biasB + b2.y) : -INFINITY;
-                        v[n2] = make_float2(va, vb);
-                        mt = fmaxf(mt, fmaxf(va, vb));
+                        // (va, vb) = (S - sref_t) c2 + bias, both classes in packed FP32x2 (same rounding)
+                        float2 vab = px::fma(px::sub(v[n2], px::bc(sref_t)), px::bc(a.c2), px::add(biasAB, b2));
+                        if (!has_b) vab.y = -INFINITY;
+                        v[n2] = vab;
+                        mt = fmaxf(mt, fmaxf(vab.x, vab.y));
                     }
                     // a row whose shifts all have zero prior mass has mt = -inf: its weights are exactly 0
                     const float mref = mt == -INFINITY ? 0.f : mt;
+                    float2 zab = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int n2 = 0; n2 < LL; ++n2) {
-                        const float ea = ex2(v[n2].x - mref);
-                        const float eb = has_b ? ex2(v[n2].y - mref) : 0.f;
+                        const float2 dm = px::sub(v[n2], px::bc(mref));
+                        const float ea = ex2(dm.x);
+                        const float eb = has_b ? ex2(dm.y) : 0.f;
                         v[n2] = make_float2(ea, eb);
-                        za += ea;
-                        zb += eb;
+                        zab = px::add(zab, v[n2]);
                     }
+                    za = zab.x;
+                    zb = zab.y;
                 }
                 sref = sref_t;
                 mall = mt;
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     rsumA = fmaf(za, f, rsumA);
                     rsumB = fmaf(zb, f, rsumB);
 #pragma unroll
-                    for (int n2 = 0; n2 < LL; ++n2) v[n2] = make_float2(v[n2].x * f, v[n2].y * f);
+                    for (int n2 = 0; n2 < LL; ++n2) v[n2] = px::mul(v[n2], px::bc(f));
                     if constexpr (JOINT) {  // posterior mass of the shifts (ra | rb, t1 = idx, t2 = n2)
                         float* ja = JA + ((size_t)ra * LL + idx) * (LL + 1);
                         float* jb = JA + ((size_t)rb * LL + idx) * (LL + 1);
