@@ -93,7 +93,9 @@ struct EmArgs {
 template <int LL>
 struct Geo {
     static constexpr int LH = LL / 2 + 1;
-    static constexpr int WS = LL + 1;  // padded row stride of the transpose buffer (float2)
+    // padded row stride of the transpose buffer (float2): even, so a row thread moves two elements per
+    // 128-bit access; (LL + 2) * 8 B = 4 banks mod 32, so 8 lanes of a row access cover all 32 banks
+    static constexpr int WS = LL + 2;
 };
 
 template <int LL>
@@ -446,7 +448,11 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 } else if (pass == 1) {
                     // E-step along k2 (row n1 = idx) of the conjugated column result
 #pragma unroll
-                    for (int k2 = 0; k2 < LL; ++k2) v[k2] = Wq[idx * WS + k2];
+                    for (int k2 = 0; k2 < LL; k2 += 2) {
+                        const float4 t = *reinterpret_cast<const float4*>(Wq + idx * WS + k2);
+                        v[k2] = make_float2(t.x, t.y);
+                        v[k2 + 1] = make_float2(t.z, t.w);
+                    }
                 } else if (pass == 3) {
                     // M-step along n1 (column c = idx)
 #pragma unroll
@@ -459,7 +465,8 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     for (int k1 = 0; k1 < LL; ++k1) Wq[k1 * WS + idx] = v[k1];
                 } else if (pass == 2) {
 #pragma unroll
-                    for (int k2 = 0; k2 < LL; ++k2) Wq[idx * WS + k2] = v[k2];
+                    for (int k2 = 0; k2 < LL; k2 += 2)
+                        *reinterpret_cast<float4*>(Wq + idx * WS + k2) = make_float4(v[k2].x, v[k2].y, v[k2 + 1].x, v[k2 + 1].y);
                 } else if (pass == 3 && TACC) {
                     // U_q[k1][c] += Yhat[k1][c] conj(Z[k1]) (c < LH) | V_q[k1][LL-c] += Yhat[k1][LL-c] Z[-k1]
 #pragma unroll
