@@ -16,7 +16,7 @@
 // observation at a time):  two classes (r, r') are packed into one complex L_low x L_low transform
 // (real part r, imaginary part r').  Each 1-D FFT of length L_low is done by ONE thread entirely in
 // registers (split radix, compile-time twiddles); the row/column transposes go through a padded shared
-// buffer (row stride L_low + 1 float2: conflict-free for both row and column access).  The scores of
+// buffer (row stride L_low + 2 float2: conflict-free for both row and column access).  The scores of
 // the observation never leave registers: softmax (3 group reductions) runs on them, and the row
 // thread immediately starts the forward transform of the posterior.  Yhat_i is prefetched with
 // cp.async into a double buffer; Xhat (per-iteration, <= 70 KB) is read through the L1/read-only
