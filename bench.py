@@ -2,13 +2,17 @@
 """Benchmark: one projected-EM iteration of 2-D SR-MRA (E-step + M-step over all N observations and
 all L_high^2 shifts, finalize, projection) per step, through libsrmra.so's C ABI.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
 Metric (BASELINE.json): obs x shift likelihoods per second per EM iteration, N * L_high^2 / t.
-Workload: BASELINE.json configs[1] (c1: L_high=64, L_low=32, K=2, N=10,000, sigma=0.25), seeded
-synthetic data (synth/).  Multi-GPU (torchrun): weak scaling, every rank holds its own N
-observations (global N = N * world) and one NCCL all-reduce of the sufficient statistics runs per
-iteration.  Prints ONE JSON line on rank 0.
+Workload: BASELINE.json configs[3] by default (c3: L_high=128, L_low=32, K=4, N=100,000, sigma=0.125;
+one of north_star's two targets, and the largest config the paper's metric names that is quoted on
+1/2/4/8 GPUs), seeded synthetic data (synth/, the same data as tests/golden/c3_oracle.npz); c0..c4 via
+--config.  Multi-GPU: STRONG scaling — the config's N observations are sharded in contiguous blocks
+(paper_2204_04754_b200.shard.shard_bounds), one NCCL all-reduce of the sufficient statistics per
+iteration (captured with the rest of the iteration in one CUDA graph).  `--gpus N` without torchrun
+re-launches itself under torch.distributed.run with N ranks (and fails loudly when the node has fewer
+than N GPUs).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -68,9 +72,9 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload(p) -> dict:
-    return {"workload": p.name, "L_high": p.L_high, "L_low": p.L_low, "K": p.K, "N_per_rank": p.N,
-            "sigma": p.sigma}
+def workload(p, world: int = 1) -> dict:
+    return {"workload": p.name, "L_high": p.L_high, "L_low": p.L_low, "K": p.K, "global_N": p.N,
+            "N_per_rank_max": -(-p.N // world), "sigma": p.sigma}
 
 
 # ---------------------------------------------------------------------- clocks
@@ -157,7 +161,7 @@ def run_reference(args):
     sample = f"first {n} of {p.N} observations of {p.name}, one EM iteration from theta_0 per step"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload(p),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": sample},
@@ -171,21 +175,27 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2204_04754_b200 as srm
+    from paper_2204_04754_b200.shard import broadcast_nccl_id, shard_bounds
 
     rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl_id = None
     if world > 1:
-        from paper_2204_04754_b200.shard import broadcast_nccl_id
         dist.init_process_group("nccl", device_id=dev)
         nccl_id = broadcast_nccl_id(srm.srmra_nccl_unique_id)
 
-    p = synth.make_config(args.config, seed_offset=1000 * rank if world > 1 else 0)
+    # strong scaling: every rank draws the same seeded config and keeps its contiguous shard
+    p = synth.make_config(args.config)
+    lo, hi = shard_bounds(p.N, world, rank)
+    y_loc = np.ascontiguousarray(p.y[lo:hi])
+    n_loc = hi - lo
     stream = torch.cuda.Stream(device=dev)
-    ctx = srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=args.path,
+    ctx = srm.Context(y_loc, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=args.path,
                       proj_every=1, device=local, rank=rank, world=world, nccl_id=nccl_id,
-                      stream=stream.cuda_stream)
+                      stream=stream.cuda_stream, nccl_timeout_ms=600_000)
     path = ctx.path
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
@@ -221,27 +231,37 @@ def run_ours(args):
     if world > 1:
         t = torch.tensor([tot_ms, em_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms, em_max = float(t[0]), float(t[1])
-    units_step = p.N * world * p.L_high ** 2
+        tot_ms = float(t[0])
+    units_step = p.N * p.L_high ** 2                     # the whole job's units (all ranks)
     value = units_step * args.steps / (tot_ms / 1e3)
 
-    # roofline of the dominant kernel (measured live: events around it inside the library, same stream)
+    # roofline of the dominant kernel on this rank (measured live: the kernel's own globaltimer stamps
+    # over the timed region, on the stream it is launched on); units = this rank's observations x shifts
     fpu = flop_per_unit(path, p.L_low)
-    traffic, traffic_src = ncu_traffic(roof_kernel(path, p.L_low), p.name)
+    kern = roof_kernel(path, p.L_low)
+    traffic, traffic_src = ncu_traffic(kern, p.name) if world == 1 else (None, None)
     em_avg_s = em_ms / 1e3 / max(n_prof, 1)
-    achieved = fpu * p.N * p.L_high ** 2 / em_avg_s / 1e12
+    achieved = fpu * n_loc * p.L_high ** 2 / em_avg_s / 1e12
+    alg_bytes = int(n_loc * p.L_low * (p.L_low // 2 + 1) * 8) if path == "fft" else int(n_loc * p.L_low ** 2 * 4)
+    hbm_peak = None
+    try:
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except (OSError, ValueError):
+        pass
     roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
-            "algorithmic_bytes_per_launch": int(p.N * p.L_low * (p.L_low // 2 + 1) * 8),
-            "kernel": roof_kernel(path, p.L_low),
-            "flop_per_unit": fpu, "kernel_ms_avg": em_avg_s * 1e3,
-            "kernel_share_of_step": em_ms / max(tot_ms, 1e-12),
+            "algorithmic_bytes_per_launch": alg_bytes, "kernel": kern,
+            "hbm_gbs": alg_bytes / em_avg_s / 1e9, "hbm_peak_gbs": hbm_peak,
+            "hbm_frac": (alg_bytes / em_avg_s / 1e9 / hbm_peak) if hbm_peak else None,
+            "flop_per_unit": fpu, "units_per_launch": n_loc * p.L_high ** 2, "kernel_ms_avg": em_avg_s * 1e3,
+            "kernel_share_of_step": em_ms / max(float(sum(step_ms)), 1e-12),
+            "rank": rank,
             "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md)"}
 
     # end-to-end through the public API with pinned host buffers: load (H2D) + cfg.iters iterations + D2H
     e2e = None
     if args.e2e_jobs > 0:
-        y_pin = torch.from_numpy(p.y).pin_memory()
+        y_pin = torch.from_numpy(y_loc).pin_memory()
         y_np = y_pin.numpy()
         jt = []
         for j in range(args.e2e_jobs + 1):
@@ -260,9 +280,10 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tj = float(t[0])
         e2e = {"value": units_step * p.iters / tj, "unit": UNIT,
-               "h2d_bytes_per_step": int(p.y.nbytes + 4 * p.L_high ** 2 + 16 * p.L_high),
-               "d2h_bytes_per_step": int(4 * p.L_high ** 2 + 16 * p.L_high + 16),
-               "step": f"srmra_load (pinned host y, x0, rho) + {p.iters} x srmra_em_iter + srmra_get_estimate",
+               "h2d_bytes_per_step": int(p.y.nbytes + world * (4 * p.L_high ** 2 + 16 * p.L_high)),
+               "d2h_bytes_per_step": int(world * (4 * p.L_high ** 2 + 16 * p.L_high + 16)),
+               "step": f"srmra_load (pinned host y shard, x0, rho) + {p.iters} x srmra_em_iter + srmra_get_estimate "
+                       "on every rank (bytes summed over ranks)",
                "timer": "host perf_counter, max over ranks"}
 
     cpu = None
@@ -275,25 +296,45 @@ def run_ours(args):
     launches = ctx.launches_per_iter() * args.steps
     ctx.close()
     if rank == 0:
-        cfg = workload(p)
+        cfg = workload(p, world)
         cfg.update({"path": path, "l2": "flushed before every timed step (256 MiB write, outside the events)",
-                    "iters_per_step": 1, "global_N": p.N * world})
+                    "iters_per_step": 1, "parallelism": f"dp{world} (observations sharded, strong scaling)"})
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "gpu_launches_note": "libsrmra kernels only" + ("; + 1 NCCL all-reduce kernel per step" if world > 1 else ""),
                 "clocks": clk, "step_ms_median": statistics.median(step_ms)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def relaunch_distributed(args) -> int:
+    """`--gpus N` outside torchrun: re-run this script under torch.distributed.run with N ranks."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but this node has {have} visible GPU(s); "
+                                   "refusing to measure fewer ranks than requested"}), flush=True)
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c1", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "fft", "direct", "gemm"])
     ap.add_argument("--e2e-jobs", type=int, default=3)
@@ -304,8 +345,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -62,6 +62,19 @@ extern "C" {
 
 typedef struct srmra_ctx srmra_ctx; /* opaque, owned by the library */
 
+/*
+ * Exchange provider for world > 1 (a6 of SURVEY.md §8: the sums over i of eq:x_EM, eq:rho_EM and
+ * eq:likelihood_EM, over the ranks' shards).  Called on the host in place
+ * of ncclAllReduce(sum, float64) with the device buffer buf_dev (float64 [n], this rank's partial sums on
+ * entry, the sum over all ranks on return) and the context stream (cudaStream_t): the input is complete
+ * once the work enqueued on `stream` before the call has finished, and the result must be visible to the
+ * work enqueued on `stream` after the hook returns (e.g. synchronise the stream, exchange, copy back and
+ * synchronise again).  Every rank calls it the same number of times with the same n.  Return 0 on success;
+ * non-zero fails the call with SRMRA_ERR_NCCL.  Use: host transports (gloo / MPI), tests that run several
+ * ranks on one GPU.  With a provider set, the iteration is never captured in a CUDA graph.
+ */
+typedef int (*srmra_allreduce_fn)(double* buf_dev, uint64_t n, void* stream, void* user);
+
 typedef struct {
     int32_t path;        /* SRMRA_PATH_*; default AUTO                                              */
     int32_t proj_every;  /* F: project after iteration t (0-based, counted over the context's life)
@@ -75,6 +88,16 @@ typedef struct {
                             broadcast by the caller (e.g. torch.distributed); ignored if world == 1  */
     void* stream;        /* cudaStream_t to enqueue on, or NULL: the context creates its own          */
     int32_t trace_cap;   /* capacity of the on-device log-likelihood trace; default 4096              */
+    srmra_allreduce_fn allreduce; /* world > 1: exchange provider used instead of NCCL (nccl_id is then
+                            ignored); NULL = NCCL                                                     */
+    void* allreduce_user; /* passed to `allreduce` unchanged                                           */
+    int32_t grid_cap;    /* upper bound on the persistent E/M grid of the FFT path (CTAs; clusters at
+                            L_low = 128), so that each CTA walks several observations even at small
+                            n_local (test hook of the persistent loop); <= 0 = one per SM (default)    */
+    int32_t nccl_timeout_ms; /* world > 1 with NCCL: a synchronising call that waits longer than this for
+                            the stream while ncclCommGetAsyncError reports no error aborts the
+                            communicator and fails with SRMRA_ERR_NCCL; <= 0 = wait without limit
+                            (errors reported by NCCL still abort); default 0                          */
 } srmra_options;
 
 /* Fill *opt with the defaults above. */
@@ -131,7 +154,12 @@ SRMRA_API int srmra_generate(srmra_ctx* ctx, const float* x_true, const double* 
 SRMRA_API int srmra_get_observations(srmra_ctx* ctx, int64_t first, int64_t count, float* y_out);
 
 /* Enqueue n_iters >= 0 EM iterations on the context stream; asynchronous (no host sync).
- * With world > 1 each iteration performs one NCCL all-reduce of the sufficient statistics. */
+ * With world > 1 each iteration performs one all-reduce (NCCL, or the options' exchange provider) of the
+ * sufficient statistics: FFT path the compact float64 frequency-domain accumulators (+ the per-shift
+ * posterior mass with a joint prior); GEMM / direct paths the packed b | class mass | marginals | LL
+ * (+ the per-shift posterior mass with a joint prior).  FFT path with NCCL: one iteration (E/M kernel,
+ * reduce, ncclAllReduce, fold / finalize / projection / prep) is captured once into a CUDA graph and
+ * replayed. */
 SRMRA_API int srmra_em_iter(srmra_ctx* ctx, int32_t n_iters);
 
 /* NEXT-3: a joint (non-separable) shift prior rho[s1 L_high + s2] (host, float64, [L_high][L_high],
@@ -162,7 +190,8 @@ SRMRA_API int srmra_set_denoiser(srmra_ctx* ctx, srmra_denoiser_fn fn, void* use
  * PAPER.md:345-349; the built-in stand-in ignores it); the run stops after the first iteration
  * t >= 1 (t counted within this run) with |LL_t - LL_{t-1}| <= rel_tol |LL_t|, LL_t the
  * log-likelihood at the input of iteration t (rel_tol <= 0: run max_iters).
- * FFT path on one rank without a denoiser hook: asynchronous — the convergence test runs on the
+ * FFT path without a denoiser hook or an exchange provider (one rank, or NCCL: every rank records the
+ * same all-reduced LL, so all take the same decision): asynchronous — the convergence test runs on the
  * device and the remaining enqueued iterations become no-ops; srmra_get_estimate reports the
  * iterations actually run.  Otherwise the host checks the log-likelihood after every iteration.
  * Errors: INVALID_ARG (max_iters < 0), STATE, CUDA, NCCL, NUMERIC (denoiser hook failure).
@@ -186,7 +215,7 @@ SRMRA_API int srmra_relative_error(srmra_ctx* ctx, const float* x_true, double* 
  * N the global number of observations.  m1: caller-owned float64 [L_low^2]; m2: float64
  * [L_low^2][L_low^2] (symmetric); either may be NULL (not both).  The sums run on the tensor cores
  * (3xTF32 tcgen05 GEMM of the transposed observations with themselves, float32 accumulation in
- * TMEM, float64 split-K combine) and are all-reduced over NCCL in float64 when world > 1.  Uses
+ * TMEM, float64 split-K combine) and are all-reduced in float64 when world > 1.  Uses
  * O(L_low^2 n_local) temporary device memory; independent of the EM state.  Synchronises.
  * Errors: INVALID_ARG (both NULL), STATE (failed context / rejected load), CUDA, NCCL.
  */

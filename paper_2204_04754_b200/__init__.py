@@ -45,10 +45,16 @@ class SrmraError(RuntimeError):
         self.code = code
 
 
+# int (*)(double* buf_dev, uint64_t n, void* stream, void* user): exchange provider (srmra_options.allreduce)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class srmra_options(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("proj_every", ctypes.c_int32), ("floor_tau", ctypes.c_double),
                 ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("trace_cap", ctypes.c_int32)]
+                ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("trace_cap", ctypes.c_int32),
+                ("allreduce", ALLREDUCE_FN), ("allreduce_user", ctypes.c_void_p), ("grid_cap", ctypes.c_int32),
+                ("nccl_timeout_ms", ctypes.c_int32)]
 
 
 # int (*)(double* x_dev, int32_t L_high, double sigma_t, void* stream, void* user)
@@ -345,8 +351,10 @@ class Context:
 
     def __init__(self, y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, path="auto", proj_every=1,
                  floor_tau=-1.0, device=-1, rank=0, world=1, nccl_id: bytes | None = None, stream=None,
-                 trace_cap=4096, n_local: int | None = None):
-        """y None: n_local observations to come from generate() / load()."""
+                 trace_cap=4096, n_local: int | None = None, allreduce=None, grid_cap=0, nccl_timeout_ms=0):
+        """y None: n_local observations to come from generate() / load().  allreduce: exchange provider
+        fn(buf_dev_ptr: int, n: int, stream: int) -> int (0 = ok) used instead of NCCL for world > 1
+        (include/srmra.h, srmra_allreduce_fn)."""
         o = srmra_default_options()
         o.path = PATH_IDS[path] if isinstance(path, str) else int(path)
         o.proj_every = int(proj_every)
@@ -359,6 +367,12 @@ class Context:
             o.nccl_id = ctypes.cast(self._id_buf, ctypes.c_void_p)
         o.stream = stream
         o.trace_cap = int(trace_cap)
+        o.grid_cap = int(grid_cap)
+        o.nccl_timeout_ms = int(nccl_timeout_ms)
+        self._allreduce = None
+        if allreduce is not None:
+            self._allreduce = ALLREDUCE_FN(lambda buf, n, st, user: int(allreduce(buf, n, st)))
+            o.allreduce = self._allreduce
         self.L_high, self.L_low, self.K = int(L_high), int(L_low), int(K)
         self.n_local = int(np.asarray(y).shape[0]) if y is not None else int(n_local)
         self.handle = srmra_init(y, L_high, L_low, K, sigma, x0, rho1_0, rho2_0, o, n_local=self.n_local)

@@ -779,6 +779,7 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     int64_t grid = (int64_t)c->num_sms * per_sm;
     const int64_t max_grid = (c->n_local + groups - 1) / groups;
     if (grid > max_grid) grid = max_grid;
+    if (c->opt.grid_cap > 0 && grid > c->opt.grid_cap) grid = c->opt.grid_cap;  // test hook: several obs per CTA
     if (c->fft_part_cap > 0 && grid > c->fft_part_cap) grid = c->fft_part_cap;  // partial buffers of the first plan
     if (grid < 1) grid = 1;
     c->fft_grid = (int)grid;
@@ -898,5 +899,6 @@ cudaError_t launch_fft_em(srmra_ctx* c) {
 // prep, em, reduce, fold
 // E/M kernel (if the shard is non-empty) + tail (+ a separate reduce-only tail when world > 1)
 int fft_launches_per_iter(const srmra_ctx* c) { return (c->n_local > 0 ? 1 : 0) + 1 + (c->opt.world > 1 ? 1 : 0); }
+// (with world > 1 the NCCL all-reduce kernel between the two tails is NCCL's, not counted here)
 
 }  // namespace srmra

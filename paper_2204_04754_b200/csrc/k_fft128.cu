@@ -577,6 +577,7 @@ cudaError_t fft128_plan(srmra_ctx* c) {
     if (max_clusters < 1) return cudaErrorInvalidConfiguration;
     int64_t clusters = max_clusters;
     if (clusters > c->n_local) clusters = c->n_local;
+    if (c->opt.grid_cap > 0 && clusters > c->opt.grid_cap) clusters = c->opt.grid_cap;  // test hook: several obs per cluster
     if (clusters < 1) clusters = 1;
     c->fft_grid = (int)clusters;  // partial slots (one per cluster)
     c->fft_groups = (c->KK + 1) / 2;

@@ -428,7 +428,7 @@ template <bool JOINT>
 __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     extern __shared__ double sm[];
     if (*reinterpret_cast<volatile int*>(a.run)) return;  // a converged srmra_run: nothing left to do
-    if (a.iter) {  // graph-replayable: the iteration index and the projection flag come from the device
+    {  // graph-replayable: the iteration index and the projection flag come from the device
         a.t = *reinterpret_cast<volatile int*>(a.iter);
         a.project = a.proj_every > 0 && ((a.t + 1) % a.proj_every == 0);
     }
@@ -480,15 +480,15 @@ int fft_tail_grid(const srmra_ctx* c) {
     return g < 1 ? 1 : g;
 }
 
-cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project) {
+cudaError_t launch_fft_tail(srmra_ctx* c, int mode) {
     const int Ll = c->Ll, Lh = Ll / 2 + 1;
     TailArgs a;
     a.stamps = c->d_stamps;
     a.mode = mode;
     a.L = c->L;
     a.K = c->K;
-    a.t = t;
-    a.project = project;
+    a.t = 0;        // both read from the device iteration counter by the kernel (graph-replayable)
+    a.project = 0;
     a.iter = c->d_iter;
     a.run = c->d_run;
     a.rtol = c->d_rtol;

@@ -4,7 +4,9 @@
 // the NCCL communicator (libnccl.so.2 is dlopen'ed on first use, so single-GPU use has no NCCL
 // dependency and, inside a PyTorch process, the already-loaded NCCL is reused).
 #include <algorithm>
+#include <chrono>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <math.h>
 #include <nccl.h>
 #include <stdio.h>
@@ -38,6 +40,8 @@ struct NcclApi {
     decltype(&ncclAllReduce) AllReduce = nullptr;
     decltype(&ncclCommDestroy) CommDestroy = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
 };
 NcclApi& nccl() {
     static NcclApi api;
@@ -53,7 +57,10 @@ NcclApi& nccl() {
         api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
         api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
         api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-        if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString)
+        api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+        api.CommAbort = (decltype(api.CommAbort))dlsym(h, "ncclCommAbort");
+        if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString ||
+            !api.CommGetAsyncError || !api.CommAbort)
             api.err = "libnccl.so.2 lacks a required symbol";
         else
             api.loaded = true;
@@ -81,6 +88,44 @@ int cuda_fail(srmra_ctx* c, cudaError_t e, const char* where) {
     do {                                                           \
         cudaError_t e_ = (call);                                   \
         if (e_ != cudaSuccess) return cuda_fail(c, e_, #call);     \
+    } while (0)
+
+// Wait for the context stream.  With an NCCL communicator the wait polls ncclCommGetAsyncError (SURVEY §5:
+// a dead peer must not hang the caller): an asynchronous NCCL error, or opt.nccl_timeout_ms without
+// completion, aborts the communicator and fails the context.
+int stream_wait(srmra_ctx* c) {
+    if (!c->nccl_comm) {
+        const cudaError_t e = cudaStreamSynchronize(c->stream);
+        return e == cudaSuccess ? SRMRA_OK : cuda_fail(c, e, "cudaStreamSynchronize");
+    }
+    NcclApi& api = nccl();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t e = cudaStreamQuery(c->stream);
+        if (e == cudaSuccess) return SRMRA_OK;
+        if (e != cudaErrorNotReady) return cuda_fail(c, e, "cudaStreamQuery");
+        ncclResult_t ae = ncclSuccess;
+        const ncclResult_t r = api.CommGetAsyncError((ncclComm_t)c->nccl_comm, &ae);
+        std::string why;
+        if (r != ncclSuccess) why = std::string("ncclCommGetAsyncError: ") + api.GetErrorString(r);
+        else if (ae != ncclSuccess && ae != ncclInProgress) why = std::string("NCCL asynchronous error: ") + api.GetErrorString(ae);
+        else if (c->opt.nccl_timeout_ms > 0 &&
+                 std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() >
+                     c->opt.nccl_timeout_ms)
+            why = "stream did not complete within nccl_timeout_ms (peer lost?)";
+        if (!why.empty()) {
+            api.CommAbort((ncclComm_t)c->nccl_comm);
+            c->nccl_comm = nullptr;
+            return fail(c, SRMRA_ERR_NCCL, why);
+        }
+        if (spin > 64) usleep(20);
+    }
+}
+
+#define SYNC()                                   \
+    do {                                         \
+        const int rc_ = stream_wait(c);          \
+        if (rc_ != SRMRA_OK) return rc_;         \
     } while (0)
 
 template <typename T>
@@ -133,7 +178,7 @@ void drop_graphs(srmra_ctx* c) {
 // FFT path: switch the E/M kernel between the separable and the joint-prior variant (NEXT-3)
 int fft_joint_mode(srmra_ctx* c, bool on) {
     if (c->path != SRMRA_PATH_FFT || c->fft_joint == on) return SRMRA_OK;
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     drop_graphs(c);
     const cudaError_t e = fft_plan_joint(c, on);
     if (e != cudaSuccess) return fail(c, SRMRA_ERR_UNSUPPORTED, std::string("FFT joint-prior plan: ") + cudaGetErrorString(e));
@@ -192,11 +237,11 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     if (c->path == SRMRA_PATH_GEMM) CK(launch_gemm_init(c));
     if (c->path == SRMRA_PATH_FFT) {
         if (!chunked) CK(launch_fft_init(c, 0, c->n_local));
-        CK(launch_fft_tail(c, TAIL_PREP, 0, 0));  // Xhat and logit bias of theta_0
+        CK(launch_fft_tail(c, TAIL_PREP));  // Xhat and logit bias of theta_0
     }
     int flag = 0;
     CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
+    SYNC();  // host vectors above go out of scope
     c->iters_done = 0;
     if (flag & 2) {  // k_ynorm found a non-finite observation value
         c->needs_load = true;
@@ -207,21 +252,41 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     return SRMRA_OK;
 }
 
-// The one data-path collective: sum this rank's sufficient statistics over all ranks (SURVEY §8(e)).
-// FFT path: the compact float64 accumulators (U, V, row sums, pair line, LL) — the fold after it is
-// linear, so fold(sum) = sum(fold);  direct path: the packed b | class mass | marginals | LL.
-int allreduce_stats(srmra_ctx* c) {
-    if (c->opt.world <= 1) return SRMRA_OK;
+// Sum a device float64 buffer over all ranks on the context stream: the options' exchange provider if
+// one is set, else ncclAllReduce (no-op for world 1).
+int exchange(srmra_ctx* c, double* buf, size_t n) {
+    if (c->opt.world <= 1 || n == 0) return SRMRA_OK;
+    if (c->opt.allreduce) {
+        if (c->opt.allreduce(buf, (uint64_t)n, (void*)c->stream, c->opt.allreduce_user) != 0)
+            return fail(c, SRMRA_ERR_NCCL, "exchange provider (srmra_options.allreduce) failed");
+        return SRMRA_OK;
+    }
     NcclApi& api = nccl();
-    double* buf = c->path == SRMRA_PATH_FFT ? c->d_bhat : c->d_pack;
-    const size_t n = c->path == SRMRA_PATH_FFT ? fft_bhat_doubles(c->KK, c->Ll) : (size_t)c->pk.total;
     ncclResult_t r = api.AllReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
     if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
-    if (c->path == SRMRA_PATH_FFT && c->fft_joint) {  // + the per-shift posterior mass of the joint prior
-        r = api.AllReduce(c->d_jacc, c->d_jacc, fft_joint_bins(c->KK, c->Ll), ncclFloat64, ncclSum,
-                          (ncclComm_t)c->nccl_comm, c->stream);
-        if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
-    }
+    return SRMRA_OK;
+}
+
+// The one data-path collective: sum this rank's sufficient statistics over all ranks (SURVEY §8(e)).
+// FFT path: the compact float64 accumulators (U, V, row sums, pair line, LL) — the fold after it is
+// linear, so fold(sum) = sum(fold) — plus, with a joint prior, the per-shift posterior mass;
+// GEMM / direct paths: the packed b | class mass | marginals | LL, and with a joint prior the per-shift
+// posterior mass colsum that finalize divides by the global total (d_colsum sits right after the pack,
+// so it is the same single collective).
+int allreduce_stats(srmra_ctx* c) {
+    if (c->opt.world <= 1) return SRMRA_OK;
+    if (c->path != SRMRA_PATH_FFT)
+        return exchange(c, c->d_pack, (size_t)c->pk.total + (c->joint ? (size_t)c->L2 : 0));
+    int rc = exchange(c, c->d_bhat, fft_bhat_doubles(c->KK, c->Ll));
+    if (rc == SRMRA_OK && c->fft_joint) rc = exchange(c, c->d_jacc, fft_joint_bins(c->KK, c->Ll));
+    return rc;
+}
+
+
+// A converged srmra_run leaves the device stop flag set, which makes the E/M and tail kernels return at
+// once (so that the remaining enqueued replays are no-ops).  Every launch outside iterate() clears it first.
+int clear_stop(srmra_ctx* c) {
+    CK(cudaMemsetAsync(c->d_run, 0, sizeof(int), c->stream));
     return SRMRA_OK;
 }
 
@@ -275,18 +340,21 @@ int set_run_control(srmra_ctx* c, double rel_tol) {
 
 // After a denoiser hook replaced x64: the float32 copy and (FFT path) the next iteration's spectra
 int refresh_after_denoise(srmra_ctx* c) {
-    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_tail(c, TAIL_PREP, c->iters_done, 0));  // also writes x32
+    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_tail(c, TAIL_PREP));  // also writes x32
     else CK(launch_x32_from_x64(c));
     return SRMRA_OK;
 }
 
 // n_iters EM iterations of Algorithm 2 (srmra_em_iter: rel_tol = 0; srmra_run: the stopping rule)
 int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
-    const bool device_loop = c->path == SRMRA_PATH_FFT && c->opt.world == 1 && !c->denoiser;
+    // one rank, or NCCL ranks (every rank records the same all-reduced LL_t, so the device stopping rule
+    // takes the same decision everywhere); a host exchange provider or a denoiser hook needs the host loop
+    const bool device_loop = c->path == SRMRA_PATH_FFT && !c->denoiser && (c->opt.world == 1 || !c->opt.allreduce);
     int rc;
     if ((rc = set_run_control(c, device_loop ? rel_tol : 0.0)) != SRMRA_OK) return rc;
-    // FFT path on one rank: replay a captured CUDA graph of one iteration (E/M kernel + cooperative
-    // tail); the tail takes t and the projection flag from the device counter.  With profiling on, the
+    // FFT path: replay a captured CUDA graph of one iteration (E/M kernel + cooperative tail; world > 1:
+    // E/M kernel, reduce-only tail, ncclAllReduce, fold / finalize / prep tail); the tail takes t and the
+    // projection flag from the device counter.  With profiling on, the
     // graph variant carries 4 event-record nodes that are re-pointed to fresh pool events per replay.
     if (device_loop && !c->graph_failed && n_iters > 0) {
         cudaGraphExec_t* exec = &c->graph;  // profiling needs no event nodes: the E/M kernel stamps itself
@@ -304,7 +372,13 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
                 if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[1], c->stream, cudaEventRecordExternal) == cudaSuccess;
                 l = l && launch_fft_em(c) == cudaSuccess;
                 if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[2], c->stream, cudaEventRecordExternal) == cudaSuccess;
-                l = l && launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP, 0, 0) == cudaSuccess;
+                if (c->opt.world > 1) {
+                    l = l && launch_fft_tail(c, TAIL_REDUCE) == cudaSuccess;
+                    l = l && allreduce_stats(c) == SRMRA_OK;
+                    l = l && launch_fft_tail(c, TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP) == cudaSuccess;
+                } else {
+                    l = l && launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP) == cudaSuccess;
+                }
                 if (prof_nodes) l = l && cudaEventRecordWithFlags(ph[3], c->stream, cudaEventRecordExternal) == cudaSuccess;
                 ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && l;
             }
@@ -331,6 +405,8 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
                 cudaGetLastError();  // clear the capture error; stream launches are used instead
                 *exec = nullptr;
                 c->graph_failed = true;
+                c->failed = false;   // an NCCL call refused under capture is not a context failure
+                c->err.clear();
             }
             // placeholders must outlive the exec (destroying them invalidates its event-record nodes)
             for (int k = 0; k < 4; ++k) {
@@ -339,6 +415,7 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
             }
         }
         if (*exec) {
+            if (rel_tol > 0) c->iters_stale = true;  // the device may stop before n_iters
             for (int it = 0; it < n_iters; ++it) {
                 CK(cudaGraphLaunch(*exec, c->stream));
                 c->iters_done++;
@@ -359,11 +436,11 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
             // (two when the NCCL all-reduce has to sit between the reduce and the fold)
             const int rest = TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP;
             if (c->opt.world > 1) {
-                CK(launch_fft_tail(c, TAIL_REDUCE, t, project));
+                CK(launch_fft_tail(c, TAIL_REDUCE));
                 if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
-                CK(launch_fft_tail(c, rest, t, project));
+                CK(launch_fft_tail(c, rest));
             } else {
-                CK(launch_fft_tail(c, TAIL_REDUCE | rest, t, project));
+                CK(launch_fft_tail(c, TAIL_REDUCE | rest));
             }
         } else {
             if ((rc = allreduce_stats(c)) != SRMRA_OK) return rc;
@@ -380,7 +457,7 @@ int iterate(srmra_ctx* c, int32_t n_iters, double rel_tol) {
         if (rel_tol > 0 && t - t0 >= 1 && t < c->opt.trace_cap) {  // host-side stopping rule
             double ll[2];
             CK(cudaMemcpyAsync(ll, c->d_trace + (t - 1), 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
+            SYNC();
             if (fabs(ll[1] - ll[0]) <= rel_tol * fabs(ll[1])) break;
         }
     }
@@ -393,9 +470,10 @@ int sync_iters(srmra_ctx* c) {
     if (c->path == SRMRA_PATH_FFT) {
         int t = 0;
         CK(cudaMemcpyAsync(&t, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        SYNC();
         c->iters_done = t;
     }
+    c->iters_stale = false;
     return SRMRA_OK;
 }
 
@@ -405,13 +483,7 @@ int sync_iters(srmra_ctx* c) {
 namespace srmra {
 // NCCL sum of a device float64 buffer over all ranks, on the context stream (no-op for world 1);
 // the moments call (k_moments.cu) uses it for its raw sums.
-int allreduce_doubles(srmra_ctx* c, double* buf, size_t n) {
-    if (c->opt.world <= 1 || n == 0) return SRMRA_OK;
-    NcclApi& api = nccl();
-    ncclResult_t r = api.AllReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
-    if (r != ncclSuccess) return fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
-    return SRMRA_OK;
-}
+int allreduce_doubles(srmra_ctx* c, double* buf, size_t n) { return exchange(c, buf, n); }
 }  // namespace srmra
 
 namespace {
@@ -444,6 +516,10 @@ void srmra_default_options(srmra_options* o) {
     o->nccl_id = nullptr;
     o->stream = nullptr;
     o->trace_cap = 4096;
+    o->allreduce = nullptr;
+    o->allreduce_user = nullptr;
+    o->grid_cap = 0;
+    o->nccl_timeout_ms = 0;
 }
 
 const char* srmra_last_error(const srmra_ctx* ctx) { return ctx ? ctx->err.c_str() : g_init_err.c_str(); }
@@ -474,7 +550,8 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     if (!(sigma > 0) || !isfinite(sigma)) return fail(c, SRMRA_ERR_INVALID_ARG, "sigma must be finite and > 0");
     if (!x0 || !rho1_0 || !rho2_0) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(c, SRMRA_ERR_INVALID_ARG, "bad rank/world");
-    if (opt.world > 1 && !opt.nccl_id) return fail(c, SRMRA_ERR_INVALID_ARG, "world > 1 needs nccl_id");
+    if (opt.world > 1 && !opt.nccl_id && !opt.allreduce)
+        return fail(c, SRMRA_ERR_INVALID_ARG, "world > 1 needs nccl_id or an exchange provider (allreduce)");
     if (opt.proj_every < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "proj_every < 0");
     if (opt.trace_cap < 1) opt.trace_cap = 4096;
     if (!all_finite_f(x0, (size_t)L_high * L_high)) return fail(c, SRMRA_ERR_INVALID_ARG, "x0 not finite");
@@ -551,8 +628,9 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     CKI(dalloc(&c->par.f32, 2 * c->L + c->KK));
     CKI(dalloc(&c->par.f64, 2 * c->KK + 2));
     CKI(cudaMemset(c->par.f64, 0, sizeof(double) * (2 * c->KK + 2)));
-    CKI(dalloc(&c->d_colsum, c->L2));
-    CKI(dalloc(&c->d_pack, c->pk.total));
+    // pack | colsum in one buffer: with a joint prior both are all-reduced by one collective
+    CKI(dalloc(&c->d_pack, c->pk.total + c->L2));
+    c->d_colsum = c->d_pack + c->pk.total;
     CKI(dalloc(&c->d_trace, opt.trace_cap));
     CKI(dalloc(&c->d_flag, 1));
     CKI(dalloc(&c->d_counter, 1));
@@ -597,21 +675,22 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
     // global N and the NCCL communicator
     c->n_global = n_local;
     if (opt.world > 1) {
-        NcclApi& api = nccl();
-        if (!api.loaded) return bail(fail(c, SRMRA_ERR_NCCL, api.err));
-        ncclUniqueId id;
-        memcpy(&id, opt.nccl_id, sizeof(id));
-        ncclComm_t comm;
-        ncclResult_t r = api.CommInitRank(&comm, opt.world, id, opt.rank);
-        if (r != ncclSuccess) return bail(fail(c, SRMRA_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
-        c->nccl_comm = comm;
+        if (!opt.allreduce) {
+            NcclApi& api = nccl();
+            if (!api.loaded) return bail(fail(c, SRMRA_ERR_NCCL, api.err));
+            ncclUniqueId id;
+            memcpy(&id, opt.nccl_id, sizeof(id));
+            ncclComm_t comm;
+            ncclResult_t r = api.CommInitRank(&comm, opt.world, id, opt.rank);
+            if (r != ncclSuccess) return bail(fail(c, SRMRA_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
+            c->nccl_comm = comm;
+        }
         double* d_n = c->d_pack;  // scratch for the one-off N all-reduce
         double hn = (double)n_local;
         CKI(cudaMemcpyAsync(d_n, &hn, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        r = api.AllReduce(d_n, d_n, 1, ncclFloat64, ncclSum, comm, c->stream);
-        if (r != ncclSuccess) return bail(fail(c, SRMRA_ERR_NCCL, std::string("ncclAllReduce(N): ") + api.GetErrorString(r)));
+        if ((rc = exchange(c, d_n, 1)) != SRMRA_OK) return bail(rc);
         CKI(cudaMemcpyAsync(&hn, d_n, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CKI(cudaStreamSynchronize(c->stream));
+        if ((rc = stream_wait(c)) != SRMRA_OK) return bail(rc);
         c->n_global = (int64_t)llround(hn);
     }
     c->tau = opt.floor_tau >= 0 ? opt.floor_tau : 1e-12 * (double)c->n_global;
@@ -685,7 +764,7 @@ int srmra_get_observations(srmra_ctx* c, int64_t first, int64_t count, float* y_
         return fail(c, SRMRA_ERR_INVALID_ARG, "range outside [0, n_local) or NULL output");
     if (count == 0) return SRMRA_OK;
     CK(cudaMemcpyAsync(y_out, c->d_y + first * c->Ll2, sizeof(float) * count * c->Ll2, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     return SRMRA_OK;
 }
 
@@ -695,6 +774,9 @@ int srmra_em_iter(srmra_ctx* c, int32_t n_iters) {
     if (c->failed) return SRMRA_ERR_STATE;
     if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
     if (c->needs_load) return fail(c, SRMRA_ERR_STATE, "no valid observations (srmra_init with y NULL, or a rejected srmra_load): srmra_load / srmra_generate first");
+    int rc;
+    // after a device-loop srmra_run with a tolerance the host count may exceed the iterations run
+    if (c->iters_stale && (rc = sync_iters(c)) != SRMRA_OK) return rc;
     return iterate(c, n_iters, 0.0);
 }
 
@@ -779,14 +861,15 @@ int srmra_set_joint_rho(srmra_ctx* c, const double* rho) {
     }
     CK(cudaMemcpyAsync(c->d_rhoj, r.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_rho, marg.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     if (c->path == SRMRA_PATH_FFT) {
         int rc;
         if ((rc = sync_iters(c)) != SRMRA_OK) return rc;
         if ((rc = fft_joint_mode(c, true)) != SRMRA_OK) return rc;
         c->joint = true;
-        CK(launch_fft_tail(c, TAIL_PREP, c->iters_done, 0));  // the per-shift log2 prior table of the E/M kernel
-        CK(cudaStreamSynchronize(c->stream));
+        if ((rc = clear_stop(c)) != SRMRA_OK) return rc;
+        CK(launch_fft_tail(c, TAIL_PREP));  // the per-shift log2 prior table of the E/M kernel
+        SYNC();
         return SRMRA_OK;
     }
     c->joint = true;
@@ -799,7 +882,7 @@ int srmra_get_joint_rho(srmra_ctx* c, double* out) {
     if (c->failed) return SRMRA_ERR_STATE;
     if (!c->joint) return fail(c, SRMRA_ERR_STATE, "no joint shift prior set (srmra_set_joint_rho)");
     CK(cudaMemcpyAsync(out, c->d_rhoj, sizeof(double) * c->L2, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     return SRMRA_OK;
 }
 
@@ -863,8 +946,9 @@ int srmra_mom_run(srmra_ctx* c, int32_t max_steps, int32_t F, double gtol, doubl
     if (rc != SRMRA_OK) return mom_fail(c, rc, err);
     c->joint = false;  // the estimate is (x, rho1, rho2) again
     if ((rc = fft_joint_mode(c, false)) != SRMRA_OK) return rc;
+    if ((rc = clear_stop(c)) != SRMRA_OK) return rc;
     if ((rc = refresh_after_denoise(c)) != SRMRA_OK) return rc;  // EM can continue from the MoM estimate
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     return SRMRA_OK;
 }
 
@@ -880,7 +964,7 @@ int srmra_profile(srmra_ctx* c, int32_t enable) {
     DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     c->prof = enable != 0;
     c->ev_used = 0;
     if (c->path == SRMRA_PATH_FFT && c->prof) {  // arm the E/M launch stamps of the window
@@ -901,7 +985,7 @@ int srmra_profile_read(srmra_ctx* c, double* em_ms, double* iter_ms, int32_t* n_
     DevGuard dg_(c);
     if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
     if (c->failed) return SRMRA_ERR_STATE;
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     double em = 0, tot = 0;
     int n = 0;
     if (c->path == SRMRA_PATH_FFT) {
@@ -957,7 +1041,7 @@ int srmra_get_estimate(srmra_ctx* c, float* x_out, double* rho1_out, double* rho
     if (t > 0 && t <= c->opt.trace_cap)
         CK(cudaMemcpyAsync(&ll, c->d_trace + (t - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     if (loglik_out) *loglik_out = ll;
     if (iters_done) *iters_done = t;
     if (flag) return fail(c, SRMRA_ERR_NUMERIC, "non-finite log-likelihood or estimate");
@@ -973,7 +1057,7 @@ int srmra_get_loglik_trace(srmra_ctx* c, double* out, int32_t cap, int32_t* n) {
     int m = c->iters_done < c->opt.trace_cap ? c->iters_done : c->opt.trace_cap;
     if (m > cap) m = cap;
     if (m > 0 && out) CK(cudaMemcpyAsync(out, c->d_trace, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     if (n) *n = c->iters_done;
     return SRMRA_OK;
 }
@@ -986,7 +1070,7 @@ int srmra_get_stats(srmra_ctx* c, double* b, double* cmass, double* m1, double* 
     if (cmass) CK(cudaMemcpyAsync(cmass, c->d_pack + c->pk.cmass, sizeof(double) * c->KK, cudaMemcpyDeviceToHost, c->stream));
     if (m1) CK(cudaMemcpyAsync(m1, c->d_pack + c->pk.m1, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
     if (m2) CK(cudaMemcpyAsync(m2, c->d_pack + c->pk.m2, sizeof(double) * c->L, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     return SRMRA_OK;
 }
 
@@ -995,7 +1079,7 @@ int srmra_get_obs_loglik(srmra_ctx* c, double* out) {
     if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
     if (c->n_local) CK(cudaMemcpyAsync(out, c->d_llobs, sizeof(double) * c->n_local, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     return SRMRA_OK;
 }
 
@@ -1003,14 +1087,16 @@ int srmra_local_stats(srmra_ctx* c, double* out) {
     DevGuard dg_(c);
     if (!c || !out) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (c->failed) return SRMRA_ERR_STATE;
+    int rc;
+    if ((rc = sync_iters(c)) != SRMRA_OK || (rc = clear_stop(c)) != SRMRA_OK) return rc;
     const bool prof = c->prof;
     c->prof = false;  // keep the profiling records aligned to whole iterations
-    int rc = local_estep_mstep(c);
+    rc = local_estep_mstep(c);
     c->prof = prof;
     if (rc != SRMRA_OK) return rc;
-    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD, 0, 0));  // local, no update
+    if (c->path == SRMRA_PATH_FFT) CK(launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD));  // local, no update
     CK(cudaMemcpyAsync(out, c->d_pack, sizeof(double) * c->pk.total, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     return SRMRA_OK;
 }
 
@@ -1021,7 +1107,7 @@ int srmra_debug_timestamps(srmra_ctx* c, uint64_t* out8) {
     if (!c || !out8) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL argument");
     if (!c->d_stamps) return fail(c, SRMRA_ERR_STATE, "set SRMRA_TAIL_STAMPS before srmra_init");
     CK(cudaMemcpyAsync(out8, c->d_stamps, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    SYNC();
     // re-arm the cross-block extremes: [6] earliest tail-block start (min), [7] latest tail-block end (max)
     const uint64_t arm[2] = {~0ull, 0ull};
     CK(cudaMemcpy(c->d_stamps + 6, arm, sizeof(arm), cudaMemcpyHostToDevice));
@@ -1045,7 +1131,7 @@ void srmra_free(srmra_ctx* c) {
         if (api.loaded) api.CommDestroy((ncclComm_t)c->nccl_comm);
     }
     void* bufs[] = {c->d_y, c->d_yhat, c->d_ysum, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
-                    c->par.f32, c->par.f64, c->d_xhat, c->d_colsum, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
+                    c->par.f32, c->par.f64, c->d_xhat, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
                     c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps};
     for (void* p : bufs)
         if (p) cudaFree(p);

@@ -107,6 +107,7 @@ struct srmra_ctx {
     unsigned long long* d_emt = nullptr;     // [trace_cap][2] E/M kernel first-CTA start / last-CTA end (globaltimer ns)
     int prof_t0 = 0;                         // first iteration of the current profiling window
     int iters_done = 0;
+    bool iters_stale = false;                // a device-loop run may have stopped early: sync_iters first
 
     // gemm path (k_gemm.cu): tf32 hi|lo splits, scores, transposed posterior, Z = W^T Y, rotated x copies
     float* g_yhl = nullptr;   // [2][n][Ll2]
@@ -176,7 +177,7 @@ cudaError_t launch_gemm_init(srmra_ctx* c);
 cudaError_t launch_gemm_em(srmra_ctx* c, cudaEvent_t ev_em0, cudaEvent_t ev_em1);
 // cooperative tail kernel of the FFT path (k_fft_tail.cu): phases selected by TAIL_* bits
 enum { TAIL_REDUCE = 1, TAIL_FOLD = 2, TAIL_FINALIZE = 4, TAIL_PREP = 8 };
-cudaError_t launch_fft_tail(srmra_ctx* c, int mode, int t, int project);
+cudaError_t launch_fft_tail(srmra_ctx* c, int mode);
 int fft_launches_per_iter(const srmra_ctx* c);
 size_t fft_bhat_doubles(int KK, int Ll);  // Bhat [KK][Ll][Lh] complex + mass lines [KK][Ll+Lh] complex
 size_t fft_yhat_stride(int Ll);           // float2 per observation in d_yhat (16-byte multiple)

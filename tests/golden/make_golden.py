@@ -6,6 +6,11 @@ north_star parity setting), the LL trace, and, for the first iteration, the per-
 log-likelihood terms of a fixed sample of observations.
 
     python tests/golden/make_golden.py c1 c3 c2
+    python tests/golden/make_golden.py --dense c4
+
+--dense uses oracle.dense.em_iter_dense (the same iteration as the dense float64 contraction
+S = Y T(x)^T, Z = W^T Y through BLAS; pinned to the brute-force oracle.em_iter in
+tests/test_oracle_pins.py): the brute-force loop would take ~30 h at configs[4].
 """
 import os
 import sys
@@ -26,7 +31,9 @@ def sample_idx(N, k=64):
     return np.unique(np.linspace(0, N - 1, k).astype(np.int64))
 
 
-def main(names):
+def main(names, dense=False):
+    if dense:
+        from oracle.dense import em_iter_dense
     for name in names:
         p = synth.make_config(name)
         t0 = time.time()
@@ -34,7 +41,10 @@ def main(names):
         trace = []
         ll_obs0 = None
         for t in range(p.iters):
-            r = oracle.em_iter(p.y, p.L_low, p.K, p.sigma, x, r1, r2, project=True)
+            if dense:
+                r = em_iter_dense(p.y, p.L_low, p.K, p.sigma, x, r1, r2, project=True, verbose=True)
+            else:
+                r = oracle.em_iter(p.y, p.L_low, p.K, p.sigma, x, r1, r2, project=True)
             if t == 0:
                 ll_obs0 = r.ll_obs[sample_idx(p.N)]
             x, r1, r2 = r.x, r.rho1, r.rho2
@@ -42,8 +52,10 @@ def main(names):
             print(f"{name} iter {t}: LL={r.loglik:.10e}  ({time.time() - t0:.1f}s)", flush=True)
         np.savez(os.path.join(OUT, f"{name}_oracle.npz"), x=x, rho1=r1, rho2=r2, trace=np.array(trace),
                  ll_obs0_idx=sample_idx(p.N), ll_obs0=ll_obs0, iters=p.iters,
-                 threads=oracle.max_threads(), seconds=time.time() - t0)
+                 threads=oracle.max_threads(), seconds=time.time() - t0,
+                 form="dense" if dense else "brute_force")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1"])
+    args = [a for a in sys.argv[1:] if a != "--dense"]
+    main(args or ["c1"], dense="--dense" in sys.argv[1:])

@@ -86,6 +86,68 @@ def test_em_iter_after_a_converged_run_resumes(srm):
         assert ctx.loglik_trace().shape == (5,)
 
 
+def _converged(srm, p, path="fft"):
+    ctx = srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path)
+    ctx.run(20, 1e30)   # stops on the device after iteration t = 1; the stop flag stays set
+    return ctx
+
+
+def test_joint_prior_after_a_converged_run(srm, oracle_mod):
+    """srmra_set_joint_rho after a converged run must build the log-prior table (its prep launch must not
+    see the stop flag) and the next iteration must be the oracle's joint iteration from that estimate."""
+    p = synth.make_config("c0")
+    L = p.L_high
+    rng = np.random.default_rng(3)
+    pr = rng.uniform(0.05, 1.0, (L, L)) ** 3
+    pr /= pr.sum()
+    with _converged(srm, p) as ctx:
+        x1, *_, it = ctx.get_estimate()
+        assert it == 2
+        ctx.set_joint_rho(pr)
+        ctx.em_iter(1)
+        x, r1, r2, ll, it = ctx.get_estimate()
+        rj = ctx.joint_rho()
+    assert it == 3
+    with srm.Context(p.y, L, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0) as ref_ctx:
+        ref_ctx.em_iter(2)                     # the same theta_2 as the converged run
+        x2, *_ = ref_ctx.get_estimate()
+    np.testing.assert_array_equal(x1, x2)
+    ref = oracle_mod.em_iter_joint(p.y, p.L_low, p.K, p.sigma, x2.astype(np.float64), pr, project=True)
+    assert np.abs(x - ref.x).max() <= X_TOL * np.abs(ref.x).max()
+    assert np.abs(rj - ref.rho).max() <= RHO_TOL * ref.rho.max()
+    assert abs(ll - ref.loglik) <= LL_TOL * abs(ref.loglik)
+
+
+def test_local_stats_after_a_converged_run(srm):
+    """srmra_local_stats after a converged run computes fresh statistics at the current theta."""
+    p = synth.make_config("c0")
+    with _converged(srm, p) as ctx:
+        st = ctx.local_stats()
+        x2, r1, r2, *_ = ctx.get_estimate()
+    with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0) as ref_ctx:
+        ref_ctx.em_iter(2)
+        ref = ref_ctx.local_stats()
+    np.testing.assert_allclose(st, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    assert abs(st[p.L_high ** 2:p.L_high ** 2 + p.K ** 2].sum() - p.N) <= 1e-6 * p.N
+
+
+def test_mom_run_after_a_converged_run_continues_em_from_the_mom_estimate(srm, oracle_mod):
+    """srmra_mom_run after a converged EM run: the refreshed spectra / log prior of the MoM estimate must be
+    written (not skipped by the stop flag), so the next EM iteration starts from the MoM estimate."""
+    p = synth.make_config("c0")
+    with _converged(srm, p) as ctx:
+        ctx.mom_set_moments()
+        ctx.mom_run(3, F=0)
+        xm, rm1, rm2, *_ = ctx.get_estimate()
+        ctx.em_iter(1)
+        x, r1, r2, ll, it = ctx.get_estimate()
+    ref = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, xm.astype(np.float64), rm1, rm2, project=True)
+    # the context keeps x in float64; xm is its float32 copy, so compare at the float32 level of x
+    assert np.abs(x - ref.x).max() <= X_TOL * np.abs(ref.x).max()
+    assert max(np.abs(r1 - ref.rho1).max() / ref.rho1.max(), np.abs(r2 - ref.rho2).max() / ref.rho2.max()) <= RHO_TOL
+    assert abs(ll - ref.loglik) <= 1e-5 * abs(ref.loglik)
+
+
 def test_denoiser_hook_identity_and_sigma_schedule(srm, oracle_mod):
     """An identity denoiser installed as the hook: the run equals EM without projection, the hook is
     called after every F-th iteration with sigma_j = 2^(-(j-1)/10)."""

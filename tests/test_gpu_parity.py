@@ -70,6 +70,8 @@ TINY = [  # (L_low, K, N, sigma, seed, rho_zeros)
     # odd K^2), K = 2 (configs[4] geometry, 2-CTA clusters) with zeros in rho; configs[4]'s image
     # recipe and noise level (the fp32 score floor at this size)
     (128, 1, 5, 0.5, 11, 0, "blobs"), (128, 2, 6, 0.5, 12, 2, "blobs"), (128, 2, 9, 0.5, 13, 0, "blobs"),
+    # K = 3: odd K^2 > 1 (five class pairs, the last with an empty half) on every path, odd N, zeros in rho
+    (4, 3, 27, 0.4, 14, 2), (8, 3, 19, 0.3, 15, 0), (32, 3, 13, 0.25, 16, 3), (2, 3, 21, 0.5, 17, 1),
 ]
 
 
@@ -141,16 +143,56 @@ def test_c1_reduced_three_iters(srm, oracle_mod):
         assert_close(g, x, r1, r2, trace, tag="c1/N=1000")
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_full_config_vs_golden(srm, name):
+    """Every config at full size, in the launch configuration bench.py times (AUTO path, default grid),
+    against the committed oracle outputs (tests/golden/make_golden.py; c4 via the dense float64 form of
+    oracle/dense.py, pinned to the brute-force loop): x, rho, the LL trace, and the first iteration's
+    per-observation LL terms of a fixed sample of observations."""
     f = os.path.join(GOLDEN, f"{name}_oracle.npz")
     if not os.path.exists(f):
         pytest.skip(f"{f} not generated (tests/golden/make_golden.py)")
     gold = np.load(f)
     p = synth.make_config(name)
-    for path in gpu_paths(srm, p):
-        g = run_gpu(srm, p, path, int(gold["iters"]))
+    paths = gpu_paths(srm, p)
+    assert "fft" in paths
+    for path in paths:
+        if gold["iters"] == 1:
+            g = run_gpu(srm, p, path, 1)
+        else:  # per-observation terms of the first iteration, then the remaining iterations
+            with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path=path) as ctx:
+                ctx.em_iter(1)
+                llo = ctx.obs_loglik()
+                ctx.em_iter(int(gold["iters"]) - 1)
+                x, r1, r2, ll, it = ctx.get_estimate()
+                g = dict(x=x, rho1=r1, rho2=r2, trace=ctx.loglik_trace(), llo=llo, path=path)
         assert_close(g, gold["x"], gold["rho1"], gold["rho2"], gold["trace"], tag=name)
+        idx = gold["ll_obs0_idx"]
+        err = np.abs(g["llo"][idx] - gold["ll_obs0"]) / np.abs(gold["ll_obs0"])
+        assert err.max() <= LL_TOL, (name, path, err.max())
+
+
+# the persistent E/M loop: every CTA (cluster at L_low = 128) walks several observations, so the
+# per-CTA accumulation across observations (TMEM at L_low >= 32) and the prefetch of the next Yhat run
+# element by element against the oracle
+PERSIST = [("c4", 40, 3), ("c4", 21, 4), ("c3", 301, 5), ("c1", 333, 4), ("c2", 65, 3)]
+
+
+@pytest.mark.parametrize("name,N,cap", PERSIST, ids=[f"{c[0]}N{c[1]}cap{c[2]}" for c in PERSIST])
+def test_persistent_loop_several_obs_per_cta(srm, oracle_mod, name, N, cap):
+    p = synth.make_config(name, N=N)
+    ref = oracle_mod.em_iter(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path="fft",
+                     grid_cap=cap) as ctx:
+        ctx.em_iter(1)
+        x, r1, r2, ll, it = ctx.get_estimate()
+        llo = ctx.obs_loglik()
+        b, cm, m1, m2 = ctx.stats()
+    assert_close(dict(x=x, rho1=r1, rho2=r2, trace=[ll], path="fft"), ref.x, ref.rho1, ref.rho2, [ref.loglik],
+                 tag=f"{name}/N={N}/grid_cap={cap}")
+    np.testing.assert_allclose(llo, ref.ll_obs, rtol=LL_TOL)
+    np.testing.assert_allclose(b, ref.b, rtol=0, atol=X_TOL * np.abs(ref.b).max())
+    np.testing.assert_allclose(m1, ref.colsum.sum(1), rtol=0, atol=RHO_TOL * ref.colsum.sum(1).max())
 
 
 @pytest.mark.slow

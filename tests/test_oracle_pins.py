@@ -587,3 +587,71 @@ def test_mom_objective_definition_zero_and_invariance(oracle_mod):
     fs = oracle_mod.mom_objective(np.roll(x, u, axis=(0, 1)), np.roll(r1, -u[0]), np.roll(r2, -u[1]), K, sigma,
                                   M1, M2)[0]
     np.testing.assert_allclose(fs, f, rtol=1e-12)
+
+
+# ----------------------------------------------------------------------- dense-contraction form
+# oracle/dense.py evaluates the same iteration as S = Y T(x)^T, Z = W^T Y through float64 BLAS (used for
+# the configs[4] golden, where the brute-force loop would take ~30 h).  Pinned to the dense matrix form
+# above (P and R_s built from their definitions) and to the brute-force loop on shapes with K = 2, 3, 4,
+# odd L_low, zeros in rho and ragged chunking.
+@pytest.mark.parametrize("Ll,K,N,sigma,seed,zeros", [(2, 2, 5, 0.7, 0, 0), (2, 2, 7, 0.5, 2, 1), (2, 3, 4, 0.6, 3, 1)])
+def test_dense_form_equals_matrix_form(Ll, K, N, sigma, seed, zeros):
+    from oracle.dense import em_iter_dense
+    p = synth.make_random(Ll, K, N, sigma, seed, rho_zeros=zeros)
+    x = p.x0.astype(np.float64)
+    d = dense_em(p.y, p.K, p.sigma, x, p.rho1_0, p.rho2_0)
+    r = em_iter_dense(p.y, p.L_low, p.K, p.sigma, x, p.rho1_0, p.rho2_0, project=False, tau=0.0, chunk=3)
+    np.testing.assert_allclose(r.A.reshape(-1), np.diag(d["A"]), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(r.b.reshape(-1), d["b"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(r.colsum, d["colsum"], rtol=1e-11, atol=1e-14)
+    assert abs(r.loglik - d["LL"]) <= 1e-12 * abs(d["LL"])
+    np.testing.assert_allclose(r.rho1, d["rho1"], rtol=1e-11, atol=1e-15)
+    np.testing.assert_allclose(r.x, np.linalg.solve(d["A"], d["b"]).reshape(x.shape), rtol=1e-11, atol=1e-12)
+
+
+@pytest.mark.parametrize("Ll,K,N,sigma,seed,zeros", [
+    (4, 2, 37, 0.3, 1, 0), (4, 3, 21, 0.5, 2, 2), (3, 3, 17, 0.4, 6, 0), (8, 4, 9, 0.4, 3, 1),
+    (16, 2, 50, 0.25, 4, 3), (5, 3, 13, 0.6, 5, 0)])
+def test_dense_form_equals_bruteforce(oracle_mod, Ll, K, N, sigma, seed, zeros):
+    from oracle.dense import em_iter_dense
+    p = synth.make_random(Ll, K, N, sigma, seed, rho_zeros=zeros)
+    a = oracle_mod.em_iter(p.y, Ll, K, sigma, p.x0, p.rho1_0, p.rho2_0, project=True)
+    b = em_iter_dense(p.y, Ll, K, sigma, p.x0, p.rho1_0, p.rho2_0, project=True, chunk=7)
+    for f in ("x", "b", "A", "colsum", "ll_obs", "rho1", "rho2"):
+        u, v = getattr(a, f), getattr(b, f)
+        assert np.abs(u - v).max() <= 1e-12 * np.abs(u).max() + 1e-300, f
+    assert abs(a.loglik - b.loglik) <= 1e-13 * abs(a.loglik)
+    assert np.all(b.rho1[p.rho1_0 == 0] == 0) and np.all(b.rho2[p.rho2_0 == 0] == 0)
+
+
+def test_dense_form_reproduces_c1_golden():
+    """configs[1]'s committed golden (10 projected iterations of the brute-force loop) from the dense form."""
+    from oracle.dense import em_iter_dense
+    g = np.load(os.path.join(GOLDEN, "c1_oracle.npz"))
+    p = synth.make_config("c1")
+    x, r1, r2, tr = p.x0, p.rho1_0, p.rho2_0, []
+    for _ in range(int(g["iters"])):
+        r = em_iter_dense(p.y, p.L_low, p.K, p.sigma, x, r1, r2, project=True, chunk=4096)
+        x, r1, r2 = r.x, r.rho1, r.rho2
+        tr.append(r.loglik)
+    assert np.abs(x - g["x"]).max() <= 1e-12
+    assert np.abs(r1 - g["rho1"]).max() <= 1e-13 and np.abs(r2 - g["rho2"]).max() <= 1e-13
+    np.testing.assert_allclose(tr, g["trace"], rtol=1e-13)
+
+
+# ----------------------------------------------------------------------- indexed log-likelihood
+@pytest.mark.parametrize("Ll,K,N,sigma,seed", [(4, 2, 23, 0.4, 1), (3, 3, 11, 0.5, 2), (8, 4, 7, 0.3, 3),
+                                               (128, 2, 3, 0.5, 4)])
+def test_loglik_obs_equals_em_iter_terms(oracle_mod, Ll, K, N, sigma, seed):
+    """oracle.loglik_obs (the per-observation checker of the full-size configs[4] test) equals the
+    per-observation terms of em_iter at any index set, order and repetition (an index-offset mistake
+    would pick another observation's term)."""
+    p = synth.make_random(Ll, K, N, sigma, seed, rho_zeros=1, image="blobs" if Ll >= 64 else "noise")
+    r = oracle_mod.em_iter(p.y, Ll, K, sigma, p.x0, p.rho1_0, p.rho2_0, project=False)
+    idx = np.array([N - 1, 0, N // 2, 0, 1 % N])
+    got = oracle_mod.loglik_obs(p.y, idx, Ll, K, sigma, p.x0, p.rho1_0, p.rho2_0)
+    np.testing.assert_allclose(got, r.ll_obs[idx], rtol=1e-14)
+    # and each term is the log normaliser of that observation's own posterior (eq:weights_EM)
+    for i in {0, N - 1}:
+        _, lse = oracle_mod.posterior(p.y[i], Ll, K, sigma, p.x0, p.rho1_0, p.rho2_0)
+        assert abs(lse - r.ll_obs[i]) <= 1e-14 * abs(lse)
