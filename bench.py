@@ -226,6 +226,7 @@ def run_ours(args):
     clk = clocks.stop()
     em_ms, iter_ms, n_prof = ctx.profile_read()
     ctx.profile(False)
+    ctx.get_estimate()  # raises SrmraError(NUMERIC) if any timed iteration produced a non-finite LL or estimate
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = float(sum(step_ms))
     if world > 1:

@@ -8,7 +8,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsrmra.so")
+# SRMRA_BUILD_OUT / SRMRA_BUILD_DEFS: an alternative build (A/B timing of kernel variants via SRMRA_LIB)
+LIB = os.environ.get("SRMRA_BUILD_OUT") or os.path.join(HERE, "libsrmra.so")
+EXTRA_DEFS = [d for d in os.environ.get("SRMRA_BUILD_DEFS", "").split() if d]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -39,14 +41,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     -ldl for the dlopen'ed NCCL).  Object files are compiled in parallel."""
     if not force and not needs_build():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if not EXTRA_DEFS else "build_" + os.path.basename(LIB).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [NVCC, *NVCC_FLAGS, *EXTRA_DEFS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     logs = []
     for src, p in procs:

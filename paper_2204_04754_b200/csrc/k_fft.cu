@@ -75,7 +75,7 @@ struct EmArgs {
     const float* par32;     // log2 units: lr1[L] | lr2[L] | beta[KK]
     const double* par64;    // E[KK] | (unused) | xm[KK]
     int64_t n;
-    int L, K, KK, ystride, groups;
+    int L, K, KK, ystride, ybuf, groups;  // ybuf: shared-memory stride of a staged Yhat (ystride + wrap row)
     float c2;               // log2(e) / sigma^2
     double inv_s2, inv_2s2;
     float2* part;           // [gridDim.x][PB] per-CTA partials, see part_bins()
@@ -96,6 +96,8 @@ struct Geo {
     // padded row stride of the transpose buffer (float2): even, so a row thread moves two elements per
     // 128-bit access; (LL + 2) * 8 B = 4 banks mod 32, so 8 lanes of a row access cover all 32 banks
     static constexpr int WS = LL + 2;
+    // Yhat row stride (float2), = yrow_of(LL)
+    static constexpr int YR = LH;
 };
 
 template <int LL>
@@ -163,7 +165,10 @@ __host__ __device__ inline bool tacc_fits(int KK, int ystride) {  // the staged 
 // Threads per CTA cap (register budget: one L_low-point complex line per thread lives in registers)
 template <int LL, bool TACC = false>
 __host__ __device__ constexpr int max_cta_threads() {
-    return LL >= 64 ? 256 : (LL >= 32 ? (TACC ? 384 : 320) : 512);
+#ifndef SRMRA_FFT32_TACC_THREADS
+#define SRMRA_FFT32_TACC_THREADS 384
+#endif
+    return LL >= 64 ? 256 : (LL >= 32 ? (TACC ? SRMRA_FFT32_TACC_THREADS : 320) : 512);
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -220,11 +225,22 @@ __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, f
     if (nwarps == 1) return;
     if (lane == 0) scratch[gwarp] = make_float4(s, m, z, 0.f);
     group_bar(bar_id, gthreads);
-    float S = scratch[0].x, Mx = scratch[0].y, Zs = scratch[0].z;
-    for (int w = 1; w < nwarps; ++w) smz_combine(S, Mx, Zs, scratch[w].x, scratch[w].y, scratch[w].z, c2);
-    s = S;
-    m = Mx;
-    z = Zs;
+    // lane j takes warp (j mod pw)'s summary (pw = nwarps rounded up to a power of two, missing warps empty);
+    // a log2(pw)-deep shuffle tree then leaves the group result in every block of pw lanes, i.e. in every
+    // lane — instead of a serial walk over the warps
+    int pw = 1;
+    while (pw < nwarps) pw <<= 1;
+    const int wj = lane & (pw - 1);
+    const float4 e = wj < nwarps ? scratch[wj] : make_float4(0.f, -INFINITY, 0.f, 0.f);
+    s = e.x;
+    m = e.y;
+    z = e.z;
+    for (int o = 1; o < pw; o <<= 1) {
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float z2 = __shfl_xor_sync(0xffffffffu, z, o);
+        smz_combine(s, m, z, s2, m2, z2, c2);
+    }
 }
 
 // PAIRS = true when K^2 is even (every complex transform carries two classes); for odd K^2 the
@@ -246,7 +262,7 @@ __host__ __device__ inline size_t xs_bytes(int KK, int xs_mode = 1) {
 template <int LL, bool PAIRS, int XS, bool TACC, bool JOINT>
 __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArgs a) {
     using G = Geo<LL>;
-    constexpr int LH = G::LH, WS = G::WS, M = LL - 1;
+    constexpr int LH = G::LH, WS = G::WS, M = LL - 1, YR = G::YR;
     if (*reinterpret_cast<const volatile int*>(a.run)) return;  // converged srmra_run: no-op iteration
     // launch duration stamps (the profiling window of srmra_profile reads them; no event nodes in the graph)
     int emt_slot = -1;
@@ -309,15 +325,15 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     if (TACC) tc::fence_before();
     __syncthreads();
     if (TACC) tc::fence_after();
-    const size_t per_g = TACC ? group_smem_t<LL>(KK, a.ystride) : group_smem<LL>(KK, a.ystride);
+    const size_t per_g = TACC ? group_smem_t<LL>(KK, a.ybuf) : group_smem<LL>(KK, a.ybuf);
     const int PB = part_bins(KK, LL);
     float* JA = reinterpret_cast<float*>(gbase + per_g * a.groups);  // JOINT accumulator (after the groups)
     if (JOINT) {
         for (int k = threadIdx.x; k < KK * LL * (LL + 1); k += blockDim.x) JA[k] = 0.f;
         __syncthreads();
     }
-    float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [2][ystride]
-    float2* Wk = Yb + 2 * a.ystride;                                    // [NP][LL][WS]
+    float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [2][ybuf]
+    float2* Wk = Yb + 2 * a.ybuf;                                       // [NP][LL][WS]
     // TACC: zc | yc | red after Wk, the partial staged over Yb (at the end); else Acc [PB] | red
     float2* Acc = TACC ? Yb : Wk + (size_t)NP * LL * WS;
     float2* zc = Wk + (size_t)NP * LL * WS;                             // [NP][2][LL] (TACC)
@@ -367,46 +383,57 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     // per-thread accumulators over this group's observations
     float rsumA = 0.f, rsumB = 0.f;     // row sums of w (class ra / rb, row idx)
     float2 cu = make_float2(0.f, 0.f);  // sum_i Z_{i,q}[0][idx]
-    double ll_acc = 0.0;
+    __shared__ double llg[16];          // per-group log-likelihood accumulators (tg == 0)
+    if (tg == 0) llg[g] = 0.0;
     // TACC roles in the M-column pass (column c = idx of pair q): c < LH accumulates U_q[., c], c >= LH
-    // accumulates V_q[., LL - c]; the V columns 0 and LL/2 (from c = 0, LL/2) go through zc / yc into
-    // vex0 / vexh, owned by thread (q, k1 = idx)
+    // accumulates V_q[., LL - c]; the V columns 0 and LL/2 (from c = 0, LL/2) go through zc [NP][2 LL + 2]
+    // (the second column at offset LL + 1: the two writer lanes of a warp hit different banks) into vex0 /
+    // vexh, owned by thread (q, k1 = idx); their Yhat factors are read from the previous observation's
+    // staged Yhat (vex_update runs before the prefetch overwrites that buffer)
     const bool role_u = idx < LH;
     const float su = role_u ? -1.f : 1.f;
     const bool vsrc = line_ok && (idx == 0 || idx == LL / 2);
     float2 vex0 = make_float2(0.f, 0.f), vexh = make_float2(0.f, 0.f);
-    auto vex_update = [&]() {
+    auto vex_update = [&](const float2* Yp) {
         if (line_ok) {
-            const float2* zq = zc + 2 * q * LL;
-            const float2* yq = yc + 2 * q * LL;
+            const float2* zq = zc + q * (2 * LL + 2);
             const int mk = (LL - idx) & M;
-            float2 yv = yq[idx], z = zq[mk];
+            float2 yv = Yp[idx * YR], z = zq[mk];
             vex0.x += yv.x * z.x - yv.y * z.y;
             vex0.y += yv.y * z.x + yv.x * z.y;
-            yv = yq[LL + idx];
-            z = zq[LL + mk];
+            yv = Yp[idx * YR + LL / 2];
+            z = zq[LL + 1 + mk];
             vexh.x += yv.x * z.x - yv.y * z.y;
             vexh.y += yv.y * z.x + yv.x * z.y;
         }
     };
     bool vex_pending = false;
 
-    const int64_t gstride = (int64_t)gridDim.x * a.groups;
-    int64_t i = (int64_t)blockIdx.x * a.groups + g;
+    const int n = (int)a.n;  // n_local is an int32 at the ABI
+    const int gstride = gridDim.x * a.groups;
+    int i = blockIdx.x * a.groups + g;
     int buf = 0;
-    auto prefetch = [&](int64_t obs, int b) {
-        if (obs < a.n) {
-            const float2* src = a.yhat + obs * a.ystride;
-            float2* dst = Yb + b * a.ystride;
-            for (int c = tg; c < a.ystride / 2; c += GT) cp_async16(dst + 2 * c, src + 2 * c);
+    // a staged Yhat carries a copy of its first row after its last (row LL): the mirrored E-column reads
+    // Yhat[(LL - k1) mod LL] then walk a constant stride
+    auto prefetch = [&](int obs, int b) {
+        if (obs < n) {
+            const float2* src = a.yhat + (int64_t)obs * a.ystride;
+            float2* dst = Yb + b * a.ybuf;
+            for (int c = tg; c < a.ybuf / 2; c += GT) {
+                const int cs = c < a.ystride / 2 ? c : c - a.ystride / 2;
+                cp_async16(dst + 2 * c, src + 2 * cs);
+            }
         }
         cp_async_commit();
     };
     prefetch(i, 0);
     cp_async_wait0();
     group_bar(bar_id, GT);
-    for (; i < a.n; i += gstride) {
-        const float2* Y = Yb + buf * a.ystride;
+    const bool flip0 = idx >= LH;  // pass 0: column k2 = idx beyond the stored half spectrum
+    const int ybase = flip0 ? LL * YR + (LL - idx) : idx;
+    const int ystep = flip0 ? -YR : YR;
+    for (; i < n; i += gstride) {
+        const float2* Y = Yb + buf * a.ybuf;
 
         float2 v[LL];
         float sref = 0.f, mall = 0.f, zall = 1.f;
@@ -430,7 +457,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const int k1 = c8 + e;
                             const int sk1 = flip ? ((LL - k1) & M) : k1;
                             const int o = sk1 * LH + sk2;
-                            const float2 yv = Y[o];
+                            const float2 yv = Y[ybase + k1 * ystep];
                             if constexpr (XS == 2) {
                                 const float4 cf = XP[k1 * LL + idx];  // (a, c, b, d), lane-contiguous: ideal wavefronts
                                 v[k1] = px::fma(px::bc(yv.x), make_float2(cf.x, cf.y), px::mul(px::bc(yv.y), make_float2(cf.z, cf.w)));
@@ -480,11 +507,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const float zy = su * z.y;
                             ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
                             ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
-                            if (vsrc) {  // (a separate loop after the chunks measured slower)
-                                const int col = idx == 0 ? 0 : LL;
-                                zc[2 * q * LL + col + k1] = z;
-                                yc[2 * q * LL + col + k1] = make_float2(ys[2 * e], ys[2 * e + 1]);
-                            }
+                            if (vsrc) zc[q * (2 * LL + 2) + (idx == 0 ? 0 : LL + 1) + k1] = z;
                         }
                         tc::tmem_st16(tacc + 16 * ch, ac);
                     }
@@ -497,7 +520,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     if (c < LH) {
 #pragma unroll
                         for (int k1 = 0; k1 < LL; ++k1) {
-                            const float2 yv = Y[k1 * LH + c];
+                            const float2 yv = Y[k1 * YR + c];
                             const float2 u = cmul_conj(yv, v[k1]);
                             Uq[k1 * LH + c] = make_float2(Uq[k1 * LH + c].x + u.x, Uq[k1 * LH + c].y + u.y);
                         }
@@ -506,7 +529,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                         const int k2 = (LL - c) & M;
 #pragma unroll
                         for (int k1 = 0; k1 < LL; ++k1) {
-                            const float2 yv = Y[k1 * LH + k2];
+                            const float2 yv = Y[k1 * YR + k2];
                             const float2 z = v[(LL - k1) & M];
                             const float2 w = make_float2(fmaf(yv.x, z.x, -yv.y * z.y), fmaf(yv.x, z.y, yv.y * z.x));
                             Vq[k1 * LH + k2] = make_float2(Vq[k1 * LH + k2].x + w.x, Vq[k1 * LH + k2].y + w.y);
@@ -567,6 +590,12 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 zall = za + zb;
                 group_reduce_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red2) + 8, gwarp, nwarps, lane,
                                  bar_id, GT);
+                if (TACC) {
+                    // the next observation's Yhat goes into the buffer vex_update read in pass 0: every thread of
+                    // the group has passed the reduction's barrier, so none still reads it
+                    if (nwarps == 1) __syncwarp();
+                    prefetch(i + gstride, buf ^ 1);
+                }
                 if (line_ok) {
                     // w = e 2^((sref_t - Sref) c2 + mt - M) / Z
                     const float f = mt == -INFINITY ? 0.f : ex2(fmaf(sref_t - sref, a.c2, mt - mall)) / zall;
@@ -587,17 +616,19 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
             }
             if (pass == 0) {
                 group_bar(bar_id, GT);
-                if (TACC && vex_pending) vex_update();  // zc / yc of the previous observation (its pass 3)
-                prefetch(i + gstride, buf ^ 1);
+                if (TACC && vex_pending) vex_update(Yb + (buf ^ 1) * a.ybuf);  // the previous observation's pass 3
+                if (!TACC) prefetch(i + gstride, buf ^ 1);
             } else if (pass == 2) {
                 cp_async_wait0();
                 group_bar(bar_id, GT);
             }
         }
         if (tg == 0) {
+            double em = __ldg(a.par64);
+            for (int r = 1; r < KK; ++r) em = fmin(em, __ldg(a.par64 + r));
             const double lse = 0.69314718055994530942 * ((double)mall + (double)log2f(zall)) +
-                               (double)sref * a.inv_s2 - (emin + a.ynorm[i]) * a.inv_2s2;
-            ll_acc += lse;
+                               (double)sref * a.inv_s2 - (em + a.ynorm[i]) * a.inv_2s2;
+            llg[g] += lse;
             if (a.llobs) a.llobs[i] = lse;
         }
         buf ^= 1;
@@ -606,7 +637,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     cp_async_wait0();
     group_bar(bar_id, GT);
     if (TACC) {
-        if (vex_pending) vex_update();
+        if (vex_pending) vex_update(Yb + (buf ^ 1) * a.ybuf);
         // stage the TMEM accumulator lines and the V columns 0 / LL/2 as this group's partial (over Yb / Wk;
         // every thread of the group is past its last use of them)
         group_bar(bar_id, GT);
@@ -639,14 +670,11 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
         if (has_b) R[rb * LL + idx] = make_float2(rsumB, 0.f);
         CU[q * LL + idx] = cu;
     }
-    if (tg == 0) red[31] = ll_acc;
     __syncthreads();
     // CTA partial (sum over groups in a fixed order) -> global slot of this CTA; the reduce kernel sums
     // the slots in a fixed order (deterministic, no atomics)
     float2* dst = a.part + (size_t)blockIdx.x * PB;
-    const size_t acc_off = TACC ? 0 : 2 * (size_t)a.ystride + (size_t)NP * LL * WS;  // float2 within a group
-    const size_t red_off = TACC ? acc_off + 2 * (size_t)a.ystride + (size_t)NP * LL * WS + 4 * (size_t)NP * LL - acc_off
-                                : acc_off + PB;
+    const size_t acc_off = TACC ? 0 : 2 * (size_t)a.ybuf + (size_t)NP * LL * WS;  // float2 within a group
     for (int k = threadIdx.x; k < PB; k += blockDim.x) {
         float2 s = make_float2(0.f, 0.f);
         for (int gg = 0; gg < a.groups; ++gg) {
@@ -665,10 +693,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     }
     if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int gg = 0; gg < a.groups; ++gg) {
-            const float2* G0 = reinterpret_cast<const float2*>(gbase + per_g * gg);
-            s += reinterpret_cast<const double*>(G0 + red_off)[31];
-        }
+        for (int gg = 0; gg < a.groups; ++gg) s += llg[gg];
         a.llpart[blockIdx.x] = s;
     }
     if (TACC) {
@@ -698,6 +723,8 @@ int ystride_of(int Ll) {
     const int n = Ll * yrow_of(Ll);
     return (n + 1) & ~1;  // even number of float2 -> 16-byte rows for cp.async / bulk copies
 }
+// shared-memory stride of one staged Yhat in k_fft_em: + a copy of row 0 (even number of float2)
+int ybuf_of(int Ll) { return ystride_of(Ll) + ((yrow_of(Ll) + 1) & ~1); }
 
 bool fft128_supported(int K);
 cudaError_t fft128_plan(srmra_ctx* c);
@@ -723,7 +750,7 @@ template <int LL, bool TACC, bool JOINT>
 static cudaError_t plan_em_tt(srmra_ctx* c) {
     const int KK = c->KK;
     const int GT = group_threads<LL>(KK);
-    const int ys = ystride_of(LL);
+    const int ys = ybuf_of(LL);
     constexpr int MAXT = max_cta_threads<LL, TACC>();
     if (GT > MAXT) return cudaErrorInvalidConfiguration;
     const size_t jb = JOINT ? joint_bytes<LL>(KK) : 0;
@@ -794,7 +821,7 @@ template <int LL, bool JOINT>
 static cudaError_t plan_em_tj(srmra_ctx* c) {
     // tensor-memory accumulators where the staged partial fits (L_low >= 32); SRMRA_FFT_TACC=0 disables
     const char* et = getenv("SRMRA_FFT_TACC");
-    const bool tacc_ok = LL >= 32 && tacc_fits<LL>(c->KK, ystride_of(LL)) && !(et && atoi(et) == 0);
+    const bool tacc_ok = LL >= 32 && tacc_fits<LL>(c->KK, ybuf_of(LL)) && !(et && atoi(et) == 0);
     if constexpr (LL >= 32) {
         if (tacc_ok && plan_em_tt<LL, true, JOINT>(c) == cudaSuccess) return cudaSuccess;
         cudaGetLastError();
@@ -819,6 +846,7 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     a.K = c->K;
     a.KK = c->KK;
     a.ystride = ystride_of(LL);
+    a.ybuf = ybuf_of(LL);
     a.groups = c->fft_groups;
     a.c2 = (float)(1.4426950408889634074 * c->inv_s2);
     a.inv_s2 = c->inv_s2;
@@ -898,7 +926,10 @@ cudaError_t launch_fft_em(srmra_ctx* c) {
 
 // prep, em, reduce, fold
 // E/M kernel (if the shard is non-empty) + tail (+ a separate reduce-only tail when world > 1)
-int fft_launches_per_iter(const srmra_ctx* c) { return (c->n_local > 0 ? 1 : 0) + 1 + (c->opt.world > 1 ? 1 : 0); }
+int fft_launches_per_iter(const srmra_ctx* c) {
+    const int em = c->n_local > 0 ? (c->Ll == 128 ? 2 : 1) : 0;  // L_low = 128: + the product-coefficient kernel
+    return em + 1 + (c->opt.world > 1 ? 1 : 0);
+}
 // (with world > 1 the NCCL all-reduce kernel between the two tails is NCCL's, not counted here)
 
 }  // namespace srmra

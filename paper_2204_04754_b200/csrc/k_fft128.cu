@@ -108,6 +108,7 @@ __device__ __forceinline__ void dit_x1(float2 (&v)[64], bool hb, float sh) {
     constexpr float c0 = (float)cos2pi(J, 128), s0 = (float)(SIGN * sin2pi(J, 128));
     constexpr float c1 = (float)cos2pi(J + 32, 128), s1 = (float)(SIGN * sin2pi(J + 32, 128));
     float2 a = v[J], b = v[J + 32];
+    // (scalar: the packed FP32x2 form of this stage measured slower at 255 registers, 31.7 vs 30.3 ms)
     if (hb) {
         a = make_float2(fmaf(a.x, c0, -a.y * s0), fmaf(a.x, s0, a.y * c0));
         b = make_float2(fmaf(b.x, c1, -b.y * s1), fmaf(b.x, s1, b.y * c1));
@@ -205,6 +206,7 @@ struct Em128Args {
     const double* ynorm;  // [n]
     const double* ysum;   // [n] sum_n y_i[n] (the DC bin Yhat_i[0][0], float64)
     const float4* xhat;   // [2 (hi | lo)][NP][128][65] pair-interleaved (Xhat_2q, Xhat_2q+1) / L_low^2
+    const float4* coef;   // COEF: [2 (hi | lo)][NP][128 k1][128 k2] E-step product coefficients (k_fft128_coef)
     const float* par32;   // log2 units: lr1[L] | lr2[L] | beta[KK]
     const double* par64;  // E[KK] | (unused) | xm[KK] (mean of x_r)
     int64_t n;
@@ -220,7 +222,32 @@ struct Em128Args {
     int emt_cap;
 };
 
-template <bool PAIRS>
+// E-step product coefficients (COEF variant): for column k2 of pair q and row k1 the conjugated packed product
+// v = conj(Yhat conj(Xhat_a) + i Yhat conj(Xhat_b)) of pass 0 is Y.x (a, c) + Y.y (b, d) (k_fft.cu, XS = 2; the
+// Hermitian mirror k2 >= 65 resolved here), with (a, c, b, d) formed in float64 from Xhat = hi + lo and stored
+// as float32 hi + lo: 4 packed FP32x2 instructions per element instead of two compensated complex products.
+__global__ void k_fft128_coef(const float4* __restrict__ xhat, int NP, float4* __restrict__ coef) {
+    const int total = NP * LL * LL;
+    const float4* xlo = xhat + (size_t)NP * LL * LH;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        const int q = k / (LL * LL), rem = k - q * LL * LL, k1 = rem / LL, k2 = rem - k1 * LL;
+        const bool fl = k2 >= LH;
+        const int o = q * LL * LH + (fl ? ((LL - k1) & (LL - 1)) : k1) * LH + (fl ? LL - k2 : k2);
+        const float4 h = xhat[o], l = xlo[o];
+        const double ax = (double)h.x + l.x, ay = (double)h.y + l.y, bx = (double)h.z + l.z, by = (double)h.w + l.w;
+        double c0, c1, c2, c3;  // (a, c, b, d)
+        if (fl) {
+            c0 = ax - by; c1 = -ay - bx; c2 = ay + bx; c3 = ax - by;
+        } else {
+            c0 = ax + by; c1 = ay - bx; c2 = ay - bx; c3 = -ax - by;
+        }
+        const float4 hi = make_float4((float)c0, (float)c1, (float)c2, (float)c3);
+        coef[k] = hi;
+        coef[(size_t)total + k] = make_float4((float)(c0 - hi.x), (float)(c1 - hi.y), (float)(c2 - hi.z), (float)(c3 - hi.w));
+    }
+}
+
+template <bool PAIRS, bool COEF>
 __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     extern __shared__ __align__(1024) unsigned char sm[];
     float2* W = reinterpret_cast<float2*>(sm + OFF_W);
@@ -292,6 +319,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const float sg = flip ? -1.f : 1.f;
     const float4* XP = a.xhat + (size_t)q * LL * LH;
     const float4* XPL = XP + (size_t)NP * LL * LH;  // lo plane
+    const float4* CH = a.coef + (size_t)q * LL * LL + l;            // COEF: hi coefficients of column l
+    const float4* CL = CH + (size_t)NP * LL * LL;                   // lo
     const float* lr1 = pars;
     const float* lr2 = pars + L;
     const float* beta = pars + 2 * L;
@@ -343,14 +372,22 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                         const int k1 = 2 * m + h;
                         const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
                         const float2 yv = Ys[sk1 * YR + sk2];
-                        const float4 xv = __ldg(XP + sk1 * LH + sk2);
-                        const float4 xl = __ldg(XPL + sk1 * LH + sk2);
                         // Yhat conj(Xhat_hi + Xhat_lo): the float32 rounding of Xhat is shared by every
                         // observation and would bias the class logits systematically; the lo part removes it
-                        const float2 A = cmul_conj_acc(yv, make_float2(xv.x, xv.y), make_float2(xl.x, xl.y));
-                        const float2 B = has_b ? cmul_conj_acc(yv, make_float2(xv.z, xv.w), make_float2(xl.z, xl.w))
-                                               : make_float2(0.f, 0.f);
-                        v[m] = make_float2(A.x - sg * B.y, -(sg * A.y + B.x));
+                        if constexpr (COEF) {
+                            const float4 ch = __ldg(CH + k1 * LL), cl = __ldg(CL + k1 * LL);
+                            const float2 lo = px::fma(px::bc(yv.x), make_float2(cl.x, cl.y),
+                                                      px::mul(px::bc(yv.y), make_float2(cl.z, cl.w)));
+                            v[m] = px::fma(px::bc(yv.x), make_float2(ch.x, ch.y),
+                                           px::fma(px::bc(yv.y), make_float2(ch.z, ch.w), lo));
+                        } else {
+                            const float4 xv = __ldg(XP + sk1 * LH + sk2);
+                            const float4 xl = __ldg(XPL + sk1 * LH + sk2);
+                            const float2 A = cmul_conj_acc(yv, make_float2(xv.x, xv.y), make_float2(xl.x, xl.y));
+                            const float2 B = has_b ? cmul_conj_acc(yv, make_float2(xv.z, xv.w), make_float2(xl.z, xl.w))
+                                                   : make_float2(0.f, 0.f);
+                            v[m] = make_float2(A.x - sg * B.y, -(sg * A.y + B.x));
+                        }
                         // the DC bin (constant over the shifts) is added back in float64 after the transform
                         if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
                         ys[2 * e] = yv.x;
@@ -563,8 +600,21 @@ static cudaLaunchConfig_t em128_config(const srmra_ctx* c, cudaLaunchAttribute* 
 
 bool fft128_supported(int K) { return K >= 1 && 2 * MAXNP >= K * K; }
 
+static bool coef_mode() {  // SRMRA_FFT128_COEF=0: the compensated complex products (A/B)
+    static const bool on = [] {
+        const char* e = getenv("SRMRA_FFT128_COEF");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+static auto em128_kernel(int KK) {
+    if (coef_mode()) return KK % 2 == 0 ? k_fft_em128<true, true> : k_fft_em128<false, true>;
+    return KK % 2 == 0 ? k_fft_em128<true, false> : k_fft_em128<false, false>;
+}
+size_t fft128_coef_float4(int KK) { return (size_t)2 * ((KK + 1) / 2) * LL * LL; }
+
 cudaError_t fft128_plan(srmra_ctx* c) {
-    auto kern = (c->KK % 2 == 0) ? k_fft_em128<true> : k_fft_em128<false>;
+    auto kern = em128_kernel(c->KK);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // = the tail's
@@ -593,6 +643,7 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.ynorm = c->d_ynorm;
     a.ysum = c->d_ysum;
     a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
+    a.coef = c->d_xcoef;
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
     a.n = c->n_local;
@@ -600,6 +651,11 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.K = c->K;
     a.KK = c->KK;
     a.NP = (c->KK + 1) / 2;
+    if (coef_mode()) {
+        k_fft128_coef<<<2 * c->num_sms, 256, 0, c->stream>>>(a.xhat, a.NP, c->d_xcoef);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     a.PB = fft_partial_bins(c->KK, LL);
     a.c2 = (float)(1.4426950408889634074 * c->inv_s2);
     a.c2d = 1.4426950408889634074 * c->inv_s2;
@@ -613,8 +669,7 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.emt_cap = c->opt.trace_cap;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = em128_config(c, attr, c->fft_grid);
-    if (c->KK % 2 == 0) return cudaLaunchKernelEx(&cfg, k_fft_em128<true>, a);
-    return cudaLaunchKernelEx(&cfg, k_fft_em128<false>, a);
+    return cudaLaunchKernelEx(&cfg, em128_kernel(c->KK), a);
 }
 
 }  // namespace srmra

@@ -652,6 +652,7 @@ int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32_t L_high,
         CKI(dalloc(&c->d_xhat, fft_xhat_float2(c->KK, c->Ll)));
         CKI(cudaMemset(c->d_xhat, 0, sizeof(float2) * fft_xhat_float2(c->KK, c->Ll)));
         CKI(dalloc(&c->d_bhat, fft_bhat_doubles(c->KK, c->Ll)));
+        if (c->Ll == 128) CKI(dalloc(&c->d_xcoef, fft128_coef_float4(c->KK)));
         CKI(fft_plan(c));
         std::vector<double> tw(2 * (size_t)c->Ll);  // cos / sin (2 pi j / L_low), float64
         for (int j = 0; j < c->Ll; ++j) {
@@ -1131,7 +1132,7 @@ void srmra_free(srmra_ctx* c) {
         if (api.loaded) api.CommDestroy((ncclComm_t)c->nccl_comm);
     }
     void* bufs[] = {c->d_y, c->d_yhat, c->d_ysum, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
-                    c->par.f32, c->par.f64, c->d_xhat, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
+                    c->par.f32, c->par.f64, c->d_xhat, c->d_xcoef, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
                     c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps};
     for (void* p : bufs)
         if (p) cudaFree(p);

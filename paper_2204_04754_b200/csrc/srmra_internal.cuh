@@ -69,6 +69,7 @@ struct srmra_ctx {
     // per-iteration
     srmra::IterParams par{};
     float2* d_xhat = nullptr;   // [KK][Ll][Lh] rfft2 of x_r (fft path)
+    float4* d_xcoef = nullptr;  // L_low = 128: E-step product coefficients [2][NP][128][128] (k_fft128.cu)
     double* d_colsum = nullptr; // [L2] sum_i w^{i,s}
     double* d_bhat = nullptr;   // fft path, float64: Bhat [KK][Ll][Lh] complex | mass lines [KK][Ll+Lh] complex
     float2* d_part = nullptr;   // fft path: per-CTA float32 partials of the above [fft_grid][...]
@@ -186,6 +187,7 @@ cudaError_t fft_plan_joint(srmra_ctx* c, bool joint);  // re-plan with / without
 size_t fft_joint_bins(int KK, int Ll);
 size_t fft_part_float2(const srmra_ctx* c);
 size_t fft_xhat_float2(int KK, int Ll);   // pair-interleaved Xhat
+size_t fft128_coef_float4(int KK);        // L_low = 128 product coefficients
 
 // cudaFuncSetAttribute is per device: run a setup functor once per device ordinal (retried after a failure)
 struct PerDeviceOnce {
