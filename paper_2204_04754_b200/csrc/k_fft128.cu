@@ -71,6 +71,10 @@ __device__ __forceinline__ float2 cmul_conj_acc(float2 a, float2 bh, float2 bl) 
     const float lx = fmaf(a.x, bl.x, a.y * bl.y), ly = fmaf(a.y, bl.x, -a.x * bl.y);
     return make_float2(fmaf(a.x, bh.x, fmaf(a.y, bh.y, lx)), fmaf(a.y, bh.x, fmaf(-a.x, bh.y, ly)));
 }
+// the float64 log2 maximum g_q a cluster peer stored in the (lo, hi, z, -) slot of its exchange float4
+__device__ __forceinline__ double xch_g(float4 e) {
+    return __longlong_as_double((long long)(((unsigned long long)__float_as_uint(e.y) << 32) | __float_as_uint(e.x)));
+}
 __device__ __forceinline__ float2 shfl_pair(float2 v) {
     return make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1), __shfl_xor_sync(0xffffffffu, v.y, 1));
 }
@@ -473,17 +477,15 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                                       make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)),
                                                   zall, 0.f));
                     cluster_sync_all();
-                    double g[MAXNP];
+                    // two passes over the exchange slots (no local array: it would live in local memory)
                     G = -INFINITY;
+                    for (int r = 0; r < NP; ++r) G = fmax(G, xch_g(xch[slot + r]));
+                    Z = 0.0;
                     for (int r = 0; r < NP; ++r) {
                         const float4 e = xch[slot + r];
-                        g[r] = __longlong_as_double(
-                            (long long)(((unsigned long long)__float_as_uint(e.y) << 32) | __float_as_uint(e.x)));
-                        G = fmax(G, g[r]);
+                        const double gr = xch_g(e);
+                        if (gr != -INFINITY) Z += (double)e.z * (double)ex2((float)(gr - G));
                     }
-                    Z = 0.0;
-                    for (int r = 0; r < NP; ++r)
-                        if (g[r] != -INFINITY) Z += (double)xch[slot + r].z * (double)ex2((float)(g[r] - G));
                 } else {
                     G = gq;
                     Z = (double)zall;
@@ -577,6 +579,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         atomicMax(a.emt + 2 * emt_slot + 1, t1);
     }
 }
+
 
 }  // namespace fft128
 
