@@ -205,16 +205,18 @@ __device__ __forceinline__ void group_reduce_ms(float& m, float& z, float2* scra
 // sum z = sum 2^(v - m); two sets combine through the difference of their maxima, (s - s') c2 + (m - m'),
 // so every thread may use its own score reference s (no separate max reduction)
 __device__ __forceinline__ void smz_combine(float& s, float& m, float& z, float s2, float m2, float z2, float c2) {
-    if (m2 == -INFINITY) return;  // the other set is empty
-    const float d = fmaf(s - s2, c2, m - m2);  // -inf when this set is empty
-    const bool keep = d >= 0.f;
-    const float e = ex2(-fabsf(d));
+    // branchless (a data-dependent return costs BSSY / BSYNC / BRA per level): the other set empty
+    // (m2 = -inf) gives e = 0 and d = +inf or NaN, so this set is kept unchanged; this set empty (m = -inf)
+    // gives d = -inf, e = 0 and the other set is taken
+    const float d = fmaf(s - s2, c2, m - m2);
+    const bool keep = !(d < 0.f);
+    const float e = m2 == -INFINITY ? 0.f : ex2(-fabsf(d));
     z = keep ? fmaf(z2, e, z) : fmaf(z, e, z2);
     s = keep ? s : s2;
     m = keep ? m : m2;
 }
 __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, float c2, float4* scratch, int gwarp,
-                                                 int nwarps, int lane, int bar_id, int gthreads) {
+                                                 int nwarps, int pw, int lane, int bar_id, int gthreads) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
@@ -228,8 +230,6 @@ __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, f
     // lane j takes warp (j mod pw)'s summary (pw = nwarps rounded up to a power of two, missing warps empty);
     // a log2(pw)-deep shuffle tree then leaves the group result in every block of pw lanes, i.e. in every
     // lane — instead of a serial walk over the warps
-    int pw = 1;
-    while (pw < nwarps) pw <<= 1;
     const int wj = lane & (pw - 1);
     const float4 e = wj < nwarps ? scratch[wj] : make_float4(0.f, -INFINITY, 0.f, 0.f);
     s = e.x;
@@ -282,6 +282,8 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     const int tg = threadIdx.x - g * GT;   // thread in group
     const int lane = threadIdx.x & 31;
     const int gwarp = tg >> 5, nwarps = GT >> 5;
+    int pw = 1;  // nwarps rounded up to a power of two (the cross-warp shuffle tree of the softmax reduction)
+    while (pw < nwarps) pw <<= 1;
     const int bar_id = 1 + g;
 
     // ---- shared layout: par table | [Xhat (XS)] | group 0 | group 1 | ...
@@ -384,7 +386,11 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
     float rsumA = 0.f, rsumB = 0.f;     // row sums of w (class ra / rb, row idx)
     float2 cu = make_float2(0.f, 0.f);  // sum_i Z_{i,q}[0][idx]
     __shared__ double llg[16];          // per-group log-likelihood accumulators (tg == 0)
-    if (tg == 0) llg[g] = 0.0;
+    __shared__ double emin_g[16];       // E_min of this iteration (the LL constant), written and read by tg == 0
+    if (tg == 0) {
+        llg[g] = 0.0;
+        emin_g[g] = emin;
+    }
     // TACC roles in the M-column pass (column c = idx of pair q): c < LH accumulates U_q[., c], c >= LH
     // accumulates V_q[., LL - c]; the V columns 0 and LL/2 (from c = 0, LL/2) go through zc [NP][2 LL + 2]
     // (the second column at offset LL + 1: the two writer lanes of a warp hit different banks) into vex0 /
@@ -588,7 +594,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 sref = sref_t;
                 mall = mt;
                 zall = za + zb;
-                group_reduce_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red2) + 8, gwarp, nwarps, lane,
+                group_reduce_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red2) + 8, gwarp, nwarps, pw, lane,
                                  bar_id, GT);
                 if (TACC) {
                     // the next observation's Yhat goes into the buffer vex_update read in pass 0: every thread of
@@ -624,10 +630,8 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
             }
         }
         if (tg == 0) {
-            double em = __ldg(a.par64);
-            for (int r = 1; r < KK; ++r) em = fmin(em, __ldg(a.par64 + r));
             const double lse = 0.69314718055994530942 * ((double)mall + (double)log2f(zall)) +
-                               (double)sref * a.inv_s2 - (em + a.ynorm[i]) * a.inv_2s2;
+                               (double)sref * a.inv_s2 - (emin_g[g] + a.ynorm[i]) * a.inv_2s2;
             llg[g] += lse;
             if (a.llobs) a.llobs[i] = lse;
         }

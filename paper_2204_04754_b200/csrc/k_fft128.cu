@@ -85,6 +85,12 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -166,10 +172,12 @@ __device__ __forceinline__ void ms_combine(float& m, float& z, float m2, float z
 // (s, m, z): log2 maximum s c2 + m and scaled sum z of a set of unnormalised weights; sets with different
 // score references s combine through (s - s') c2 + (m - m') (see k_fft.cu)
 __device__ __forceinline__ void smz_combine(float& s, float& m, float& z, float s2, float m2, float z2, float c2) {
-    if (m2 == -INFINITY) return;
+    // branchless (a data-dependent return costs BSSY / BSYNC / BRA per level): the other set empty
+    // (m2 = -inf) gives e = 0 and d = +inf or NaN, so this set is kept unchanged; this set empty (m = -inf)
+    // gives d = -inf, e = 0 and the other set is taken
     const float d = fmaf(s - s2, c2, m - m2);
-    const bool keep = d >= 0.f;
-    const float e = ex2(-fabsf(d));
+    const bool keep = !(d < 0.f);
+    const float e = m2 == -INFINITY ? 0.f : ex2(-fabsf(d));
     z = keep ? fmaf(z2, e, z) : fmaf(z, e, z2);
     s = keep ? s : s2;
     m = keep ? m : m2;
@@ -362,7 +370,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         phase ^= 1;
         float2 v[64];
         float za = 0.f, zb = 0.f, mt = -INFINITY, mall = 0.f, zall = 1.f;
-        double G = 0.0, Z = 1.0;
+        double gq = 0.0;         // this pair's log2 maximum (pass 1 -> pass 3)
+        float zq = 1.f, rpa = 0.f, rpb = 0.f;
 #pragma unroll 1
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == 0) {
@@ -468,15 +477,35 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 const double sref_d = Da + (double)sref;  // the pair's score reference, float64
                 // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64)
                 // g_q = log2 of this pair's largest unnormalised weight: Sref c2 + m_q
-                const double gq = mall == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)mall;
-                if (NP > 1) {
+                gq = mall == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)mall;
+                zq = zall;
+                if (NP > 1) {  // publish (g_q, z_q); the wait is deferred to pass 3 (pass 2 overlaps the exchange)
                     const int slot = (it & 1) * MAXNP;
                     const unsigned long long gb = (unsigned long long)__double_as_longlong(gq);
                     if (t < NP)
                         st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t,
                                       make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)),
                                                   zall, 0.f));
-                    cluster_sync_all();
+                    cluster_arrive();
+                }
+                // weights relative to this pair's reference; the cluster factor 2^(g_q - G) / Z scales them after
+                // the (linear) forward transforms, in pass 3
+                const float floc = mt == -INFINITY ? 0.f : ex2(fmaf(sref_t - sref, a.c2, mt - mall));
+                rpa = za * floc;
+                rpb = zb * floc;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) v[j] = make_float2(v[j].x * floc, v[j].y * floc);
+            } else if (pass == 2) {
+                // each thread rewrites the row elements it read in pass 1
+#pragma unroll
+                for (int k = 0; k < 64; ++k) W[swz(l, 2 * k + h)] = v[k];
+                __syncthreads();
+            } else {
+                // cluster factor of this pair: 2^(g_q - G) / Z (log-sum-exp over all classes, float64)
+                double G = gq, Z = (double)zq;
+                if (NP > 1) {
+                    cluster_wait();
+                    const int slot = (it & 1) * MAXNP;
                     // two passes over the exchange slots (no local array: it would live in local memory)
                     G = -INFINITY;
                     for (int r = 0; r < NP; ++r) G = fmax(G, xch_g(xch[slot + r]));
@@ -486,29 +515,18 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                         const double gr = xch_g(e);
                         if (gr != -INFINITY) Z += (double)e.z * (double)ex2((float)(gr - G));
                     }
-                } else {
-                    G = gq;
-                    Z = (double)zall;
                 }
-                const float dq = gq == -INFINITY ? -INFINITY : (float)(gq - G);
-                const float f = (mt == -INFINITY || dq == -INFINITY) ? 0.f
-                                                                      : ex2(fmaf(sref_t - sref, a.c2, mt - mall) + dq) / (float)Z;
-                rsumA = fmaf(za, f, rsumA);
-                rsumB = fmaf(zb, f, rsumB);
-#pragma unroll
-                for (int j = 0; j < 64; ++j) v[j] = make_float2(v[j].x * f, v[j].y * f);
+                const float fcl = gq == -INFINITY ? 0.f : ex2((float)(gq - G)) / (float)Z;
+                rsumA = fmaf(rpa, fcl, rsumA);
+                rsumB = fmaf(rpb, fcl, rsumB);
                 if (q == 0 && t == 0) {
                     const double lse = 0.69314718055994530942 * (G + (double)log2f((float)Z)) -
                                        (emin + a.ynorm[i]) * a.inv_2s2;
                     ll_acc += lse;
                     if (a.llobs) a.llobs[i] = lse;
                 }
-            } else if (pass == 2) {
-                // each thread rewrites the row elements it read in pass 1
 #pragma unroll
-                for (int k = 0; k < 64; ++k) W[swz(l, 2 * k + h)] = v[k];
-                __syncthreads();
-            } else {
+                for (int m = 0; m < 64; ++m) v[m] = px::mul(v[m], px::bc(fcl));
                 // v[m] = Z_{i,q}[k1 = 2m + h][l]
                 if (h == 0) {
                     cu.x += v[0].x;
