@@ -372,7 +372,11 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         float za = 0.f, zb = 0.f, mt = -INFINITY, mall = 0.f, zall = 1.f;
         double gq = 0.0;         // this pair's log2 maximum (pass 1 -> pass 3)
         float zq = 1.f, rpa = 0.f, rpb = 0.f;
+#ifdef SRMRA_FFT128_PASS_UNROLL  // (A/B build: the four passes as separate code bodies)
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == 0) {
                 // E-step along k1 for column k2 = l: conj of Z = Yhat conj(Xa) + i Yhat conj(Xb)
