@@ -96,7 +96,9 @@ struct Geo {
     // padded row stride of the transpose buffer (float2): even, so a row thread moves two elements per
     // 128-bit access; (LL + 2) * 8 B = 4 banks mod 32, so 8 lanes of a row access cover all 32 banks
     static constexpr int WS = LL + 2;
-    // Yhat row stride (float2), = yrow_of(LL)
+    // Yhat row stride (float2), = yrow_of(LL).  (Rows padded to 24 at LL = 32 — each 8-byte bank pair hit
+    // exactly twice by a warp's E-column read — and the full mirrored LL x LL spectrum both measured no faster
+    // at c3 and slower at c1 / c2: the extra staging bytes cost more than the bank conflicts.)
     static constexpr int YR = LH;
 };
 

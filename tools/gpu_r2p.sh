@@ -1,0 +1,13 @@
+mkdir -p gpurun_out
+T=r2p
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > gpurun_out/pytest_full_$T.log 2>&1
+tail -3 gpurun_out/pytest_full_$T.log
+for cfg in c3 c1 c2; do
+  timeout 600 python bench.py --config $cfg --steps 30 --warmup 5 --no-cpu-baseline --e2e-jobs 0 > gpurun_out/bench_${cfg}_$T.log 2>&1
+done
+for f in gpurun_out/bench_c*_$T.log; do echo $f; python -c "
+import json
+for line in open('$f'):
+    if line.startswith('{'):
+        d=json.loads(line); r=d['roofline']; print(d['config']['workload'], d['value'], d['ms_per_step'], r['kernel_ms_avg'], r['frac'], d['config'].get('path'))
+" || tail -3 $f; done
