@@ -42,8 +42,9 @@ constexpr int LL = 128, LH = 65, YR = 72, NT = 256, MAXNP = 8;
 constexpr uint32_t YBYTES = LL * YR * 8;  // one observation's staged spectrum, 73,728 B
 
 // dynamic shared memory layout (bytes)
-constexpr int OFF_W = 0;                      // float2 [128][128] swizzled transpose buffer
-constexpr int OFF_Y = OFF_W + LL * LL * 8;    // float2 [128][72]  Yhat_i
+constexpr int WSP = 130;                      // transpose-buffer row stride (float2), = 2 (mod 16)
+constexpr int OFF_W = 0;                      // float2 transpose buffer, 128 rows of WSP (+ gaps, wofs)
+constexpr int OFF_Y = OFF_W + (LL * WSP + 16) * 8;  // float2 [128][72]  Yhat_i
 constexpr int OFF_PAR = OFF_Y + (int)YBYTES;  // float [2L + KK] logit bias (log2 units), L <= 512
 constexpr int OFF_ZC = OFF_PAR + 4224;        // float2 [2][128]  Z columns 0 and 64 (V extra)
 constexpr int OFF_YC = OFF_ZC + 2048;         // float2 [2][128]  Yhat columns 0 and 64
@@ -56,7 +57,12 @@ constexpr int SMEM = OFF_TSLOT + 8;
 
 // element (r, c) of the transpose buffer: rows 32 apart and the two parities of a column land in
 // different 8-byte bank groups for both row-wise and column-wise thread-pair access
-__device__ __forceinline__ int swz(int r, int c) { return r * LL + (c ^ (((r << 1) & 14) ^ (((r >> 5) & 1) << 3))); }
+// Element (r, c) lives at r WSP + c + 8 (bit 5 of r) + 8 (bit 6 of r): every thread's four access patterns are
+// a thread-constant base plus compile-time offsets (no per-element address arithmetic, unlike an XOR swizzle),
+// rows never overlap (the bit-6 gap after row 63), and the accesses are conflict-free — row passes (row l,
+// columns 2m + h): bank pair 2 l + h + const over 8 rows x 2 halves; column passes (rows 32 h + j (+ 64),
+// column l): l + 8 h + const
+__device__ __forceinline__ int wofs(int r, int c) { return r * WSP + c + (((r >> 5) & 1) << 3) + ((r >> 6) << 3); }
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -287,7 +293,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const int t = threadIdx.x, h = t & 1, l = t >> 1, lane = t & 31, warp = t >> 5;
     const int NP = a.NP, K = a.K, L = a.L, KK = a.KK;
     const int q = NP > 1 ? (int)cluster_rank() : 0;
-    const int64_t cl = blockIdx.x / NP, ncl = gridDim.x / NP;
+    const int cl = blockIdx.x / NP, ncl = gridDim.x / NP;
+    const int n = (int)a.n;  // n_local is an int32 at the ABI
     const int ra = 2 * q, rb = 2 * q + 1;
     const bool has_b = PAIRS || rb < KK;
 
@@ -296,6 +303,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     double emin = __ldg(a.par64);
     for (int r = 1; r < KK; ++r) emin = fmin(emin, __ldg(a.par64 + r));
     for (int r = t; r < KK; r += NT) pars[2 * L + r] = (float)((emin - __ldg(a.par64 + r)) * a.inv_2s2 * 1.4426950408889634074);
+    __shared__ double emin_cta;
+    if (t == 0) emin_cta = emin;
     if (t == 0) {
         tc::mbar_init(mbar, 1);
         tc::fence_mbar_init();
@@ -316,13 +325,15 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         for (int ch = 0; ch < 8; ++ch) tc::tmem_st16(tacc + 16 * ch, z);
         tc::tmem_wait_st();
     }
-    int64_t i = cl;
-    if (t == 0 && i < a.n) {
+    int i = cl;
+    if (t == 0 && i < n) {
         mbar_expect_tx(mbar, YBYTES);
-        bulk_g2s(tc::smem_u32(Ys), a.yhat + i * (int64_t)(LL * YR), YBYTES, mbar);
+        bulk_g2s(tc::smem_u32(Ys), a.yhat + (int64_t)i * (LL * YR), YBYTES, mbar);
     }
 
     // this thread's line: column l (passes 0, 3) / row l (passes 1, 2), half / parity h
+    const int wrow = wofs(l, h);            // row passes: element (l, 2m + h) at wrow + 2m
+    const int wcol = wofs(32 * h, l);       // column passes: (32 h + j, l) at wcol + j WSP, (64 + 32 h + j, l) + 64 WSP + 8
     const bool flip = l >= LH;             // column beyond the stored half spectrum (Hermitian mirror)
     const bool role_u = l < LH;            // accumulates U_q[., l]; otherwise V_q[., 128 - l]
     const bool both = (l == 0 || l == LL / 2);  // columns that also need V (added via zc / yc)
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const int ra2 = ra % K, rb2 = rb % K;
     const float biasA = lr1[ra / K + K * l] + beta[ra];
     const float biasB = has_b ? lr1[rb / K + K * l] + beta[rb] : 0.f;
-    const double xmA = a.par64[KK + 1 + ra], xmB = has_b ? a.par64[KK + 1 + rb] : 0.0;  // means of x_ra, x_rb
+    // (the class means xm[ra], xm[rb] and E_min are re-read when needed: fewer live registers)
 
     // lr2 of (class ra, class rb) at the n2 of (half h, element j): n2 = 32h + j + 32 (j >= 32); rows
     // padded to 65 so the two halves of a warp read different banks
@@ -352,7 +363,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     float rsumA = 0.f, rsumB = 0.f;        // row sums of the posterior (row l, this half), classes ra / rb
     float2 cu = make_float2(0.f, 0.f);     // sum_i Z_{i,q}[0][l]
     float2 vex = make_float2(0.f, 0.f);    // V_q[t & 127][64 (t >> 7)] (columns 0 / 64)
-    double ll_acc = 0.0;
+    __shared__ double ll_acc;  // t == 0 of the q == 0 CTA accumulates the observations' log-likelihood terms
+    if (t == 0) ll_acc = 0.0;
     uint32_t phase = 0;
     int it = 0;
     auto vex_update = [&]() {
@@ -365,17 +377,19 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     // One forward 64-point FFT body serves all four passes (the kernel is otherwise instruction-fetch
     // bound): the two inverse passes use ifft(z) = conj(fft(conj z)) — the conjugation is folded into
     // the E-column input (conj Z) and the score read-out (S = conj of the E-row output).
-    for (; i < a.n; i += ncl, ++it) {
+    for (; i < n; i += ncl, ++it) {
         tc::mbar_wait(mbar, phase);
         phase ^= 1;
         float2 v[64];
         float za = 0.f, zb = 0.f, mt = -INFINITY, mall = 0.f, zall = 1.f;
         double gq = 0.0;         // this pair's log2 maximum (pass 1 -> pass 3)
         float zq = 1.f, rpa = 0.f, rpb = 0.f;
-#ifdef SRMRA_FFT128_PASS_UNROLL  // (A/B build: the four passes as separate code bodies)
-#pragma unroll
-#else
+        // the four passes as four code bodies (with the linear transpose layout: c4 28.1 -> 23.5 ms; with the XOR
+        // swizzle the unrolled variant was slower); SRMRA_FFT128_PASS_ROLLED builds one shared body for A/B
+#ifdef SRMRA_FFT128_PASS_ROLLED
 #pragma unroll 1
+#else
+#pragma unroll
 #endif
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == 0) {
@@ -414,12 +428,12 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 }
             } else if (pass == 1) {
 #pragma unroll
-                for (int m = 0; m < 64; ++m) v[m] = W[swz(l, 2 * m + h)];
+                for (int m = 0; m < 64; ++m) v[m] = W[wrow + 2 * m];
             } else if (pass == 3) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    v[j] = W[swz(32 * h + j, l)];
-                    v[32 + j] = W[swz(64 + 32 * h + j, l)];
+                    v[j] = W[wcol + j * WSP];
+                    v[32 + j] = W[wcol + (64 + j) * WSP + 8];
                 }
             }
             // pass 2: v holds the posterior row of the pair (forward transform along n2)
@@ -430,23 +444,23 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
             if (pass == 0) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    W[swz(32 * h + j, l)] = v[j];
-                    W[swz(64 + 32 * h + j, l)] = v[32 + j];
+                    W[wcol + j * WSP] = v[j];
+                    W[wcol + (64 + j) * WSP + 8] = v[32 + j];
                 }
                 __syncthreads();
                 // Yhat_i has been consumed: stream the next observation's spectrum in behind passes 1-3
-                if (t == 0 && i + ncl < a.n) {
+                if (t == 0 && i + ncl < n) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(mbar, YBYTES);
-                    bulk_g2s(tc::smem_u32(Ys), a.yhat + (i + ncl) * (int64_t)(LL * YR), YBYTES, mbar);
+                    bulk_g2s(tc::smem_u32(Ys), a.yhat + (int64_t)(i + ncl) * (LL * YR), YBYTES, mbar);
                 }
                 if (it > 0) vex_update();  // columns 0 / 64 of the previous observation (zc, yc of its pass 3)
             } else if (pass == 1) {
                 // S_a + i S_b = conj(v) at n2 = 32h + j (v[j]) and 64 + 32h + j (v[32 + j]), without the DC
                 // terms D_c = ysum_i mean(x_c) (float64): S_c = . + D_c; scores are kept relative to D_a
                 const double ysi = a.ysum[i];
-                const double Da = ysi * xmA;
-                const float dba = has_b ? (float)(ysi * xmB - Da) : 0.f;
+                const double Da = ysi * __ldg(a.par64 + KK + 1 + ra);  // mean of x_ra
+                const float dba = has_b ? (float)(ysi * __ldg(a.par64 + KK + 1 + rb) - Da) : 0.f;
                 float lmax = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
@@ -502,7 +516,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
             } else if (pass == 2) {
                 // each thread rewrites the row elements it read in pass 1
 #pragma unroll
-                for (int k = 0; k < 64; ++k) W[swz(l, 2 * k + h)] = v[k];
+                for (int k = 0; k < 64; ++k) W[wrow + 2 * k] = v[k];
                 __syncthreads();
             } else {
                 // cluster factor of this pair: 2^(g_q - G) / Z (log-sum-exp over all classes, float64)
@@ -525,7 +539,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 rsumB = fmaf(rpb, fcl, rsumB);
                 if (q == 0 && t == 0) {
                     const double lse = 0.69314718055994530942 * (G + (double)log2f((float)Z)) -
-                                       (emin + a.ynorm[i]) * a.inv_2s2;
+                                       (emin_cta + a.ynorm[i]) * a.inv_2s2;
                     ll_acc += lse;
                     if (a.llobs) a.llobs[i] = lse;
                 }
