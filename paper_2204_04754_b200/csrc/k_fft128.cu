@@ -94,6 +94,9 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_arrive() {
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -124,7 +127,7 @@ __device__ __forceinline__ void dit_x1(float2 (&v)[64], bool hb, float sh) {
     constexpr float c0 = (float)cos2pi(J, 128), s0 = (float)(SIGN * sin2pi(J, 128));
     constexpr float c1 = (float)cos2pi(J + 32, 128), s1 = (float)(SIGN * sin2pi(J + 32, 128));
     float2 a = v[J], b = v[J + 32];
-    // (scalar: the packed FP32x2 form of this stage measured slower at 255 registers, 31.7 vs 30.3 ms)
+    // (scalar: the packed FP32x2 form of this stage measured slower twice: 31.7 vs 30.3 ms, 24.1 vs 23.4 ms)
     if (hb) {
         a = make_float2(fmaf(a.x, c0, -a.y * s0), fmaf(a.x, s0, a.y * c0));
         b = make_float2(fmaf(b.x, c1, -b.y * s1), fmaf(b.x, s1, b.y * c1));
@@ -469,25 +472,25 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 }
                 const float sref_t = lmax;  // this thread's score reference (relative to D_a)
                 // posterior (eq:weights_EM) in log2 units: v2 = (S - sref_t) log2e / sigma^2 + bias
+                const float2 biasAB = make_float2(biasA, biasB);
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
-                    const float2 b2 = lrp[h * 65 + j];  // lr2 of (class ra, class rb) at this thread's n2
-                    const float va = fmaf(v[j].x - sref_t, a.c2, biasA + b2.x);
-                    const float vb = has_b ? fmaf(v[j].y - sref_t, a.c2, biasB + b2.y) : -INFINITY;
-                    v[j] = make_float2(va, vb);
-                    mt = fmaxf(mt, fmaxf(va, vb));
+                    float2 vab = px::fma(px::sub(v[j], px::bc(sref_t)), px::bc(a.c2), px::add(biasAB, lrp[h * 65 + j]));
+                    if (!has_b) vab.y = -INFINITY;
+                    v[j] = vab;
+                    mt = fmaxf(mt, fmaxf(vab.x, vab.y));
                 }
                 const float mref = mt == -INFINITY ? 0.f : mt;
-                float za1 = 0.f, zb1 = 0.f;
+                float2 zab = make_float2(0.f, 0.f), zab1 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
-                    const float ea = ex2(v[j].x - mref);
-                    const float eb = has_b ? ex2(v[j].y - mref) : 0.f;
-                    v[j] = make_float2(ea, eb);
-                    if (j & 1) { za1 += ea; zb1 += eb; } else { za += ea; zb += eb; }
+                    const float2 dm = px::sub(v[j], px::bc(mref));
+                    v[j] = make_float2(ex2(dm.x), has_b ? ex2(dm.y) : 0.f);
+                    if (j & 1) zab1 = px::add(zab1, v[j]);
+                    else zab = px::add(zab, v[j]);
                 }
-                za += za1;
-                zb += zb1;
+                za = zab.x + zab1.x;
+                zb = zab.y + zab1.y;
                 float sref = sref_t;
                 mall = mt;
                 zall = za + zb;
@@ -504,7 +507,9 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                         st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t,
                                       make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)),
                                                   zall, 0.f));
-                    cluster_arrive();
+                    // only warp 0 (t < NP) wrote remote data: the other warps arrive without a release fence
+                    if (warp == 0) cluster_arrive();
+                    else cluster_arrive_relaxed();
                 }
                 // weights relative to this pair's reference; the cluster factor 2^(g_q - G) / Z scales them after
                 // the (linear) forward transforms, in pass 3
@@ -560,8 +565,13 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                         const int m = ch * 8 + e;
                         const float2 z = v[m];
                         const float zy = su * z.y;
-                        ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
-                        ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
+                        {
+                            const float2 yy = make_float2(ys[2 * e], ys[2 * e + 1]);
+                            const float2 r = px::fma(make_float2(-yy.y, yy.x), px::bc(zy),
+                                                     px::fma(yy, px::bc(z.x), make_float2(ac[2 * e], ac[2 * e + 1])));
+                            ac[2 * e] = r.x;
+                            ac[2 * e + 1] = r.y;
+                        }
                         if (both) {
                             zc[(l >> 6) * LL + 2 * m + h] = z;
                             yc[(l >> 6) * LL + 2 * m + h] = make_float2(ys[2 * e], ys[2 * e + 1]);
