@@ -630,7 +630,11 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                 }
             }
             if (pass == 0) {
-                group_bar(bar_id, GT);
+                // at LL = 32 a class pair's lines are exactly one warp: its transpose buffer, its zc rows and its
+                // vex entries are warp-local, so the column -> row transpose needs only a warp barrier (the Yhat
+                // buffers are ordered by the reduction and pass-2 group barriers)
+                if constexpr (TACC && LL == 32) __syncwarp();
+                else group_bar(bar_id, GT);
                 if (TACC && vex_pending) vex_update(Yb + (buf ^ 1) * a.ybuf);  // the previous observation's pass 3
                 if (!TACC) prefetch(i + gstride, buf ^ 1);
             } else if (pass == 2) {
