@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-T=r2w
+T=r2x
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > gpurun_out/pytest_full_$T.log 2>&1
 tail -3 gpurun_out/pytest_full_$T.log
 for cfg in c3 c1 c3 c1; do
