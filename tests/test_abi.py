@@ -58,3 +58,33 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "srmra_oracle" not in txt, f
+
+
+def test_round2_options_layout_and_world_validation_without_gpu():
+    """The ctypes mirror of srmra_options matches the C defaults (exchange provider, grid cap, NCCL
+    timeout), and world > 1 without an NCCL id or a provider is rejected before any device call."""
+    import numpy as np
+    import paper_2204_04754_b200 as m
+    o = m.srmra_default_options()
+    assert not o.allreduce and o.allreduce_user is None and o.grid_cap == 0 and o.nccl_timeout_ms == 0
+    a = dict(y=np.zeros((3, 4, 4), np.float32), L_high=8, L_low=4, K=2, sigma=0.5, x0=np.zeros((8, 8)),
+             rho1_0=np.ones(8) / 8, rho2_0=np.ones(8) / 8)
+    for kw in (dict(world=2, rank=0), dict(world=2, rank=2), dict(world=0)):
+        try:
+            m.Context(**dict(a, **kw))
+            raise AssertionError(f"accepted {kw}")
+        except m.SrmraError as e:
+            assert e.code == m.SRMRA_ERR_INVALID_ARG, (kw, e)
+
+
+def test_bench_refuses_more_gpus_than_the_node_has():
+    """`bench.py --gpus N` outside torchrun must not silently measure fewer ranks (here: no GPU at all)."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k != "WORLD_SIZE"}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 2, (r.returncode, r.stdout[-500:], r.stderr[-500:])
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert "error" in line and "--gpus 2" in line["error"]

@@ -154,3 +154,26 @@ def test_world2_exchange_matches_full_data_oracle(world2, oracle_mod, key):
     # both ranks hold the same (all-reduced) estimate
     np.testing.assert_array_equal(r0["x"], r1["x"])
     np.testing.assert_array_equal(r0["b"], r1["b"])
+
+
+def test_exchange_provider_failure_is_reported():
+    """A failing exchange provider fails the call with SRMRA_ERR_NCCL (at init: the global-N sum; later: the
+    iteration's statistics sum) and leaves the context failed (every later call returns STATE)."""
+    import paper_2204_04754_b200 as srm
+    p = synth.make_random(8, 2, 9, 0.3, 2)
+    args = (p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0)
+    with pytest.raises(srm.SrmraError) as ei:
+        srm.Context(*args, world=2, rank=0, allreduce=lambda ptr, n, st: 1)
+    assert ei.value.code == srm.SRMRA_ERR_NCCL
+    calls = [0]
+
+    def flaky(ptr, n, st):  # the init-time N sum succeeds (a one-rank "sum" is the identity), then fail
+        calls[0] += 1
+        return 0 if calls[0] == 1 else 1
+    with srm.Context(*args, world=2, rank=0, allreduce=flaky) as ctx:
+        with pytest.raises(srm.SrmraError) as ei:
+            ctx.em_iter(1)
+        assert ei.value.code == srm.SRMRA_ERR_NCCL
+        with pytest.raises(srm.SrmraError) as ei:
+            ctx.get_estimate()
+        assert ei.value.code == srm.SRMRA_ERR_STATE
