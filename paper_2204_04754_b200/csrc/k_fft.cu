@@ -464,15 +464,30 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                     const bool flip = k2 >= LH;
                     const int sk2 = flip ? LL - k2 : k2;
                     const float sgn = flip ? -1.f : 1.f;
+                    // all of this column's Yhat reads first (LL loads in flight), the TMEM stash, then the
+                    // products in place
+#pragma unroll
+                    for (int k1 = 0; k1 < LL; ++k1) v[k1] = Y[ybase + k1 * ystep];
+                    if constexpr (TACC) {
+#pragma unroll
+                        for (int c8 = 0; c8 < LL; c8 += 8) {
+                            float ys[16];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                ys[2 * e] = v[c8 + e].x;
+                                ys[2 * e + 1] = v[c8 + e].y;
+                            }
+                            tc::tmem_st16(tys + 2 * c8, ys);
+                        }
+                    }
 #pragma unroll
                     for (int c8 = 0; c8 < LL; c8 += 8) {
-                        float ys[16];
 #pragma unroll
                         for (int e = 0; e < 8 && c8 + e < LL; ++e) {
                             const int k1 = c8 + e;
                             const int sk1 = flip ? ((LL - k1) & M) : k1;
                             const int o = sk1 * LH + sk2;
-                            const float2 yv = Y[ybase + k1 * ystep];
+                            const float2 yv = v[k1];
                             if constexpr (XS == 2) {
                                 const float4 cf = XP[k1 * LL + idx];  // (a, c, b, d), lane-contiguous: ideal wavefronts
                                 v[k1] = px::fma(px::bc(yv.x), make_float2(cf.x, cf.y), px::mul(px::bc(yv.y), make_float2(cf.z, cf.w)));
@@ -482,10 +497,7 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                                 const float2 B = cmul_conj(yv, make_float2(xv.z, xv.w));
                                 v[k1] = make_float2(A.x - sgn * B.y, -sgn * A.y - B.x);
                             }
-                            ys[2 * e] = yv.x;
-                            ys[2 * e + 1] = yv.y;
                         }
-                        if constexpr (TACC) tc::tmem_st16(tys + 2 * c8, ys);
                     }
                 } else if (pass == 1) {
                     // E-step along k2 (row n1 = idx) of the conjugated column result

@@ -396,38 +396,31 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
 #endif
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == 0) {
-                // E-step along k1 for column k2 = l: conj of Z = Yhat conj(Xa) + i Yhat conj(Xb)
+                // all of this column's Yhat reads first (64 loads in flight), the TMEM stash, then the products
+                // in place
+#pragma unroll
+                for (int m = 0; m < 64; ++m) {
+                    const int k1 = 2 * m + h;
+                    v[m] = Ys[(flip ? ((LL - k1) & (LL - 1)) : k1) * YR + sk2];
+                }
 #pragma unroll
                 for (int ch = 0; ch < 8; ++ch) {
                     float ys[16];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        const int m = ch * 8 + e;
-                        const int k1 = 2 * m + h;
-                        const int sk1 = flip ? ((LL - k1) & (LL - 1)) : k1;
-                        const float2 yv = Ys[sk1 * YR + sk2];
-                        // Yhat conj(Xhat_hi + Xhat_lo): the float32 rounding of Xhat is shared by every
-                        // observation and would bias the class logits systematically; the lo part removes it
-                        if constexpr (COEF) {
-                            const float4 ch = __ldg(CH + k1 * LL), cl = __ldg(CL + k1 * LL);
-                            const float2 lo = px::fma(px::bc(yv.x), make_float2(cl.x, cl.y),
-                                                      px::mul(px::bc(yv.y), make_float2(cl.z, cl.w)));
-                            v[m] = px::fma(px::bc(yv.x), make_float2(ch.x, ch.y),
-                                           px::fma(px::bc(yv.y), make_float2(ch.z, ch.w), lo));
-                        } else {
-                            const float4 xv = __ldg(XP + sk1 * LH + sk2);
-                            const float4 xl = __ldg(XPL + sk1 * LH + sk2);
-                            const float2 A = cmul_conj_acc(yv, make_float2(xv.x, xv.y), make_float2(xl.x, xl.y));
-                            const float2 B = has_b ? cmul_conj_acc(yv, make_float2(xv.z, xv.w), make_float2(xl.z, xl.w))
-                                                   : make_float2(0.f, 0.f);
-                            v[m] = make_float2(A.x - sg * B.y, -(sg * A.y + B.x));
-                        }
-                        // the DC bin (constant over the shifts) is added back in float64 after the transform
-                        if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
-                        ys[2 * e] = yv.x;
-                        ys[2 * e + 1] = yv.y;
+                        ys[2 * e] = v[ch * 8 + e].x;
+                        ys[2 * e + 1] = v[ch * 8 + e].y;
                     }
-                    tc::tmem_st16(ty + 16 * ch, ys);  // the Yhat values this thread's M-column pass needs
+                    tc::tmem_st16(ty + 16 * ch, ys);
+                }
+#pragma unroll
+                for (int m = 0; m < 64; ++m) {
+                    const int k1 = 2 * m + h;
+                    const float2 yv = v[m];
+                    const float4 ch = __ldg(CH + k1 * LL), cl = __ldg(CL + k1 * LL);
+                    const float2 lo = px::fma(px::bc(yv.x), make_float2(cl.x, cl.y), px::mul(px::bc(yv.y), make_float2(cl.z, cl.w)));
+                    v[m] = px::fma(px::bc(yv.x), make_float2(ch.x, ch.y), px::fma(px::bc(yv.y), make_float2(ch.z, ch.w), lo));
+                    if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
                 }
             } else if (pass == 1) {
 #pragma unroll
