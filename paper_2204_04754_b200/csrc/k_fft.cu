@@ -532,8 +532,12 @@ __global__ void __launch_bounds__(max_cta_threads<LL, TACC>(), 1) k_fft_em(EmArg
                             const int k1 = 8 * ch + e;
                             const float2 z = v[k1];
                             const float zy = su * z.y;
-                            ac[2 * e] = fmaf(ys[2 * e], z.x, fmaf(-ys[2 * e + 1], zy, ac[2 * e]));
-                            ac[2 * e + 1] = fmaf(ys[2 * e + 1], z.x, fmaf(ys[2 * e], zy, ac[2 * e + 1]));
+                            // packed: (-y.y, y.x) is a free operand modifier of FFMA2 (swapped halves, one negated)
+                            const float2 yy = make_float2(ys[2 * e], ys[2 * e + 1]);
+                            const float2 r = px::fma(yy, px::bc(z.x),
+                                                     px::fma(make_float2(-yy.y, yy.x), px::bc(zy), make_float2(ac[2 * e], ac[2 * e + 1])));
+                            ac[2 * e] = r.x;
+                            ac[2 * e + 1] = r.y;
                             if (vsrc) zc[q * (2 * LL + 2) + (idx == 0 ? 0 : LL + 1) + k1] = z;
                         }
                         tc::tmem_st16(tacc + 16 * ch, ac);

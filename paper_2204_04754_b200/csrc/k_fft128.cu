@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
             }
             // pass 2: v holds the posterior row of the pair (forward transform along n2)
             if (pass >= 2) dif_xall<-1>(v, h != 0, std::make_integer_sequence<int, 32>{});
-            fft_sr2<64, -1>(v);  // split radix, packed FP32x2
+            fft_sr2<64, -1, false>(v);  // split radix, packed FP32x2 (pair-constant twiddles: fewer spills here)
             if (pass < 2) dit_xall<-1>(v, h != 0, h ? -1.f : 1.f, std::make_integer_sequence<int, 32>{});
 
             if (pass == 0) {

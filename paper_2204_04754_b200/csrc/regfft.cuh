@@ -258,8 +258,12 @@ __device__ __forceinline__ float2 fma(float2 a, float2 b, float2 c) {
 __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
 }  // namespace px
 
-// b * W_N^TK (SIGN convention of twmul) in packed form: bx (c, s) + by (-s, c); +-i and -1 as swaps / signs
-template <int N, int SIGN, int TK>
+// b * W_N^TK (SIGN convention of twmul) in packed form; +-i and -1 as swaps / signs.  IMM: b w = c b + s (i b),
+// both constants scalar immediates of FMUL2 / FFMA2 and i b = (-b.y, b.x) a free operand modifier (swapped
+// halves, one negated: .F32x2.LO_HI.NP).  !IMM: bx (c, s) + by (-s, c), whose constant pairs are moved into
+// registers (UMOV / MOV) for every product — 232 fewer instructions per k_fft_em body with IMM, but at L_low = 128
+// (255 registers) ptxas spills more with IMM and k_fft_em128 measured slower (23.00 vs 22.62 ms), so it keeps !IMM
+template <int N, int SIGN, int TK, bool IMM>
 __device__ __forceinline__ float2 twmul2(float2 b) {
     constexpr int T = ((TK % N) + N) % N;
     if constexpr (T == 0 || 2 * T == N || 4 * T == N || 4 * T == 3 * N) {
@@ -267,12 +271,13 @@ __device__ __forceinline__ float2 twmul2(float2 b) {
     } else {
         constexpr float c = (float)cos2pi(T, N);
         constexpr float s = (float)(SIGN * sin2pi(T, N));
-        return px::fma(px::bc(b.y), make_float2(-s, c), px::mul(px::bc(b.x), make_float2(c, s)));
+        if constexpr (IMM) return px::fma(make_float2(-b.y, b.x), px::bc(s), px::mul(b, px::bc(c)));
+        else return px::fma(px::bc(b.y), make_float2(-s, c), px::mul(px::bc(b.x), make_float2(c, s)));
     }
 }
-template <int N, int SIGN, int K>
+template <int N, int SIGN, bool IMM, int K>
 __device__ __forceinline__ void sr2_comb(const float2* U, const float2* Z, const float2* Zp, float2* X) {
-    const float2 a = twmul2<N, SIGN, K>(Z[K]), b = twmul2<N, SIGN, 3 * K>(Zp[K]);
+    const float2 a = twmul2<N, SIGN, K, IMM>(Z[K]), b = twmul2<N, SIGN, 3 * K, IMM>(Zp[K]);
     const float2 sm = px::add(a, b);
     const float2 id = twmul<N, SIGN, N / 4>(px::sub(a, b));
     const float2 u0 = U[K], u1 = U[K + N / 4];
@@ -281,12 +286,12 @@ __device__ __forceinline__ void sr2_comb(const float2* U, const float2* Z, const
     X[K + N / 4] = px::add(u1, id);
     X[K + 3 * N / 4] = px::sub(u1, id);
 }
-template <int N, int SIGN, int... Ks>
+template <int N, int SIGN, bool IMM, int... Ks>
 __device__ __forceinline__ void sr2_combine(const float2* U, const float2* Z, const float2* Zp, float2* X,
                                             std::integer_sequence<int, Ks...>) {
-    (sr2_comb<N, SIGN, Ks>(U, Z, Zp, X), ...);
+    (sr2_comb<N, SIGN, IMM, Ks>(U, Z, Zp, X), ...);
 }
-template <int N, int SIGN, int OFF, int ST>
+template <int N, int SIGN, bool IMM, int OFF, int ST>
 __device__ __forceinline__ void sr2_rec(const float2* x, float2* X) {
     if constexpr (N == 1) {
         X[0] = x[OFF];
@@ -296,17 +301,17 @@ __device__ __forceinline__ void sr2_rec(const float2* x, float2* X) {
         X[1] = px::sub(a, b);
     } else {
         float2 U[N / 2], Z[N / 4], Zp[N / 4];
-        sr2_rec<N / 2, SIGN, OFF, 2 * ST>(x, U);
-        sr2_rec<N / 4, SIGN, OFF + ST, 4 * ST>(x, Z);
-        sr2_rec<N / 4, SIGN, OFF + 3 * ST, 4 * ST>(x, Zp);
-        sr2_combine<N, SIGN>(U, Z, Zp, X, std::make_integer_sequence<int, N / 4>{});
+        sr2_rec<N / 2, SIGN, IMM, OFF, 2 * ST>(x, U);
+        sr2_rec<N / 4, SIGN, IMM, OFF + ST, 4 * ST>(x, Z);
+        sr2_rec<N / 4, SIGN, IMM, OFF + 3 * ST, 4 * ST>(x, Zp);
+        sr2_combine<N, SIGN, IMM>(U, Z, Zp, X, std::make_integer_sequence<int, N / 4>{});
     }
 }
 // split radix in packed FP32x2 arithmetic
-template <int N, int SIGN>
+template <int N, int SIGN, bool IMM = true>
 __device__ __forceinline__ void fft_sr2(float2 (&v)[N]) {
     float2 X[N];
-    sr2_rec<N, SIGN, 0, 1>(v, X);
+    sr2_rec<N, SIGN, IMM, 0, 1>(v, X);
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = X[i];
 }
