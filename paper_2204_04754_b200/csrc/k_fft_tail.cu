@@ -23,6 +23,16 @@
 
 namespace cg = cooperative_groups;
 
+// SRMRA_TAIL_ROLLED (A/B): every loop of the tail rolled, the smallest code (the tail runs once per iteration from a
+// cold instruction cache)
+#ifdef SRMRA_TAIL_ROLLED
+#define TAIL_UNROLL _Pragma("unroll 1")
+#define TAIL_INNER _Pragma("unroll 1")
+#else
+#define TAIL_UNROLL _Pragma("unroll")
+#define TAIL_INNER
+#endif
+
 namespace srmra {
 
 int fft_partial_bins(int KK, int Ll);
@@ -67,41 +77,55 @@ struct TailArgs {
 };
 
 __device__ inline void grid_sync() { cg::this_grid().sync(); }
+__device__ inline unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
-// ---- phase R: bins in rounds of 32, kSlices threads per bin, 4 independent chains per thread
+// ---- phase R: bins in rounds of 32, kSlices threads per bin, two rounds per pass.  A thread issues the loads of
+// all its partials of both rounds (up to kMaxP each, unrolled and predicated) before the first add: one L2 round
+// trip per pass instead of one per group of four partials; the sum over them is a fixed-order chain.
+constexpr int kMaxP = 20;
 template <bool JOINT>
 __device__ void phase_reduce(const TailArgs& a) {
-    __shared__ double2 red[kSlices][33];
+    __shared__ double2 red[2][kSlices][33];
     const int b = threadIdx.x & 31, sl = threadIdx.x >> 5;
-    for (int base = blockIdx.x * 32; base < a.PB; base += gridDim.x * 32) {
-        const int k = base + b;
-        double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
-        if (k < a.PB) {
-            int c = sl;
-            for (; c + 3 * kSlices < a.nparts; c += 4 * kSlices) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float2 v = __ldcg(a.part + (size_t)(c + u * kSlices) * a.PB + k);
-                    sx[u] += v.x;
-                    sy[u] += v.y;
-                }
+    const int step = gridDim.x * 32;
+    for (int base = blockIdx.x * 32; base < a.PB; base += 2 * step) {
+        const int k0 = base + b, k1 = base + step + b;
+        double sx0 = 0.0, sy0 = 0.0, sx1 = 0.0, sy1 = 0.0;
+        for (int c0 = sl; c0 < a.nparts; c0 += kMaxP * kSlices) {
+            float2 v0[kMaxP], v1[kMaxP];
+TAIL_UNROLL
+            for (int u = 0; u < kMaxP; ++u) {
+                const int c = c0 + u * kSlices;
+                const float2* pc = a.part + (size_t)c * a.PB;
+                v0[u] = (c < a.nparts && k0 < a.PB) ? __ldcg(pc + k0) : make_float2(0.f, 0.f);
+                v1[u] = (c < a.nparts && k1 < a.PB) ? __ldcg(pc + k1) : make_float2(0.f, 0.f);
             }
-            for (; c < a.nparts; c += kSlices) {
-                const float2 v = __ldcg(a.part + (size_t)c * a.PB + k);
-                sx[0] += v.x;
-                sy[0] += v.y;
+TAIL_UNROLL
+            for (int u = 0; u < kMaxP; ++u) {
+                sx0 += v0[u].x;
+                sy0 += v0[u].y;
+                sx1 += v1[u].x;
+                sy1 += v1[u].y;
             }
         }
-        red[sl][b] = make_double2((sx[0] + sx[1]) + (sx[2] + sx[3]), (sy[0] + sy[1]) + (sy[2] + sy[3]));
+        red[0][sl][b] = make_double2(sx0, sy0);
+        red[1][sl][b] = make_double2(sx1, sy1);
         __syncthreads();
-        if (sl == 0 && k < a.PB) {
-            double tx = 0.0, ty = 0.0;
-            for (int j = 0; j < kSlices; ++j) {
-                tx += red[j][b].x;
-                ty += red[j][b].y;
+        if (sl < 2) {
+            const int k = sl ? k1 : k0;
+            if (k < a.PB) {
+                double tx = 0.0, ty = 0.0;
+                for (int j = 0; j < kSlices; ++j) {
+                    tx += red[sl][j][b].x;
+                    ty += red[sl][j][b].y;
+                }
+                a.acc[2 * k] = tx;
+                a.acc[2 * k + 1] = ty;
             }
-            a.acc[2 * k] = tx;
-            a.acc[2 * k + 1] = ty;
         }
         __syncthreads();
     }
@@ -109,16 +133,20 @@ __device__ void phase_reduce(const TailArgs& a) {
         __shared__ double redj[kSlices][33];
         for (int base = blockIdx.x * 32; base < a.JB; base += gridDim.x * 32) {
             const int k = base + b;
-            double sx[4] = {0, 0, 0, 0};
+            double sx = 0.0;
             if (k < a.JB) {
-                int c = sl;
-                for (; c + 3 * kSlices < a.nparts; c += 4 * kSlices) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) sx[u] += __ldcg(a.jpart + (size_t)(c + u * kSlices) * a.JB + k);
+                for (int c0 = sl; c0 < a.nparts; c0 += kMaxP * kSlices) {
+                    float v[kMaxP];
+TAIL_UNROLL
+                    for (int u = 0; u < kMaxP; ++u) {
+                        const int c = c0 + u * kSlices;
+                        v[u] = c < a.nparts ? __ldcg(a.jpart + (size_t)c * a.JB + k) : 0.f;
+                    }
+TAIL_UNROLL
+                    for (int u = 0; u < kMaxP; ++u) sx += v[u];
                 }
-                for (; c < a.nparts; c += kSlices) sx[0] += __ldcg(a.jpart + (size_t)c * a.JB + k);
             }
-            redj[sl][b] = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+            redj[sl][b] = sx;
             __syncthreads();
             if (sl == 0 && k < a.JB) {
                 double tx = 0.0;
@@ -134,6 +162,22 @@ __device__ void phase_reduce(const TailArgs& a) {
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (b == 0) a.acc[2 * a.PB] = s;
     }
+}
+
+// class mass: the sum of a line of Ll row sums, by one warp — lane sums of a stride-32 walk, then an xor shuffle
+// tree (the same fixed order in every caller, and the same value in every lane).  `pre` holds this lane's values
+// (t = lane + 32 j, j < 4, zero past Ll), loaded by the caller together with its other loads.
+__device__ __forceinline__ double line_sum(const double (&pre)[4]) {
+    double s = ((pre[0] + pre[1]) + pre[2]) + pre[3];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+template <typename F>
+__device__ __forceinline__ void line_load(double (&pre)[4], int Ll, F at) {
+    const int lane = threadIdx.x & 31;
+TAIL_UNROLL
+    for (int j = 0; j < 4; ++j) pre[j] = lane + 32 * j < Ll ? at(lane + 32 * j) : 0.0;
 }
 
 // ---- phase F: item (r, ch) -> rows [ch R, ch R + R) of b_r (and x' there when `update`);
@@ -157,23 +201,40 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
         if (item < KK * a.nchunk) {
             const int r = item / a.nchunk, ch = item - r * a.nchunk, r1 = r / K, r2 = r % K;
             const int m1a = ch * R;
-            if (update && threadIdx.x == 0) {  // class mass of class r, summed as in the marginals item
-                const double2* Rr = A + (size_t)2 * NP * Ll * Lh + (size_t)r * Ll;
-                double cmr = 0.0;
-                for (int t = 0; t < Ll; ++t) cmr += __ldcg(&Rr[t].x);
-                cm_s = cmr;
-            }
+            // class mass of class r (warp 0, summed as in the marginals item), its loads issued with the first
+            // chunk of the B loads: one L2 round trip per chunk of kE bins per thread
+            double pre[4] = {0.0, 0.0, 0.0, 0.0};
+            const double2* Rr = A + (size_t)2 * NP * Ll * Lh + (size_t)r * Ll;
+            if (update && threadIdx.x < 32) line_load(pre, Ll, [&](int t) { return __ldcg(&Rr[t].x); });
             const double2* U = A + (size_t)(r / 2) * 2 * Ll * Lh;
             const double2* V = U + (size_t)Ll * Lh;
-            for (int e = threadIdx.x; e < Ll * Lh; e += blockDim.x) {
-                const double2 u = __ldcg(U + e), v = __ldcg(V + e);
-                B[e] = (r & 1) ? make_double2(-0.5 * (u.y - v.y), 0.5 * (u.x - v.x))
-                               : make_double2(0.5 * (u.x + v.x), 0.5 * (u.y + v.y));
+            constexpr int kE = 4;
+            for (int e0 = threadIdx.x; e0 < Ll * Lh; e0 += kE * blockDim.x) {
+                double2 uu[kE], vv[kE];
+TAIL_UNROLL
+                for (int q = 0; q < kE; ++q) {
+                    const int e = e0 + q * blockDim.x;
+                    uu[q] = e < Ll * Lh ? __ldcg(U + e) : make_double2(0.0, 0.0);
+                    vv[q] = e < Ll * Lh ? __ldcg(V + e) : make_double2(0.0, 0.0);
+                }
+TAIL_UNROLL
+                for (int q = 0; q < kE; ++q) {
+                    const int e = e0 + q * blockDim.x;
+                    const double2 u = uu[q], v = vv[q];
+                    if (e < Ll * Lh)
+                        B[e] = (r & 1) ? make_double2(-0.5 * (u.y - v.y), 0.5 * (u.x - v.x))
+                                       : make_double2(0.5 * (u.x + v.x), 0.5 * (u.y + v.y));
+                }
+            }
+            if (update && threadIdx.x < 32) {
+                const double cmr = line_sum(pre);
+                if (threadIdx.x == 0) cm_s = cmr;
             }
             __syncthreads();
             for (int e = threadIdx.x; e < R * Lh; e += blockDim.x) {  // inverse along k1
                 const int mm = e / Lh, k2 = e - mm * Lh, m1 = m1a + mm;
                 double re = 0, im = 0;
+                TAIL_INNER
                 for (int k1 = 0; k1 < Ll; ++k1) {
                     const int j = (k1 * m1) & M;
                     const double2 t = B[k1 * Lh + k2];
@@ -188,6 +249,7 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                 const int mm = e / Ll, m2 = e - mm * Ll, m1 = m1a + mm;
                 const double2* Tr = T + mm * Lh;
                 double s = Tr[0].x + ((m2 & 1) ? -Tr[Ll / 2].x : Tr[Ll / 2].x);
+                TAIL_INNER
                 for (int k2 = 1; k2 < Ll / 2; ++k2) {
                     const int j = (k2 * m2) & M;
                     s += 2.0 * (Tr[k2].x * cs[j] - Tr[k2].y * sn[j]);
@@ -208,28 +270,63 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
             const double2* CU = Rg + (size_t)KK * Ll;
             double* Rs = reinterpret_cast<double*>(B);            // [KK][Ll]
             double2* crow = reinterpret_cast<double2*>(Rs + KK * Ll);  // [KK][Lh]
+            // every load of the item first (chunks of kE elements per thread: one L2 round trip each)
             if (threadIdx.x == 0) a.pack[a.off_ll] = __ldcg(a.acc + 2 * (size_t)a.PB);
-            for (int e = threadIdx.x; e < KK * Ll; e += blockDim.x) Rs[e] = __ldcg(&Rg[e].x);
-            for (int e = threadIdx.x; e < KK * Lh; e += blockDim.x) {
-                const int cls = e / Lh, k2 = e - cls * Lh, qq = cls / 2;
-                const double2 zp = __ldcg(CU + (size_t)qq * Ll + k2), zm = __ldcg(CU + (size_t)qq * Ll + ((Ll - k2) & M));
-                crow[e] = (cls & 1) ? make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x))
-                                    : make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+            double2 rho_pre[2];  // (rho1[k], rho2[k]) of the update's k = threadIdx.x + u blockDim.x
+TAIL_UNROLL
+            for (int u = 0; u < 2; ++u) {
+                const int k = threadIdx.x + u * blockDim.x;
+                rho_pre[u] = (update && !JOINT && k < L) ? make_double2(a.rho[k], a.rho[L + k]) : make_double2(0.0, 0.0);
+            }
+            constexpr int kE = 4;
+            const int nR = KK * Ll, nC = KK * Lh;
+            for (int e0 = threadIdx.x; e0 < nR + nC; e0 += kE * blockDim.x) {
+                double2 zp[kE], zm[kE];
+TAIL_UNROLL
+                for (int q = 0; q < kE; ++q) {
+                    const int e = e0 + q * blockDim.x;
+                    zp[q] = zm[q] = make_double2(0.0, 0.0);
+                    if (e < nR) {
+                        zp[q].x = __ldcg(&Rg[e].x);
+                    } else if (e < nR + nC) {
+                        const int ec = e - nR, cls = ec / Lh, k2 = ec - cls * Lh, qq = cls / 2;
+                        zp[q] = __ldcg(CU + (size_t)qq * Ll + k2);
+                        zm[q] = __ldcg(CU + (size_t)qq * Ll + ((Ll - k2) & M));
+                    }
+                }
+TAIL_UNROLL
+                for (int q = 0; q < kE; ++q) {
+                    const int e = e0 + q * blockDim.x;
+                    if (e < nR) {
+                        Rs[e] = zp[q].x;
+                    } else if (e < nR + nC) {
+                        const int ec = e - nR, cls = ec / Lh;
+                        crow[ec] = (cls & 1) ? make_double2(0.5 * (zp[q].y + zm[q].y), 0.5 * (zm[q].x - zp[q].x))
+                                             : make_double2(0.5 * (zp[q].x + zm[q].x), 0.5 * (zp[q].y - zm[q].y));
+                    }
+                }
             }
             __syncthreads();
-            for (int rr = threadIdx.x; rr < KK; rr += blockDim.x) {
-                double s = 0.0;
-                for (int t = 0; t < Ll; ++t) s += Rs[rr * Ll + t];
-                a.pack[a.off_cm + rr] = s;   // class mass sum_i sum_{s in class r} w^{i,s}
+            for (int rr = threadIdx.x >> 5; rr < KK; rr += blockDim.x >> 5) {  // one warp per class
+                double pre[4];
+                line_load(pre, Ll, [&](int t) { return Rs[rr * Ll + t]; });
+                const double s = line_sum(pre);
+                if ((threadIdx.x & 31) == 0) a.pack[a.off_cm + rr] = s;   // class mass sum_i sum_{s in class r} w^{i,s}
             }
             const double invL = 1.0 / Ll;
-            for (int s = threadIdx.x; s < L; s += blockDim.x) {
+            // this thread's marginals stay in registers for the rho update (L <= 2 blockDim: at most 2 per thread)
+            double m1v[2] = {0.0, 0.0}, m2v[2] = {0.0, 0.0};
+TAIL_UNROLL
+            for (int u = 0; u < 2; ++u) {
+                const int s = threadIdx.x + u * blockDim.x;
+                if (s >= L) break;
                 const int rs = s % K, t = s / K;
                 double a1 = 0.0, a2 = 0.0;
                 for (int ro = 0; ro < K; ++ro) {
                     a1 += Rs[(rs * K + ro) * Ll + t];   // marg1[s] = sum_{r2} R_{(rs, r2)}[t]
                     const double2* cr = crow + (ro * K + rs) * Lh;  // marg2[s] = sum_{r1} C_{(r1, rs)}[t]
                     a2 += cr[0].x + ((t & 1) ? -cr[Ll / 2].x : cr[Ll / 2].x);
+                    TAIL_INNER
                     for (int k2 = 1; k2 < Ll / 2; ++k2) {
                         const int j = (k2 * t) & M;
                         a2 += 2.0 * (cr[k2].x * cs[j] - cr[k2].y * sn[j]);
@@ -237,6 +334,8 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                 }
                 a.pack[a.off_m1 + s] = a1;
                 a.pack[a.off_m2 + s] = a2 * invL;
+                m1v[u] = a1;
+                m2v[u] = a2 * invL;
             }
             if (JOINT && update) {
                 // eq:rho_EM as written: rho'[s] = sum_i w^{i,s} / sum_i sum_s' w^{i,s'} (zero prior mass stays
@@ -268,20 +367,39 @@ __device__ void phase_fold(const TailArgs& a, double* sm, bool update) {
                     a.rho[L + k] = r2;
                 }
             } else if (update) {
-                // eq:rho_EM marginals; zero prior mass stays exactly zero; per-axis normalisation
-                __syncthreads();  // this block's marginal writes visible to the block
+                // eq:rho_EM marginals; zero prior mass stays exactly zero; per-axis normalisation (the marginals
+                // from registers, rho prefetched at the top of the item, both sums in one block reduction)
                 double m1s = 0.0, m2s = 0.0;
-                for (int k = threadIdx.x; k < L; k += blockDim.x) {
-                    m1s += a.rho[k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m1 + k], 0.0);
-                    m2s += a.rho[L + k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m2 + k], 0.0);
+                double g1[2], g2[2];
+TAIL_UNROLL
+                for (int u = 0; u < 2; ++u) {
+                    const int k = threadIdx.x + u * blockDim.x;
+                    g1[u] = k < L && rho_pre[u].x != 0.0 ? fmax(m1v[u], 0.0) : 0.0;
+                    g2[u] = k < L && rho_pre[u].y != 0.0 ? fmax(m2v[u], 0.0) : 0.0;
+                    m1s += g1[u];
+                    m2s += g2[u];
                 }
-                m1s = block_sum(m1s, red);
-                m2s = block_sum(m2s, red);
+                m1s = warp_sum(m1s);
+                m2s = warp_sum(m2s);
+                __shared__ double red2[2][32];
+                if ((threadIdx.x & 31) == 0) {
+                    red2[0][threadIdx.x >> 5] = m1s;
+                    red2[1][threadIdx.x >> 5] = m2s;
+                }
                 __syncthreads();
+                {
+                    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+                    m1s = warp_sum(lane < nw ? red2[0][lane] : 0.0);
+                    m2s = warp_sum(lane < nw ? red2[1][lane] : 0.0);
+                }
                 if (m1s > 0.0 && m2s > 0.0) {
-                    for (int k = threadIdx.x; k < L; k += blockDim.x) {
-                        a.rho[k] = a.rho[k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m1 + k], 0.0) / m1s;
-                        a.rho[L + k] = a.rho[L + k] == 0.0 ? 0.0 : fmax(a.pack[a.off_m2 + k], 0.0) / m2s;
+TAIL_UNROLL
+                    for (int u = 0; u < 2; ++u) {
+                        const int k = threadIdx.x + u * blockDim.x;
+                        if (k < L) {
+                            a.rho[k] = g1[u] / m1s;
+                            a.rho[L + k] = g2[u] / m2s;
+                        }
                     }
                 }
             }
@@ -323,6 +441,8 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
             // project); at load time, x_0.  The ch == 0 item of class r also stores x'' and E_r, mean(x''_r)
             const bool from_tmp = (a.mode & TAIL_FINALIZE) != 0;
             double e2 = 0.0, e1 = 0.0;
+            // (4 pixels per thread with all 36 stencil loads issued before the first use, and x' stored polyphase by phase
+            // F so that every stencil load of a warp is a contiguous run instead of a stride-K gather: neither was faster)
             for (int m = threadIdx.x; m < Ll * Ll; m += blockDim.x) {
                 const int m1 = m / Ll, m2 = m - m1 * Ll;
                 const int p1 = imod(K * m1 - r1, L), p2 = imod(K * m2 - r2, L);
@@ -364,6 +484,7 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
                 const int n1 = e / nw, kk = e - n1 * nw, k2 = k2a + kk;
                 const double* row = src + n1 * Ll;
                 double re = 0, im = 0;
+                TAIL_INNER
                 for (int n2 = 0; n2 < Ll; ++n2) {
                     const int j = (k2 * n2) & M;
                     re = fma(row[n2], cs[j], re);
@@ -378,6 +499,7 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
             for (int e = threadIdx.x; e < Ll * nw; e += blockDim.x) {  // along n1: rows k1, columns of the chunk
                 const int k1 = e / nw, kk = e - k1 * nw, k2 = k2a + kk;
                 double re = 0, im = 0;
+                TAIL_INNER
                 for (int n1 = 0; n1 < Ll; ++n1) {
                     const int j = (k1 * n1) & M;
                     const double2 t = tmp[n1 * Wq + kk];
@@ -416,6 +538,17 @@ __device__ void phase_prep(const TailArgs& a, double* sm) {
     }
 }
 
+// debug (SRMRA_TAIL_STAMPS): the slowest block's item-loop duration of a phase (ns << 12 | its last item), slot k
+__device__ inline void stamp_items(const TailArgs& a, int k, unsigned long long t0, int nitems) {
+    if (!a.stamps) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int last = -1;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) last = it;
+        atomicMax(a.stamps + k, ((gtime() - t0) << 12) | (unsigned long long)(last & 0xfff));
+    }
+}
+
 __device__ inline void stamp(const TailArgs& a, int k) {
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
@@ -425,7 +558,7 @@ __device__ inline void stamp(const TailArgs& a, int k) {
 }
 
 template <bool JOINT>
-__global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_fft_tail(TailArgs a) {
     extern __shared__ double sm[];
     if (*reinterpret_cast<volatile int*>(a.run)) return;  // a converged srmra_run: nothing left to do
     {  // graph-replayable: the iteration index and the projection flag come from the device
@@ -446,13 +579,17 @@ __global__ void __launch_bounds__(kThreads) k_fft_tail(TailArgs a) {
     if (a.mode & TAIL_FOLD) {
         if (!synced) grid_sync();
         stamp(a, 1);
+        const unsigned long long t0 = a.stamps ? gtime() : 0ull;
         phase_fold<JOINT>(a, sm, (a.mode & TAIL_FINALIZE) != 0);
+        stamp_items(a, 2, t0, a.K * a.K * a.nchunk + 1);
         synced = false;
     }
     if (a.mode & TAIL_PREP) {
         if (!synced) grid_sync();
         stamp(a, 4);
+        const unsigned long long t0 = a.stamps ? gtime() : 0ull;
         phase_prep<JOINT>(a, sm);
+        stamp_items(a, 3, t0, a.K * a.K * a.nchunk_q + 1);
     }
     if (a.stamps) {
         __syncthreads();

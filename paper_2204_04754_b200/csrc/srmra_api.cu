@@ -1112,6 +1112,7 @@ int srmra_debug_timestamps(srmra_ctx* c, uint64_t* out8) {
     // re-arm the cross-block extremes: [6] earliest tail-block start (min), [7] latest tail-block end (max)
     const uint64_t arm[2] = {~0ull, 0ull};
     CK(cudaMemcpy(c->d_stamps + 6, arm, sizeof(arm), cudaMemcpyHostToDevice));
+    CK(cudaMemset(c->d_stamps + 2, 0, 2 * sizeof(uint64_t)));  // [2] / [3]: slowest block's fold / prep item loop
     return SRMRA_OK;
 }
 

@@ -27,3 +27,5 @@ with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0)
         print(f"    tail span {(st[7] - st[6]) / 1e3:.1f} us "
               f"(phases: reduce {(st[1] - st[0]) / 1e3:.1f}, fold+update {(st[4] - st[1]) / 1e3:.1f}, "
               f"prep {(st[5] - st[4]) / 1e3:.1f})")
+        for k, nm in ((2, "fold"), (3, "prep")):
+            print(f"    slowest {nm} block: {(int(st[k]) >> 12) / 1e3:.1f} us of item work (last item {int(st[k]) & 0xfff})")
