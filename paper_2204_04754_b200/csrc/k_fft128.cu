@@ -227,7 +227,7 @@ struct Em128Args {
     const double* ynorm;  // [n]
     const double* ysum;   // [n] sum_n y_i[n] (the DC bin Yhat_i[0][0], float64)
     const float4* xhat;   // [2 (hi | lo)][NP][128][65] pair-interleaved (Xhat_2q, Xhat_2q+1) / L_low^2
-    const float4* coef;   // COEF: [2 (hi | lo)][NP][128 k1][128 k2] E-step product coefficients (k_fft128_coef)
+    const float2* coef;   // COEF: [2 (hi | lo)][NP][128 k1][128 k2] E-step product coefficients (A, B) (k_fft128_coef)
     const float* par32;   // log2 units: lr1[L] | lr2[L] | beta[KK]
     const double* par64;  // E[KK] | (unused) | xm[KK] (mean of x_r)
     int64_t n;
@@ -244,10 +244,14 @@ struct Em128Args {
 };
 
 // E-step product coefficients (COEF variant): for column k2 of pair q and row k1 the conjugated packed product
-// v = conj(Yhat conj(Xhat_a) + i Yhat conj(Xhat_b)) of pass 0 is Y.x (a, c) + Y.y (b, d) (k_fft.cu, XS = 2; the
-// Hermitian mirror k2 >= 65 resolved here), with (a, c, b, d) formed in float64 from Xhat = hi + lo and stored
-// as float32 hi + lo: 4 packed FP32x2 instructions per element instead of two compensated complex products.
-__global__ void k_fft128_coef(const float4* __restrict__ xhat, int NP, float4* __restrict__ coef) {
+// v = conj(Yhat conj(Xhat_a) + i Yhat conj(Xhat_b)) of pass 0 is, with the true spectrum values Y (k2 >= 65: the
+// conjugate of the stored mirror),  v = Y.x (A, B) + Y.y (B, -A),  A = Xa.x + Xb.y, B = Xa.y - Xb.x  (k_fft.cu XS = 2
+// stores the same as four numbers (A, B, B, -A) / (A, B, -B, A)).  Two numbers per (k1, k2), formed in float64 from
+// Xhat = hi + lo and stored as float32 hi + lo planes: 16 B per element where the four-number form streamed 32 B
+// from L2 into pass 0 (whose loads were the kernel's largest latency stall); the kernel forms
+// Y.y (B, -A) = (-Y.y) (-B, A) with (-B, A) a free FFMA2 operand modifier and -Y.y (conjugation of a mirrored
+// stored value included) one FMUL.
+__global__ void k_fft128_coef(const float4* __restrict__ xhat, int NP, float2* __restrict__ coef) {
     const int total = NP * LL * LL;
     const float4* xlo = xhat + (size_t)NP * LL * LH;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
@@ -256,15 +260,11 @@ __global__ void k_fft128_coef(const float4* __restrict__ xhat, int NP, float4* _
         const int o = q * LL * LH + (fl ? ((LL - k1) & (LL - 1)) : k1) * LH + (fl ? LL - k2 : k2);
         const float4 h = xhat[o], l = xlo[o];
         const double ax = (double)h.x + l.x, ay = (double)h.y + l.y, bx = (double)h.z + l.z, by = (double)h.w + l.w;
-        double c0, c1, c2, c3;  // (a, c, b, d)
-        if (fl) {
-            c0 = ax - by; c1 = -ay - bx; c2 = ay + bx; c3 = ax - by;
-        } else {
-            c0 = ax + by; c1 = ay - bx; c2 = ay - bx; c3 = -ax - by;
-        }
-        const float4 hi = make_float4((float)c0, (float)c1, (float)c2, (float)c3);
+        // true values of a mirrored column: Xa = conj(stored), Xb = conj(stored)
+        const double A = fl ? ax - by : ax + by, B = fl ? -ay - bx : ay - bx;
+        const float2 hi = make_float2((float)A, (float)B);
         coef[k] = hi;
-        coef[(size_t)total + k] = make_float4((float)(c0 - hi.x), (float)(c1 - hi.y), (float)(c2 - hi.z), (float)(c3 - hi.w));
+        coef[(size_t)total + k] = make_float2((float)(A - hi.x), (float)(B - hi.y));
     }
 }
 
@@ -345,8 +345,9 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const float sg = flip ? -1.f : 1.f;
     const float4* XP = a.xhat + (size_t)q * LL * LH;
     const float4* XPL = XP + (size_t)NP * LL * LH;  // lo plane
-    const float4* CH = a.coef + (size_t)q * LL * LL + l;            // COEF: hi coefficients of column l
-    const float4* CL = CH + (size_t)NP * LL * LL;                   // lo
+    const float2* CH = a.coef + (size_t)q * LL * LL + l;            // COEF: hi coefficients of column l
+    const float2* CL = CH + (size_t)NP * LL * LL;                   // lo
+    const float ysg = flip ? 1.f : -1.f;                            // -Y.y = ysg * (stored Y).y
     const float* lr1 = pars;
     const float* lr2 = pars + L;
     const float* beta = pars + 2 * L;
@@ -417,9 +418,12 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 for (int m = 0; m < 64; ++m) {
                     const int k1 = 2 * m + h;
                     const float2 yv = v[m];
-                    const float4 ch = __ldg(CH + k1 * LL), cl = __ldg(CL + k1 * LL);
-                    const float2 lo = px::fma(px::bc(yv.x), make_float2(cl.x, cl.y), px::mul(px::bc(yv.y), make_float2(cl.z, cl.w)));
-                    v[m] = px::fma(px::bc(yv.x), make_float2(ch.x, ch.y), px::fma(px::bc(yv.y), make_float2(ch.z, ch.w), lo));
+                    const float2 ch = __ldg(CH + k1 * LL), cl = __ldg(CL + k1 * LL);
+                    const float ny = ysg * yv.y;  // -Y.y of the true spectrum value
+                    // v = Y.x (A, B) + (-Y.y) (-B, A), lo part first; the pair is the first operand (its swapped,
+                    // half-negated form is then an operand modifier)
+                    const float2 lo = px::fma(cl, px::bc(yv.x), px::mul(make_float2(-cl.y, cl.x), px::bc(ny)));
+                    v[m] = px::fma(ch, px::bc(yv.x), px::fma(make_float2(-ch.y, ch.x), px::bc(ny), lo));
                     if (m == 0 && (l | h) == 0) v[m] = make_float2(0.f, 0.f);
                 }
             } else if (pass == 1) {
@@ -653,7 +657,7 @@ static auto em128_kernel(int KK) {
     if (coef_mode()) return KK % 2 == 0 ? k_fft_em128<true, true> : k_fft_em128<false, true>;
     return KK % 2 == 0 ? k_fft_em128<true, false> : k_fft_em128<false, false>;
 }
-size_t fft128_coef_float4(int KK) { return (size_t)2 * ((KK + 1) / 2) * LL * LL; }
+size_t fft128_coef_float4(int KK) { return (size_t)((KK + 1) / 2) * LL * LL; }  // [2][NP][LL][LL] float2
 
 cudaError_t fft128_plan(srmra_ctx* c) {
     auto kern = em128_kernel(c->KK);
@@ -685,7 +689,7 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.ynorm = c->d_ynorm;
     a.ysum = c->d_ysum;
     a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
-    a.coef = c->d_xcoef;
+    a.coef = reinterpret_cast<const float2*>(c->d_xcoef);
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
     a.n = c->n_local;
@@ -694,7 +698,7 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.KK = c->KK;
     a.NP = (c->KK + 1) / 2;
     if (coef_mode()) {
-        k_fft128_coef<<<2 * c->num_sms, 256, 0, c->stream>>>(a.xhat, a.NP, c->d_xcoef);
+        k_fft128_coef<<<2 * c->num_sms, 256, 0, c->stream>>>(a.xhat, a.NP, reinterpret_cast<float2*>(c->d_xcoef));
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
