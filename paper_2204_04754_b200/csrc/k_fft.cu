@@ -256,9 +256,11 @@ __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, f
 // so one float4 per (bin, g) turns the two complex products and their combination (10 FP32
 // instructions) into 2 FMUL + 2 FFMA.  Stored per (k1, k2 < LL) in the order the column threads read
 // them (the mirror resolved at staging), so a warp's load is 32 consecutive float4.
+// (Mode 2 stores two numbers per (k1, k2): (b, d) = (B, -A) for g = +1 and (-B, A) for g = -1 with (a, c) = (A, B),
+// see the kernel.)
 template <int LL>
 __host__ __device__ inline size_t xs_bytes(int KK, int xs_mode = 1) {
-    return sizeof(float4) * (size_t)((KK + 1) / 2) * LL * (xs_mode == 2 ? LL : LL / 2 + 1);
+    return (xs_mode == 2 ? sizeof(float2) : sizeof(float4)) * (size_t)((KK + 1) / 2) * LL * (xs_mode == 2 ? LL : LL / 2 + 1);
 }
 
 // MAXT: the launch bound (register budget).  L_low = 32 with a 256-thread group (K^2 >= 15) fits one group in the
@@ -316,15 +318,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
         for (int k = threadIdx.x; k < NP * LL * LH; k += blockDim.x) dst[k] = __ldg(src + k);
     } else if (XS == 2) {  // product coefficients in the order pass 0 reads them: [q][k1][k2], k2 < LL
         const float4* src = a.xhat;
-        float4* dst = reinterpret_cast<float4*>(smem_raw + pb);
+        float2* dst = reinterpret_cast<float2*>(smem_raw + pb);
         for (int k = threadIdx.x; k < NP * LL * LL; k += blockDim.x) {
             const int qq = k / (LL * LL), rem = k - qq * LL * LL, k1 = rem / LL, k2 = rem - k1 * LL;
             const bool fl = k2 >= LH;  // Hermitian mirror of a stored bin, g = -1
             const int o = (fl ? ((LL - k1) & M) : k1) * LH + (fl ? LL - k2 : k2);
             const float4 x = __ldg(src + (size_t)qq * LL * LH + o);  // (xa, xb)
-            // stored as (a, c, b, d): v = Y.x (a, c) + Y.y (b, d) in packed FP32x2
-            dst[k] = fl ? make_float4(x.x - x.w, -x.y - x.z, x.y + x.z, x.x - x.w)
-                        : make_float4(x.x + x.w, x.y - x.z, x.y - x.z, -x.x - x.w);
+            // (a, c) = (A, B); v = Y.x (A, B) + Y.y (b, d) with (b, d) = (B, -A) (g = +1) or (-B, A) (g = -1)
+            dst[k] = fl ? make_float2(x.x - x.w, -x.y - x.z) : make_float2(x.x + x.w, x.y - x.z);
         }
     }
     __shared__ uint32_t tmem_slot;
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
     const int idx = line_ok ? tg - q * LL : 0;
     const int ra = 2 * q, rb = 2 * q + 1;
     const bool has_b = PAIRS || rb < KK;
-    const float4* XP = (XS ? reinterpret_cast<const float4*>(smem_raw + pb) : a.xhat) + (size_t)q * LL * (XS == 2 ? LL : LH);
+    const float4* XP = (XS ? reinterpret_cast<const float4*>(smem_raw + pb) : a.xhat) + (size_t)q * LL * LH;
+    const float2* XP2 = reinterpret_cast<const float2*>(smem_raw + pb) + (size_t)q * LL * LL;  // XS = 2
     float2* Wq = Wk + (size_t)q * LL * WS;
     float2* Uq = Acc + (size_t)(2 * q) * LL * LH;
     float2* Vq = Uq + (size_t)LL * LH;
@@ -492,8 +494,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                             const int o = sk1 * LH + sk2;
                             const float2 yv = v[k1];
                             if constexpr (XS == 2) {
-                                const float4 cf = XP[k1 * LL + idx];  // (a, c, b, d), lane-contiguous: ideal wavefronts
-                                v[k1] = px::fma(px::bc(yv.x), make_float2(cf.x, cf.y), px::mul(px::bc(yv.y), make_float2(cf.z, cf.w)));
+                                // (A, B), lane-contiguous; Y.y (b, d) = (-g Y.y) (-B, A): the pair as the first operand makes
+                                // (-B, A) a free FFMA2 operand modifier (half the table of the (a, c, b, d) form: 8 B per bin)
+                                const float2 cf = XP2[k1 * LL + idx];
+                                v[k1] = px::fma(cf, px::bc(yv.x), px::mul(make_float2(-cf.y, cf.x), px::bc(-sgn * yv.y)));
                             } else {
                                 const float4 xv = XS ? XP[o] : __ldg(XP + o);
                                 const float2 A = cmul_conj(yv, make_float2(xv.x, xv.y));
