@@ -127,7 +127,7 @@ __device__ __forceinline__ void dit_x1(float2 (&v)[64], bool hb, float sh) {
     constexpr float c0 = (float)cos2pi(J, 128), s0 = (float)(SIGN * sin2pi(J, 128));
     constexpr float c1 = (float)cos2pi(J + 32, 128), s1 = (float)(SIGN * sin2pi(J + 32, 128));
     float2 a = v[J], b = v[J + 32];
-    // (scalar: the packed FP32x2 form of this stage measured slower twice: 31.7 vs 30.3 ms, 24.1 vs 23.4 ms)
+#ifdef SRMRA_FFT128_X_SCALAR
     if (hb) {
         a = make_float2(fmaf(a.x, c0, -a.y * s0), fmaf(a.x, s0, a.y * c0));
         b = make_float2(fmaf(b.x, c1, -b.y * s1), fmaf(b.x, s1, b.y * c1));
@@ -136,6 +136,17 @@ __device__ __forceinline__ void dit_x1(float2 (&v)[64], bool hb, float sh) {
     const float2 rcv = shfl_pair(snd);
     v[J] = make_float2(own.x + rcv.x, own.y + rcv.y);
     v[J + 32] = make_float2(sh * (own.x - rcv.x), sh * (own.y - rcv.y));
+#else
+    // packed: a w = c a + s (i a) with scalar immediates and (-a.y, a.x) a free operand modifier (pair first)
+    if (hb) {
+        a = px::fma(make_float2(-a.y, a.x), px::bc(s0), px::mul(a, px::bc(c0)));
+        b = px::fma(make_float2(-b.y, b.x), px::bc(s1), px::mul(b, px::bc(c1)));
+    }
+    const float2 own = hb ? b : a, snd = hb ? a : b;
+    const float2 rcv = shfl_pair(snd);
+    v[J] = px::add(own, rcv);
+    v[J + 32] = px::mul(px::sub(own, rcv), px::bc(sh));
+#endif
 }
 template <int SIGN, int... Js>
 __device__ __forceinline__ void dit_xall(float2 (&v)[64], bool hb, float sh, std::integer_sequence<int, Js...>) {
@@ -148,9 +159,15 @@ template <int SIGN, int J>
 __device__ __forceinline__ void dif_x1(float2 (&v)[64], bool hb) {
     constexpr float c = (float)cos2pi(J, 128), s = (float)(SIGN * sin2pi(J, 128));
     const float2 x0 = v[J], x1 = v[J + 32];
+#ifdef SRMRA_FFT128_X_SCALAR
     const float2 a = make_float2(x0.x + x1.x, x0.y + x1.y);
     const float2 d = make_float2(x0.x - x1.x, x0.y - x1.y);
     float2 b = make_float2(fmaf(d.x, c, -d.y * s), fmaf(d.x, s, d.y * c));
+#else
+    const float2 a = px::add(x0, x1);
+    const float2 d = px::sub(x0, x1);
+    float2 b = px::fma(make_float2(-d.y, d.x), px::bc(s), px::mul(d, px::bc(c)));
+#endif
     if (hb) b = SIGN > 0 ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);  // w^32 = SIGN i
     const float2 own = hb ? b : a, snd = hb ? a : b;
     const float2 rcv = shfl_pair(snd);
