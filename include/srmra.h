@@ -128,6 +128,17 @@ SRMRA_API int srmra_init(srmra_ctx** out, const float* y, int32_t n_local, int32
 SRMRA_API int srmra_load(srmra_ctx* ctx, const float* y, const float* x0, const double* rho1_0,
                const double* rho2_0);
 
+/* srmra_load followed by n_iters EM iterations (Algorithm 2's EM steps; eq:weights_EM,
+ * eq:x_EM, eq:rho_EM), with the upload overlapped: on the FFT path with one rank and no
+ * denoiser hook, the first iteration's E-step / M-step runs per observation range as soon as that range's
+ * host->device copy has landed, while the next range is still being copied (pass y in pinned host memory for
+ * an asynchronous copy).  Arguments and errors as srmra_load and srmra_em_iter; synchronous (returns after the
+ * first iteration, with the later n_iters - 1 enqueued).  The result equals srmra_load + srmra_em_iter(n_iters)
+ * up to the float32 rounding of the per-CTA partial sums (the partials are grouped by range).  Other paths /
+ * world > 1 / a denoiser hook: exactly srmra_load + srmra_em_iter(n_iters). */
+SRMRA_API int srmra_load_iterate(srmra_ctx* ctx, const float* y, const float* x0, const double* rho1_0,
+               const double* rho2_0, int32_t n_iters);
+
 /*
  * NEXT-4 device data generator: like srmra_load, but the n_local observations are drawn on the GPU from
  * the model of PAPER.md:37-38 (eq:model_1), y_j[n1, n2] = x[(n1 K - s^1) mod L_high, (n2 K - s^2) mod

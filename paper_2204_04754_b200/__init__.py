@@ -30,7 +30,7 @@ PATH_NAMES = {PATH_AUTO: "auto", PATH_GEMM: "gemm", PATH_FFT: "fft", PATH_DIRECT
 PATH_IDS = {v: k for k, v in PATH_NAMES.items()}
 
 # every symbol include/srmra.h declares (checked by tests/test_abi.py)
-ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_em_iter", "srmra_get_estimate",
+ABI_SYMBOLS = ("srmra_default_options", "srmra_init", "srmra_load", "srmra_load_iterate", "srmra_em_iter", "srmra_get_estimate",
                "srmra_get_loglik_trace", "srmra_get_stats", "srmra_get_obs_loglik", "srmra_local_stats",
                "srmra_get_path", "srmra_launches_per_iter", "srmra_profile", "srmra_profile_read", "srmra_debug_timestamps",
                "srmra_nccl_unique_id", "srmra_free",
@@ -77,6 +77,7 @@ def _load():
         "srmra_init": (ctypes.c_int, [ctypes.POINTER(_ctxp), _fp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, ctypes.c_double, _fp, _dp, _dp, ctypes.POINTER(srmra_options)]),
         "srmra_load": (ctypes.c_int, [_ctxp, _fp, _fp, _dp, _dp]),
+        "srmra_load_iterate": (ctypes.c_int, [_ctxp, _fp, _fp, _dp, _dp, ctypes.c_int32]),
         "srmra_em_iter": (ctypes.c_int, [_ctxp, ctypes.c_int32]),
         "srmra_get_estimate": (ctypes.c_int, [_ctxp, _fp, _dp, _dp, _dp, _ip]),
         "srmra_get_loglik_trace": (ctypes.c_int, [_ctxp, _dp, ctypes.c_int32, _ip]),
@@ -164,6 +165,13 @@ def srmra_load(ctx, y, x0, rho1_0, rho2_0):
     _check(_lib.srmra_load(ctx, _ptr(y, _fp), _ptr(np.ascontiguousarray(x0, dtype=np.float32), _fp),
                            _ptr(np.ascontiguousarray(rho1_0, dtype=np.float64), _dp),
                            _ptr(np.ascontiguousarray(rho2_0, dtype=np.float64), _dp)), ctx)
+
+
+def srmra_load_iterate(ctx, y, x0, rho1_0, rho2_0, n_iters: int):
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    _check(_lib.srmra_load_iterate(ctx, _ptr(y, _fp), _ptr(np.ascontiguousarray(x0, dtype=np.float32), _fp),
+                                   _ptr(np.ascontiguousarray(rho1_0, dtype=np.float64), _dp),
+                                   _ptr(np.ascontiguousarray(rho2_0, dtype=np.float64), _dp), int(n_iters)), ctx)
 
 
 def srmra_generate(ctx, x_true, rho1_true, rho2_true, seed: int, first_index: int, x0, rho1_0, rho2_0,
@@ -396,6 +404,13 @@ class Context:
             raise ValueError(f"srmra_load: y must hold n_local = {self.n_local} observations of "
                              f"{self.L_low} x {self.L_low}")
         srmra_load(self.handle, y, x0, rho1_0, rho2_0)
+
+    def load_iterate(self, y, x0, rho1_0, rho2_0, n_iters=1):
+        """load + n_iters iterations, the first one overlapped with the upload (srmra_load_iterate)."""
+        if np.asarray(y).size != self.n_local * self.L_low * self.L_low:
+            raise ValueError(f"srmra_load_iterate: y must hold n_local = {self.n_local} observations of "
+                             f"{self.L_low} x {self.L_low}")
+        srmra_load_iterate(self.handle, y, x0, rho1_0, rho2_0, n_iters)
 
     def em_iter(self, n_iters=1):
         srmra_em_iter(self.handle, n_iters)

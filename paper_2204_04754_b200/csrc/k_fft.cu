@@ -888,12 +888,13 @@ static cudaError_t plan_em_t(srmra_ctx* c) {
 template <int LL>
 static cudaError_t launch_em_t(srmra_ctx* c) {
     EmArgs a;
-    a.yhat = c->d_yhat;
-    a.ynorm = c->d_ynorm;
+    const int64_t off = c->em_n >= 0 ? c->em_off : 0;  // srmra_load_iterate: one observation range
+    a.yhat = c->d_yhat + off * ystride_of(LL);
+    a.ynorm = c->d_ynorm + off;
     a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
-    a.n = c->n_local;
+    a.n = c->em_n >= 0 ? c->em_n : c->n_local;
     a.L = c->L;
     a.K = c->K;
     a.KK = c->KK;
@@ -903,9 +904,9 @@ static cudaError_t launch_em_t(srmra_ctx* c) {
     a.c2 = (float)(1.4426950408889634074 * c->inv_s2);
     a.inv_s2 = c->inv_s2;
     a.inv_2s2 = c->inv_2s2;
-    a.part = c->d_part;
-    a.llpart = c->d_llpart;
-    a.llobs = c->d_llobs;
+    a.part = c->em_n >= 0 ? c->em_part : c->d_part;
+    a.llpart = c->em_n >= 0 ? c->em_llpart : c->d_llpart;
+    a.llobs = c->d_llobs ? c->d_llobs + off : nullptr;
     a.tmem_cols = c->fft_tmem_cols;
     a.run = c->d_run;
     a.emt = c->d_emt;

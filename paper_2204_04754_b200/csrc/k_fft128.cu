@@ -703,14 +703,15 @@ cudaError_t fft128_plan(srmra_ctx* c) {
 
 cudaError_t launch_fft_em128(srmra_ctx* c) {
     Em128Args a;
-    a.yhat = c->d_yhat;
-    a.ynorm = c->d_ynorm;
-    a.ysum = c->d_ysum;
+    const int64_t off = c->em_n >= 0 ? c->em_off : 0;  // srmra_load_iterate: one observation range
+    a.yhat = c->d_yhat + off * (LL * YR);
+    a.ynorm = c->d_ynorm + off;
+    a.ysum = c->d_ysum + off;
     a.xhat = reinterpret_cast<const float4*>(c->d_xhat);
     a.coef = reinterpret_cast<const float2*>(c->d_xcoef);
     a.par32 = c->par.f32;
     a.par64 = c->par.f64;
-    a.n = c->n_local;
+    a.n = c->em_n >= 0 ? c->em_n : c->n_local;
     a.L = c->L;
     a.K = c->K;
     a.KK = c->KK;
@@ -724,9 +725,9 @@ cudaError_t launch_fft_em128(srmra_ctx* c) {
     a.c2 = (float)(1.4426950408889634074 * c->inv_s2);
     a.c2d = 1.4426950408889634074 * c->inv_s2;
     a.inv_2s2 = c->inv_2s2;
-    a.part = c->d_part;
-    a.llpart = c->d_llpart;
-    a.llobs = c->d_llobs;
+    a.part = c->em_n >= 0 ? c->em_part : c->d_part;
+    a.llpart = c->em_n >= 0 ? c->em_llpart : c->d_llpart;
+    a.llobs = c->d_llobs ? c->d_llobs + off : nullptr;
     a.run = c->d_run;
     a.emt = c->d_emt;
     a.iter = c->d_iter;

@@ -633,9 +633,9 @@ cudaError_t launch_fft_tail(srmra_ctx* c, int mode) {
     a.trace_cap = c->opt.trace_cap;
     a.tau = c->tau;
     a.inv_2s2 = c->inv_2s2;
-    a.part = c->d_part;
-    a.llpart = c->d_llpart;
-    a.nparts = c->n_local > 0 ? c->fft_grid : 0;
+    a.part = c->tail_nparts ? c->tail_part : c->d_part;
+    a.llpart = c->tail_nparts ? c->tail_llpart : c->d_llpart;
+    a.nparts = c->n_local > 0 ? (c->tail_nparts ? c->tail_nparts : c->fft_grid) : 0;
     a.PB = fft_partial_bins(c->KK, Ll);
     a.acc = c->d_bhat;
     a.tw = c->d_tw;

@@ -252,6 +252,95 @@ int upload(srmra_ctx* c, const float* y, const float* x0, const std::vector<doub
     return SRMRA_OK;
 }
 
+// srmra_load_iterate on the FFT path (one rank, built-in projection): upload y and theta_0 and run the first EM iteration
+// with its E/M step split over `stream_chunks` observation ranges — range j's E/M kernel starts as soon as its chunked
+// host->device copies and init kernels are done, while range j+1 is still in flight on the copy stream.  Each range
+// writes its own per-CTA partial slots; the tail then reduces all of them in its fixed order (the same float64 sums,
+// grouped by range).  Same result as upload + one iteration up to the float32 rounding of the per-CTA partials.
+int upload_streamed(srmra_ctx* c, const float* y, const float* x0, const std::vector<double>& r1,
+                    const std::vector<double>& r2) {
+    const int S = c->stream_chunks > 0 ? c->stream_chunks : 8;
+    const int PB = fft_partial_bins(c->KK, c->Ll);
+    const size_t slots = (size_t)S * c->fft_grid;
+    if (!c->d_part_s || c->stream_chunks != S) {
+        if (c->d_part_s) cudaFree(c->d_part_s);
+        if (c->d_llpart_s) cudaFree(c->d_llpart_s);
+        c->d_part_s = nullptr;
+        c->d_llpart_s = nullptr;
+        if (dalloc(&c->d_part_s, slots * PB) != cudaSuccess || dalloc(&c->d_llpart_s, slots) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, SRMRA_ERR_OOM, "srmra_load_iterate: partial slots");
+        }
+        c->stream_chunks = S;
+    }
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    std::vector<double> x64(c->L2), rho(2 * c->L);
+    for (int k = 0; k < c->L2; ++k) x64[k] = (double)x0[k];
+    for (int k = 0; k < c->L; ++k) { rho[k] = r1[k]; rho[c->L + k] = r2[k]; }
+    CK(cudaMemcpyAsync(c->d_x64, x64.data(), sizeof(double) * c->L2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_x32, x0, sizeof(float) * c->L2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_rho, rho.data(), sizeof(double) * 2 * c->L, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+    c->joint = false;
+    {
+        const int rcj = fft_joint_mode(c, false);
+        if (rcj != SRMRA_OK) return rcj;
+    }
+    CK(cudaMemsetAsync(c->d_run, 0, 2 * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->d_rtol, 0, sizeof(double), c->stream));
+    c->n_proj = 0;
+    CK(launch_fft_tail(c, TAIL_PREP));  // Xhat and logit bias of theta_0, before the first range's E/M kernel
+    static const int64_t chunk_bytes = [] {
+        const char* e = getenv("SRMRA_H2D_CHUNK_MB");
+        const int64_t mb = e ? atoll(e) : 4;
+        return (mb > 0 ? mb : 4) << 20;
+    }();
+    const int64_t per = std::max<int64_t>(1, chunk_bytes / (int64_t)(sizeof(float) * c->Ll2));
+    const int64_t range = (c->n_local + S - 1) / S;
+    for (int j = 0; j < S; ++j) {
+        const int64_t r0 = j * range, r1e = std::min<int64_t>(c->n_local, r0 + range);
+        float2* part = c->d_part_s + (size_t)j * c->fft_grid * PB;
+        double* llp = c->d_llpart_s + (size_t)j * c->fft_grid;
+        for (int64_t o = r0; o < r1e; o += per) {
+            const int64_t m = std::min<int64_t>(per, r1e - o);
+            CK(cudaMemcpyAsync(c->d_y + o * c->Ll2, y + o * c->Ll2, sizeof(float) * m * c->Ll2, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+            CK(cudaEventRecord(c->copy_event, c->copy_stream));
+            CK(cudaStreamWaitEvent(c->stream, c->copy_event, 0));
+            CK(launch_init_obs(c, o, m));
+            CK(launch_fft_init(c, o, m));
+        }
+        c->em_off = r0;
+        c->em_n = std::max<int64_t>(0, r1e - r0);
+        c->em_part = part;
+        c->em_llpart = llp;
+        const cudaError_t e = c->em_n > 0 ? launch_fft_em(c) : cudaSuccess;
+        c->em_n = -1;
+        if (e != cudaSuccess) return cuda_fail(c, e, "launch_fft_em (range)");
+        if (r1e <= r0) {  // an empty range still owns slots the tail reads
+            CK(cudaMemsetAsync(part, 0, sizeof(float2) * (size_t)c->fft_grid * PB, c->stream));
+            CK(cudaMemsetAsync(llp, 0, sizeof(double) * c->fft_grid, c->stream));
+        }
+    }
+    c->tail_part = c->d_part_s;
+    c->tail_llpart = c->d_llpart_s;
+    c->tail_nparts = (int)slots;
+    const cudaError_t et = launch_fft_tail(c, TAIL_REDUCE | TAIL_FOLD | TAIL_FINALIZE | TAIL_PREP);
+    c->tail_nparts = 0;
+    if (et != cudaSuccess) return cuda_fail(c, et, "launch_fft_tail (streamed)");
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    SYNC();
+    c->iters_done = 1;
+    if (flag & 2) {
+        c->needs_load = true;
+        CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        return fail(c, SRMRA_ERR_INVALID_ARG, "y not finite");
+    }
+    c->needs_load = false;
+    return SRMRA_OK;
+}
+
 // Sum a device float64 buffer over all ranks on the context stream: the options' exchange provider if
 // one is set, else ncclAllReduce (no-op for world 1).
 int exchange(srmra_ctx* c, double* buf, size_t n) {
@@ -713,6 +802,30 @@ int srmra_load(srmra_ctx* c, const float* y, const float* x0, const double* rho1
     return upload(c, y, x0, r1, r2);
 }
 
+int srmra_load_iterate(srmra_ctx* c, const float* y, const float* x0, const double* rho1_0, const double* rho2_0,
+                       int32_t n_iters) {
+    DevGuard dg_(c);
+    if (!c) return fail(nullptr, SRMRA_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->failed) return SRMRA_ERR_STATE;
+    if (n_iters < 0) return fail(c, SRMRA_ERR_INVALID_ARG, "n_iters < 0");
+    if (!x0 || !rho1_0 || !rho2_0 || (c->n_local > 0 && !y)) return fail(c, SRMRA_ERR_INVALID_ARG, "NULL input");
+    if (!all_finite_f(x0, (size_t)c->L2)) return fail(c, SRMRA_ERR_INVALID_ARG, "x0 not finite");
+    std::vector<double> r1, r2;
+    if (check_rho(rho1_0, c->L, r1) || check_rho(rho2_0, c->L, r2))
+        return fail(c, SRMRA_ERR_INVALID_ARG, "rho must be >= 0, finite and sum to 1 (within 1e-6)");
+    // the streamed first iteration: FFT path, one rank, the built-in projection (a denoiser hook or a host exchange
+    // needs the host loop around every iteration)
+    const bool streamed = n_iters > 0 && c->path == SRMRA_PATH_FFT && c->copy_stream && c->n_local > 0 &&
+                          c->opt.world == 1 && !c->denoiser;
+    int rc;
+    if (!streamed) {
+        if ((rc = upload(c, y, x0, r1, r2)) != SRMRA_OK) return rc;
+        return n_iters > 0 ? iterate(c, n_iters, 0.0) : SRMRA_OK;
+    }
+    if ((rc = upload_streamed(c, y, x0, r1, r2)) != SRMRA_OK) return rc;
+    return n_iters > 1 ? iterate(c, n_iters - 1, 0.0) : SRMRA_OK;
+}
+
 int srmra_generate(srmra_ctx* c, const float* x_true, const double* rho1_true, const double* rho2_true, uint64_t seed,
                    int64_t first_index, const float* x0, const double* rho1_0, const double* rho2_0,
                    int32_t* shifts_out) {
@@ -1134,7 +1247,7 @@ void srmra_free(srmra_ctx* c) {
     }
     void* bufs[] = {c->d_y, c->d_yhat, c->d_ysum, c->d_ynorm, c->d_llobs, c->d_x64, c->d_x32, c->d_xtmp, c->d_rho,
                     c->par.f32, c->par.f64, c->d_xhat, c->d_xcoef, c->d_bhat, c->d_pack, c->d_trace, c->d_flag,
-                    c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps};
+                    c->d_part, c->d_llpart, c->d_tw, c->d_counter, c->d_stamps, c->d_part_s, c->d_llpart_s};
     for (void* p : bufs)
         if (p) cudaFree(p);
     gemm_free(c);

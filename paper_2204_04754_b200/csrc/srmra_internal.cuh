@@ -84,6 +84,18 @@ struct srmra_ctx {
     float* d_jpart = nullptr;   // NEXT-3, FFT path: per-CTA posterior mass per shift [fft_part_cap][KK Ll^2]
     double* d_jacc = nullptr;   // NEXT-3, FFT path: its fixed-order float64 sum [KK Ll^2]
     int fft_tmem_cols = 0;      // tensor-memory columns per CTA (fft_tacc)
+    // srmra_load_iterate (FFT path): the first iteration's E/M kernel runs per observation range as the range lands;
+    // em_* select that range and its partial slots for launch_fft_em (em_n < 0: all observations, d_part / d_llpart),
+    // tail_* the partial slots the tail reduces (tail_nparts 0: fft_grid slots of d_part / d_llpart)
+    int64_t em_off = 0, em_n = -1;
+    float2* em_part = nullptr;
+    double* em_llpart = nullptr;
+    float2* tail_part = nullptr;
+    double* tail_llpart = nullptr;
+    int tail_nparts = 0;
+    float2* d_part_s = nullptr;   // [stream_chunks][fft_grid][PB] partial slots of the streamed first iteration
+    double* d_llpart_s = nullptr; // [stream_chunks][fft_grid]
+    int stream_chunks = 0;
     size_t fft_smem = 0;
     double* d_pack = nullptr;   // packed statistics, see PackLayout
     srmra::PackLayout pk{};
@@ -169,6 +181,7 @@ bool direct_supported(int L, int Ll, int K);
 cudaError_t launch_fft_em(srmra_ctx* c);        // k_fft.cu
 bool fft_supported(int L, int Ll, int K);
 cudaError_t launch_fft_init(srmra_ctx* c, int64_t first, int64_t count);  // Yhat_i, sum y_i
+int fft_partial_bins(int KK, int Ll);  // per-CTA partial bins of the FFT E/M kernels (k_fft.cu)
 // tcgen05 3xTF32 GEMM path (k_gemm.cu)
 bool gemm_supported(int L, int Ll, int K);
 size_t gemm_bytes(const srmra_ctx* c);

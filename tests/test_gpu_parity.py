@@ -309,3 +309,42 @@ def test_torch_stream(srm):
         ctx.em_iter(2)
         x, *_ = ctx.get_estimate()
     assert np.all(np.isfinite(x))
+
+
+@pytest.mark.parametrize("name,N,iters", [("c1", 1000, 3), ("c3", 700, 1), ("c4", 24, 1), ("c0", 500, 2)])
+def test_load_iterate_streamed_first_iteration(srm, oracle_mod, name, N, iters):
+    """srmra_load_iterate: the first iteration's E/M step runs per observation range while the next range is
+    still being copied (8 ranges, each with its own partial slots).  Against the oracle element by element
+    (eq:weights_EM / eq:x_EM / eq:rho_EM) and against srmra_load + srmra_em_iter on the same
+    context type (the partials are grouped differently, so up to their float32 rounding)."""
+    p = synth.make_config(name, N=N)
+    x, r1, r2, trace = oracle_mod.run(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, iters=iters, proj_every=1)
+    other = synth.make_config(name, N=N, seed_offset=7)
+    with srm.Context(other.y, p.L_high, p.L_low, p.K, p.sigma, other.x0, other.rho1_0, other.rho2_0,
+                     path="fft") as ctx:
+        ctx.em_iter(1)  # a context that has already iterated on other data
+        ctx.load_iterate(p.y, p.x0, p.rho1_0, p.rho2_0, iters)
+        gx, g1, g2, gll, it = ctx.get_estimate()
+        assert it == iters
+        gtrace = ctx.loglik_trace()
+        llo = ctx.obs_loglik()
+    assert_close(dict(x=gx, rho1=g1, rho2=g2, trace=gtrace, path="fft/streamed"), x, r1, r2, trace,
+                 tag=f"{name}/N={N} load_iterate")
+    g = run_gpu(srm, p, "fft", iters)
+    np.testing.assert_allclose(gx, g["x"], rtol=0, atol=2e-5 * np.abs(g["x"]).max())
+    np.testing.assert_allclose(gtrace[0], g["trace"][0], rtol=1e-12)  # LL_0 depends on theta_0 only
+    np.testing.assert_allclose(gtrace, g["trace"], rtol=1e-6)
+    if iters == 1:
+        np.testing.assert_allclose(llo, g["llo"], rtol=1e-9)  # per-observation LL_i land in their own slots
+
+
+def test_load_iterate_falls_back_without_fft(srm, oracle_mod):
+    """Other paths: srmra_load_iterate is exactly srmra_load + srmra_em_iter."""
+    p = synth.make_config("c0")
+    x, r1, r2, trace = oracle_mod.run(p.y, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, iters=2, proj_every=1)
+    with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path="direct") as ctx:
+        ctx.load_iterate(p.y, p.x0, p.rho1_0, p.rho2_0, 2)
+        gx, g1, g2, gll, it = ctx.get_estimate()
+        assert it == 2
+        gtrace = ctx.loglik_trace()
+    assert_close(dict(x=gx, rho1=g1, rho2=g2, trace=gtrace, path="direct"), x, r1, r2, trace, tag="c0 direct")
