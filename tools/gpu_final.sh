@@ -12,8 +12,13 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 for c in c3 c1 c4; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches_${c}_$T.csv python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > /dev/null 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fft_em -s 3 -c 1 -o gpurun_out/prof_c3_$T python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fft_em -s 3 -c 1 -o gpurun_out/prof_c1_$T python bench.py --config c1 --steps 5 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fft_em128 -s 1 -c 1 -o gpurun_out/prof_c4_$T python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > /dev/null 2>&1
+prof() {  # $1 = config, $2 = kernel regex, $3 = launches to skip; text summaries only (the reports exceed gpurun's 64 MiB)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o gpurun_out/prof_$1_$T python bench.py --config $1 --steps 3 --warmup 3 --no-cpu-baseline --e2e-jobs 0 > /dev/null 2>&1
+  { python profiles/ncu_summary.py gpurun_out/prof_$1_$T.ncu-rep; echo; python tools/sass_dyn.py gpurun_out/prof_$1_$T.ncu-rep 30; echo; python tools/ncu_lines.py gpurun_out/prof_$1_$T.ncu-rep 25; } > gpurun_out/ncu_$1_$T.txt 2>&1
+  rm -f gpurun_out/prof_$1_$T.ncu-rep
+}
+prof c3 "k_fft_em" 3
+prof c1 "k_fft_em" 3
+prof c4 "k_fft_em128" 1
 for c in c1 c3 c4; do python tools/gap_stamps.py $c 2>&1 | tail -4; done > gpurun_out/gaps_$T.log
 cat gpurun_out/smoke_$T.log; tail -3 gpurun_out/pytest_$T.log; tail -1 gpurun_out/bench_c3_$T.log; tail -1 gpurun_out/bench_ref_$T.log
