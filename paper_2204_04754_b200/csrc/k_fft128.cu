@@ -282,7 +282,15 @@ __global__ void k_fft128_coef(const float4* __restrict__ xhat, int NP, float2* _
         const double A = fl ? ax - by : ax + by, B = fl ? -ay - bx : ay - bx;
         const float2 hi = make_float2((float)A, (float)B);
         coef[k] = hi;
+#ifndef SRMRA_FFT128_LO_F32
+        // lo plane as bfloat16 pairs (round to nearest): |lo| <= 2^-24 |A|, kept to 2^-9 of itself, i.e. the
+        // coefficients to ~2^-33 instead of float32's 2^-24 (the systematic error of DESIGN 6.5 scales with it)
+        const unsigned lo_a = __float_as_uint((float)(A - hi.x)), lo_b = __float_as_uint((float)(B - hi.y));
+        const unsigned ra = (lo_a + 0x7fffu + ((lo_a >> 16) & 1u)) >> 16, rb = (lo_b + 0x7fffu + ((lo_b >> 16) & 1u)) >> 16;
+        reinterpret_cast<unsigned*>(coef + total)[k] = (rb << 16) | (ra & 0xffffu);
+#else
         coef[(size_t)total + k] = make_float2((float)(A - hi.x), (float)(B - hi.y));
+#endif
     }
 }
 
@@ -364,7 +372,8 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     const float4* XP = a.xhat + (size_t)q * LL * LH;
     const float4* XPL = XP + (size_t)NP * LL * LH;  // lo plane
     const float2* CH = a.coef + (size_t)q * LL * LL + l;            // COEF: hi coefficients of column l
-    const float2* CL = CH + (size_t)NP * LL * LL;                   // lo
+    const float2* CL = CH + (size_t)NP * LL * LL;                   // lo (float32 pairs, SRMRA_FFT128_LO_F32)
+    const unsigned* CLB = reinterpret_cast<const unsigned*>(a.coef + (size_t)NP * LL * LL) + (size_t)q * LL * LL + l;  // lo (bf16 pairs)
     const float ysg = flip ? 1.f : -1.f;                            // -Y.y = ysg * (stored Y).y
     const float* lr1 = pars;
     const float* lr2 = pars + L;
@@ -436,7 +445,13 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 for (int m = 0; m < 64; ++m) {
                     const int k1 = 2 * m + h;
                     const float2 yv = v[m];
+#ifndef SRMRA_FFT128_LO_F32
+                    const float2 ch = __ldg(CH + k1 * LL);
+                    const unsigned lw = __ldg(CLB + k1 * LL);
+                    const float2 cl = make_float2(__uint_as_float(lw << 16), __uint_as_float(lw & 0xffff0000u));
+#else
                     const float2 ch = __ldg(CH + k1 * LL), cl = __ldg(CL + k1 * LL);
+#endif
                     const float ny = ysg * yv.y;  // -Y.y of the true spectrum value
                     // v = Y.x (A, B) + (-Y.y) (-B, A), lo part first; the pair is the first operand (its swapped,
                     // half-negated form is then an operand modifier)
