@@ -470,7 +470,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                     const int sk2 = flip ? LL - k2 : k2;
                     const float sgn = flip ? -1.f : 1.f;
                     // all of this column's Yhat reads first (LL loads in flight), the TMEM stash, then the
-                    // products in place
+                    // products in place; at LL <= 32 with the XS = 2 table its coefficient reads are issued first too
+                    constexpr bool CF_FIRST = XS == 2 && LL <= 32;
+                    float2 cfv[CF_FIRST ? LL : 1];
+                    if constexpr (CF_FIRST) {
+#pragma unroll
+                        for (int k1 = 0; k1 < LL; ++k1) cfv[k1] = XP2[k1 * LL + idx];
+                    }
 #pragma unroll
                     for (int k1 = 0; k1 < LL; ++k1) v[k1] = Y[ybase + k1 * ystep];
                     if constexpr (TACC) {
@@ -496,7 +502,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                             if constexpr (XS == 2) {
                                 // (A, B), lane-contiguous; Y.y (b, d) = (-g Y.y) (-B, A): the pair as the first operand makes
                                 // (-B, A) a free FFMA2 operand modifier (half the table of the (a, c, b, d) form: 8 B per bin)
-                                const float2 cf = XP2[k1 * LL + idx];
+                                float2 cf;
+                                if constexpr (CF_FIRST) cf = cfv[k1];
+                                else cf = XP2[k1 * LL + idx];
                                 v[k1] = px::fma(cf, px::bc(yv.x), px::mul(make_float2(-cf.y, cf.x), px::bc(-sgn * yv.y)));
                             } else {
                                 const float4 xv = XS ? XP[o] : __ldg(XP + o);
