@@ -151,11 +151,28 @@ __host__ __device__ inline size_t joint_bytes(int KK) {
 // shared memory, which leaves room for more groups (warps) per SM.  Group shared memory then holds
 // Yb [2][ystride] | Wk [NP][LL][WS] | zc [NP][2][LL] | yc [NP][2][LL] | red [32]; at the end the group's
 // partial (layout part_bins) is staged over Yb / Wk.
+// OVL (TACC without the joint prior): the softmax reduction is split around the M-row transform — each warp
+// publishes its (s, m, z) summary with an mbarrier arrive, transforms its rows of unnormalised weights, and
+// only then waits and scales the transformed rows (the transform is linear), so the cross-warp wait overlaps
+// the pass-2 FFT instead of idling at a barrier.  Yhat then needs a ring of three staged buffers: the
+// prefetch of observation j + 1 is issued at the start of observation j into the buffer of j - 2, whose last
+// reader (the deferred vex_update in j - 1's pass 0) is ordered by j - 1's pass-2 group barrier.
+// L_low = 32 only: measured c3 3.342 -> 3.198 ms, c1 83.4 -> 83.1 us; at L_low = 64 (c2) the third buffer
+// (17 KB per group) costs a group, 0.832 -> 1.045 ms.
+// SRMRA_FFT_NO_OVL builds the previous form (reduction barrier before the transform) for A/B.
+template <int LL, bool TACC, bool JOINT>
+__host__ __device__ constexpr bool ovl_mode() {
+#ifdef SRMRA_FFT_NO_OVL
+    return false;
+#else
+    return LL == 32 && TACC && !JOINT;
+#endif
+}
 template <int LL>
-__host__ __device__ inline size_t group_smem_t(int KK, int ystride) {
+__host__ __device__ inline size_t group_smem_t(int KK, int ystride, int nybuf = 2) {
     using G = Geo<LL>;
     const int NP = (KK + 1) / 2;
-    size_t b = sizeof(float2) * (2 * (size_t)ystride + (size_t)NP * LL * G::WS + 4 * (size_t)NP * LL) +
+    size_t b = sizeof(float2) * ((size_t)nybuf * ystride + (size_t)NP * LL * G::WS + 4 * (size_t)NP * LL) +
                sizeof(double) * 32;
     return (b + 15) & ~(size_t)15;
 }
@@ -217,8 +234,9 @@ __device__ __forceinline__ void smz_combine(float& s, float& m, float& z, float 
     s = keep ? s : s2;
     m = keep ? m : m2;
 }
-__device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, float c2, float4* scratch, int gwarp,
-                                                 int nwarps, int pw, int lane, int bar_id, int gthreads) {
+__device__ __forceinline__ void smz_cross(float& s, float& m, float& z, float c2, const float4* scratch, int nwarps,
+                                          int pw, int lane);
+__device__ __forceinline__ void smz_warp(float& s, float& m, float& z, float c2) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
@@ -226,12 +244,24 @@ __device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, f
         const float z2 = __shfl_xor_sync(0xffffffffu, z, o);
         smz_combine(s, m, z, s2, m2, z2, c2);
     }
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t saddr) {  // release.cta: orders this thread's prior stores
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr) : "memory");
+}
+__device__ __forceinline__ void group_reduce_smz(float& s, float& m, float& z, float c2, float4* scratch, int gwarp,
+                                                 int nwarps, int pw, int lane, int bar_id, int gthreads) {
+    smz_warp(s, m, z, c2);
     if (nwarps == 1) return;
     if (lane == 0) scratch[gwarp] = make_float4(s, m, z, 0.f);
     group_bar(bar_id, gthreads);
-    // lane j takes warp (j mod pw)'s summary (pw = nwarps rounded up to a power of two, missing warps empty);
-    // a log2(pw)-deep shuffle tree then leaves the group result in every block of pw lanes, i.e. in every
-    // lane — instead of a serial walk over the warps
+    smz_cross(s, m, z, c2, scratch, nwarps, pw, lane);
+}
+// the cross-warp half of group_reduce_smz, once every warp's summary is in scratch:
+// lane j takes warp (j mod pw)'s summary (pw = nwarps rounded up to a power of two, missing warps empty);
+// a log2(pw)-deep shuffle tree then leaves the group result in every block of pw lanes, i.e. in every
+// lane — instead of a serial walk over the warps
+__device__ __forceinline__ void smz_cross(float& s, float& m, float& z, float c2, const float4* scratch, int nwarps,
+                                          int pw, int lane) {
     const int wj = lane & (pw - 1);
     const float4 e = wj < nwarps ? scratch[wj] : make_float4(0.f, -INFINITY, 0.f, 0.f);
     s = e.x;
@@ -333,15 +363,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
     if (TACC) tc::fence_before();
     __syncthreads();
     if (TACC) tc::fence_after();
-    const size_t per_g = TACC ? group_smem_t<LL>(KK, a.ybuf) : group_smem<LL>(KK, a.ybuf);
+    constexpr bool OVL = ovl_mode<LL, TACC, JOINT>();
+    constexpr int NYB = OVL ? 3 : 2;  // staged Yhat buffers
+    const size_t per_g = TACC ? group_smem_t<LL>(KK, a.ybuf, NYB) : group_smem<LL>(KK, a.ybuf);
     const int PB = part_bins(KK, LL);
     float* JA = reinterpret_cast<float*>(gbase + per_g * a.groups);  // JOINT accumulator (after the groups)
     if (JOINT) {
         for (int k = threadIdx.x; k < KK * LL * (LL + 1); k += blockDim.x) JA[k] = 0.f;
         __syncthreads();
     }
-    float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [2][ybuf]
-    float2* Wk = Yb + 2 * a.ybuf;                                       // [NP][LL][WS]
+    float2* Yb = reinterpret_cast<float2*>(gbase + per_g * g);          // [NYB][ybuf]
+    float2* Wk = Yb + NYB * a.ybuf;                                     // [NP][LL][WS]
     // TACC: zc | yc | red after Wk, the partial staged over Yb (at the end); else Acc [PB] | red
     float2* Acc = TACC ? Yb : Wk + (size_t)NP * LL * WS;
     float2* zc = Wk + (size_t)NP * LL * WS;                             // [NP][2][LL] (TACC)
@@ -426,6 +458,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
     const int gstride = gridDim.x * a.groups;
     int i = blockIdx.x * a.groups + g;
     int buf = 0;
+    auto nxt = [](int b) { return OVL ? (b == 2 ? 0 : b + 1) : (b ^ 1); };  // next / previous staged buffer
+    auto prv = [](int b) { return OVL ? (b == 0 ? 2 : b - 1) : (b ^ 1); };
+    // OVL: one mbarrier per group, one arrival per warp and observation (its softmax summary is in scratch)
+    __shared__ __align__(8) unsigned long long ovl_mbar[16];
+    const uint32_t ovl_mb = (uint32_t)__cvta_generic_to_shared(ovl_mbar + g);
+    uint32_t ovl_ph = 0;
+    if (OVL && tg == 0) {
+        tc::mbar_init(ovl_mb, (uint32_t)nwarps);
+        tc::fence_mbar_init();
+    }
+    float4* const smz_scratch = reinterpret_cast<float4*>(red2) + 8;
     // a staged Yhat carries a copy of its first row after its last (row LL): the mirrored E-column reads
     // Yhat[(LL - k1) mod LL] then walk a constant stride
     auto prefetch = [&](int obs, int b) {
@@ -447,6 +490,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
     const int ystep = flip0 ? -YR : YR;
     for (; i < n; i += gstride) {
         const float2* Y = Yb + buf * a.ybuf;
+        if constexpr (OVL) prefetch(i + gstride, nxt(buf));
+        float row_s = 0.f, row_m = -INFINITY, row_za = 0.f, row_zb = 0.f;  // OVL: this row's softmax summary
 
         float2 v[LL];
         float sref = 0.f, mall = 0.f, zall = 1.f;
@@ -529,6 +574,21 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                 }
                 // pass 2: v holds the posterior row w of the pair (forward transform along n2)
                 fft_sr2<LL, -1>(v);  // split radix, packed FP32x2 arithmetic
+                if (OVL && pass == 2) {
+                    // the cross-warp half of the softmax reduction, then w = e 2^((sref_t - Sref) c2 + mt - M) / Z
+                    // applied to the transformed row (OVL implies L_low >= 32: every thread owns a line, so the
+                    // whole warp is here for the shuffles)
+                    if (nwarps > 1) {
+                        tc::mbar_wait(ovl_mb, ovl_ph);
+                        ovl_ph ^= 1;
+                        smz_cross(sref, mall, zall, a.c2, smz_scratch, nwarps, pw, lane);
+                    }
+                    const float f = row_m == -INFINITY ? 0.f : ex2(fmaf(row_s - sref, a.c2, row_m - mall)) / zall;
+                    rsumA = fmaf(row_za, f, rsumA);
+                    rsumB = fmaf(row_zb, f, rsumB);
+#pragma unroll
+                    for (int n2 = 0; n2 < LL; ++n2) v[n2] = px::mul(v[n2], px::bc(f));
+                }
                 if (pass == 0) {
 #pragma unroll
                     for (int k1 = 0; k1 < LL; ++k1) Wq[k1 * WS + idx] = v[k1];
@@ -634,13 +694,24 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                 sref = sref_t;
                 mall = mt;
                 zall = za + zb;
-                group_reduce_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red2) + 8, gwarp, nwarps, pw, lane,
-                                 bar_id, GT);
+                if constexpr (OVL) {
+                    // publish this warp's summary; the rows are transformed before the wait (pass 2)
+                    row_s = sref_t;
+                    row_m = mt;
+                    row_za = za;
+                    row_zb = zb;
+                    smz_warp(sref, mall, zall, a.c2);
+                    if (nwarps > 1 && lane == 0) {
+                        smz_scratch[gwarp] = make_float4(sref, mall, zall, 0.f);
+                        mbar_arrive(ovl_mb);
+                    }
+                } else {
+                group_reduce_smz(sref, mall, zall, a.c2, smz_scratch, gwarp, nwarps, pw, lane, bar_id, GT);
                 if (TACC) {
                     // the next observation's Yhat goes into the buffer vex_update read in pass 0: every thread of
                     // the group has passed the reduction's barrier, so none still reads it
                     if (nwarps == 1) __syncwarp();
-                    prefetch(i + gstride, buf ^ 1);
+                    prefetch(i + gstride, nxt(buf));
                 }
                 if (line_ok) {
                     // w = e 2^((sref_t - Sref) c2 + mt - M) / Z
@@ -659,6 +730,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                         }
                     }
                 }
+                }  // !OVL
             }
             if (pass == 0) {
                 // at LL = 32 a class pair's lines are exactly one warp: its transpose buffer, its zc rows and its
@@ -666,8 +738,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                 // buffers are ordered by the reduction and pass-2 group barriers)
                 if constexpr (TACC && LL == 32) __syncwarp();
                 else group_bar(bar_id, GT);
-                if (TACC && vex_pending) vex_update(Yb + (buf ^ 1) * a.ybuf);  // the previous observation's pass 3
-                if (!TACC) prefetch(i + gstride, buf ^ 1);
+                if (TACC && vex_pending) vex_update(Yb + prv(buf) * a.ybuf);  // the previous observation's pass 3
+                if (!TACC) prefetch(i + gstride, nxt(buf));
             } else if (pass == 2) {
                 cp_async_wait0();
                 group_bar(bar_id, GT);
@@ -679,13 +751,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
             llg[g] += lse;
             if (a.llobs) a.llobs[i] = lse;
         }
-        buf ^= 1;
+        buf = nxt(buf);
         vex_pending = true;
     }
     cp_async_wait0();
     group_bar(bar_id, GT);
     if (TACC) {
-        if (vex_pending) vex_update(Yb + (buf ^ 1) * a.ybuf);
+        if (vex_pending) vex_update(Yb + prv(buf) * a.ybuf);
         // stage the TMEM accumulator lines and the V columns 0 / LL/2 as this group's partial (over Yb / Wk;
         // every thread of the group is past its last use of them)
         group_bar(bar_id, GT);
@@ -814,7 +886,8 @@ static cudaError_t plan_em_tt(srmra_ctx* c) {
     const int MAXT = use_big<LL, TACC>(KK) ? 256 : max_cta_threads<LL, TACC>();
     if (GT > MAXT) return cudaErrorInvalidConfiguration;
     const size_t jb = JOINT ? joint_bytes<LL>(KK) : 0;
-    auto gsm = [&](int g) { return (TACC ? group_smem_t<LL>(KK, ys) : group_smem<LL>(KK, ys)) * g + par_bytes<LL>(KK) + jb; };
+    constexpr int NYB = ovl_mode<LL, TACC, JOINT>() ? 3 : 2;
+    auto gsm = [&](int g) { return (TACC ? group_smem_t<LL>(KK, ys, NYB) : group_smem<LL>(KK, ys)) * g + par_bytes<LL>(KK) + jb; };
     int groups = MAXT / GT;
     if (groups > 15) groups = 15;
     const char* eg = getenv("SRMRA_FFT_GROUPS");  // tuning override

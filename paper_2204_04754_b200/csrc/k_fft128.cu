@@ -53,7 +53,18 @@ constexpr int OFF_XCH = OFF_RED + 128;        // float4 [2][MAXNP] cluster softm
 constexpr int OFF_LRP = OFF_XCH + 32 * MAXNP;    // float2 [2][65] lr2 table per (half, element)
 constexpr int OFF_MBAR = OFF_LRP + 8 * 2 * 65 + 16;
 constexpr int OFF_TSLOT = OFF_MBAR + 8;
-constexpr int SMEM = OFF_TSLOT + 8;
+constexpr int OFF_MBAR2 = OFF_TSLOT + 8;      // OVL: the CTA softmax summary barrier (one arrival per warp)
+constexpr int SMEM = OFF_MBAR2 + 8;
+// OVL: the CTA softmax reduction is split around the pass-2 (M-row) transform — each warp publishes its
+// (s, m, z) summary with an mbarrier arrive, transforms its rows of weights relative to its own reference,
+// then waits, combines, publishes the pair's (g_q, z_q) to the cluster and scales the transformed rows (the
+// transform is linear), instead of idling at a CTA barrier before the transform.  SRMRA_FFT128_NO_OVL builds
+// the previous form for A/B.
+#ifdef SRMRA_FFT128_NO_OVL
+constexpr bool OVL = false;
+#else
+constexpr bool OVL = true;
+#endif
 
 // element (r, c) of the transpose buffer: rows 32 apart and the two parities of a column land in
 // different 8-byte bank groups for both row-wise and column-wise thread-pair access
@@ -208,6 +219,14 @@ __device__ __forceinline__ void smz_combine(float& s, float& m, float& z, float 
     s = keep ? s : s2;
     m = keep ? m : m2;
 }
+__device__ __forceinline__ void smz_warp(float& s, float& m, float& z, float c2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o), m2 = __shfl_xor_sync(0xffffffffu, m, o),
+                    z2 = __shfl_xor_sync(0xffffffffu, z, o);
+        smz_combine(s, m, z, s2, m2, z2, c2);
+    }
+}
 __device__ __forceinline__ void cta_smz(float& s, float& m, float& z, float c2, float4* red4, int lane, int warp) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -317,6 +336,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     float4* xch = reinterpret_cast<float4*>(sm + OFF_XCH);
     float2* lrp = reinterpret_cast<float2*>(sm + OFF_LRP);
     const uint32_t mbar = tc::smem_u32(sm + OFF_MBAR);
+    const uint32_t mbar2 = tc::smem_u32(sm + OFF_MBAR2);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + OFF_TSLOT);
 
     const int t = threadIdx.x, h = t & 1, l = t >> 1, lane = t & 31, warp = t >> 5;
@@ -336,6 +356,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     if (t == 0) emin_cta = emin;
     if (t == 0) {
         tc::mbar_init(mbar, 1);
+        if (OVL) tc::mbar_init(mbar2, NT / 32);
         tc::fence_mbar_init();
     }
     if (warp == 0) tc::tmem_alloc<512>(tslot);
@@ -396,7 +417,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
     float2 vex = make_float2(0.f, 0.f);    // V_q[t & 127][64 (t >> 7)] (columns 0 / 64)
     __shared__ double ll_acc;  // t == 0 of the q == 0 CTA accumulates the observations' log-likelihood terms
     if (t == 0) ll_acc = 0.0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, phase2 = 0;
     int it = 0;
     auto vex_update = [&]() {
         const int col = t >> 7, k1 = t & (LL - 1);
@@ -415,6 +436,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
         float za = 0.f, zb = 0.f, mt = -INFINITY, mall = 0.f, zall = 1.f;
         double gq = 0.0;         // this pair's log2 maximum (pass 1 -> pass 3)
         float zq = 1.f, rpa = 0.f, rpb = 0.f;
+        float row_s = 0.f, sref = 0.f;  // OVL: this row's score reference (pass 1 -> pass 2); the CTA's
         // the four passes as four code bodies (with the linear transpose layout: c4 28.1 -> 23.5 ms; with the XOR
         // swizzle the unrolled variant was slower); SRMRA_FFT128_PASS_ROLLED builds one shared body for A/B
 #ifdef SRMRA_FFT128_PASS_ROLLED
@@ -500,6 +522,9 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                     v[j].y = dba - v[j].y;
                     lmax = fmaxf(lmax, has_b ? fmaxf(v[j].x, v[j].y) : v[j].x);
                 }
+                // OVL: the line's two threads share one reference (the pass-2 transform mixes their halves, so
+                // the deferred row factor must be common to both)
+                if constexpr (OVL) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, 1));
                 const float sref_t = lmax;  // this thread's score reference (relative to D_a)
                 // posterior (eq:weights_EM) in log2 units: v2 = (S - sref_t) log2e / sigma^2 + bias
                 const float2 biasAB = make_float2(biasA, biasB);
@@ -510,6 +535,7 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                     v[j] = vab;
                     mt = fmaxf(mt, fmaxf(vab.x, vab.y));
                 }
+                if constexpr (OVL) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
                 const float mref = mt == -INFINITY ? 0.f : mt;
                 float2 zab = make_float2(0.f, 0.f), zab1 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -521,9 +547,17 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 }
                 za = zab.x + zab1.x;
                 zb = zab.y + zab1.y;
-                float sref = sref_t;
+                sref = sref_t;
                 mall = mt;
                 zall = za + zb;
+                if constexpr (OVL) {
+                    row_s = sref_t;
+                    smz_warp(sref, mall, zall, a.c2);
+                    if (lane == 0) {
+                        reinterpret_cast<float4*>(red)[warp] = make_float4(sref, mall, zall, 0.f);
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar2) : "memory");
+                    }
+                } else {
                 cta_smz(sref, mall, zall, a.c2, reinterpret_cast<float4*>(red), lane, warp);
                 const double sref_d = Da + (double)sref;  // the pair's score reference, float64
                 // log-sum-exp over all classes: combine the pairs of the cluster (log2 units, float64)
@@ -548,7 +582,37 @@ __global__ void __launch_bounds__(NT, 1) k_fft_em128(Em128Args a) {
                 rpb = zb * floc;
 #pragma unroll
                 for (int j = 0; j < 64; ++j) v[j] = make_float2(v[j].x * floc, v[j].y * floc);
+                }  // !OVL
             } else if (pass == 2) {
+                if constexpr (OVL) {
+                    // every warp's summary is in red: the CTA (pair) reduction in the fixed warp order of cta_smz
+                    tc::mbar_wait(mbar2, phase2);
+                    phase2 ^= 1;
+                    const float4* red4 = reinterpret_cast<const float4*>(red);
+                    float S = red4[0].x, Mx = red4[0].y, Z = red4[0].z;
+#pragma unroll
+                    for (int w = 1; w < NT / 32; ++w) smz_combine(S, Mx, Z, red4[w].x, red4[w].y, red4[w].z, a.c2);
+                    // the class-ra DC term of pass 1 re-read (not kept live across the transform)
+                    const double sref_d = a.ysum[i] * __ldg(a.par64 + KK + 1 + ra) + (double)S;
+                    gq = Mx == -INFINITY ? -INFINITY : sref_d * a.c2d + (double)Mx;
+                    zq = Z;
+                    if (NP > 1) {  // publish (g_q, z_q); the wait is in pass 3
+                        const int slot = (it & 1) * MAXNP;
+                        const unsigned long long gb = (unsigned long long)__double_as_longlong(gq);
+                        if (t < NP)
+                            st_cluster_f4(tc::smem_u32(&xch[slot + q]), (uint32_t)t,
+                                          make_float4(__uint_as_float((unsigned)gb), __uint_as_float((unsigned)(gb >> 32)), Z,
+                                                      0.f));
+                        if (warp == 0) cluster_arrive();
+                        else cluster_arrive_relaxed();
+                    }
+                    // weights relative to the pair's reference: the row factor on the transformed row
+                    const float floc = mt == -INFINITY ? 0.f : ex2(fmaf(row_s - S, a.c2, mt - Mx));
+                    rpa = za * floc;
+                    rpb = zb * floc;
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) v[j] = px::mul(v[j], px::bc(floc));
+                }
                 // each thread rewrites the row elements it read in pass 1
 #pragma unroll
                 for (int k = 0; k < 64; ++k) W[wrow + 2 * k] = v[k];
