@@ -468,7 +468,20 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
         tc::mbar_init(ovl_mb, (uint32_t)nwarps);
         tc::fence_mbar_init();
     }
-    float4* const smz_scratch = reinterpret_cast<float4*>(red2) + 8;
+    // OVL: two summary slots by observation parity (a warp can be one observation ahead of a slower one
+    // still combining: the pass-2 transpose is warp-local at L_low = 32, so no group barrier separates them)
+    float4* const smz_scratch0 = reinterpret_cast<float4*>(red2) + 8;
+    // OVL: one "staged" mbarrier per Yhat buffer: every thread's cp.async of a prefetch arrives on it
+    // (cp.async.mbarrier.arrive.noinc), and pass 0 waits on it instead of a group barrier after the copies
+    __shared__ __align__(8) unsigned long long ovl_full[16][3];
+    const uint32_t ovl_full0 = (uint32_t)__cvta_generic_to_shared(&ovl_full[g][0]);
+    uint32_t ovl_fph = 0;  // per-buffer phase parity bits
+    int ovl_j = 0;         // this group's observation count
+    if (OVL && tg == 0) {
+        for (int b = 0; b < 3; ++b) tc::mbar_init(ovl_full0 + 8 * b, (uint32_t)GT);
+        tc::fence_mbar_init();
+    }
+    __syncthreads();  // the mbarriers are initialised before any cp.async arrives on them
     // a staged Yhat carries a copy of its first row after its last (row LL): the mirrored E-column reads
     // Yhat[(LL - k1) mod LL] then walk a constant stride
     auto prefetch = [&](int obs, int b) {
@@ -481,16 +494,26 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
             }
         }
         cp_async_commit();
+        if constexpr (OVL)
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ovl_full0 + 8 * b) : "memory");
     };
     prefetch(i, 0);
-    cp_async_wait0();
-    group_bar(bar_id, GT);
+    if constexpr (!OVL) {
+        cp_async_wait0();
+        group_bar(bar_id, GT);
+    }
     const bool flip0 = idx >= LH;  // pass 0: column k2 = idx beyond the stored half spectrum
     const int ybase = flip0 ? LL * YR + (LL - idx) : idx;
     const int ystep = flip0 ? -YR : YR;
     for (; i < n; i += gstride) {
         const float2* Y = Yb + buf * a.ybuf;
-        if constexpr (OVL) prefetch(i + gstride, nxt(buf));
+        float4* const smz_scratch = OVL ? reinterpret_cast<float4*>(red2) + 8 * (ovl_j & 1) : smz_scratch0;
+        if constexpr (OVL) {
+            prefetch(i + gstride, nxt(buf));
+            tc::mbar_wait(ovl_full0 + 8 * buf, (ovl_fph >> buf) & 1u);  // this observation's Yhat has landed
+            ovl_fph ^= 1u << buf;
+            ++ovl_j;
+        }
         float row_s = 0.f, row_m = -INFINITY, row_za = 0.f, row_zb = 0.f;  // OVL: this row's softmax summary
 
         float2 v[LL];
@@ -741,8 +764,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_fft_em(EmArgs a) {
                 if (TACC && vex_pending) vex_update(Yb + prv(buf) * a.ybuf);  // the previous observation's pass 3
                 if (!TACC) prefetch(i + gstride, nxt(buf));
             } else if (pass == 2) {
-                cp_async_wait0();
-                group_bar(bar_id, GT);
+                if constexpr (OVL) {
+                    __syncwarp();  // the pair's transpose is warp-local at L_low = 32
+                } else {
+                    cp_async_wait0();
+                    group_bar(bar_id, GT);
+                }
             }
         }
         if (tg == 0) {
