@@ -156,9 +156,11 @@ __host__ __device__ inline size_t joint_bytes(int KK) {
 // only then waits and scales the transformed rows (the transform is linear), so the cross-warp wait overlaps
 // the pass-2 FFT instead of idling at a barrier.  Yhat then needs a ring of three staged buffers: the
 // prefetch of observation j + 1 is issued at the start of observation j into the buffer of j - 2, whose last
-// reader (the deferred vex_update in j - 1's pass 0) is ordered by j - 1's pass-2 group barrier.
-// L_low = 32 only: measured c3 3.342 -> 3.198 ms, c1 83.4 -> 83.1 us; at L_low = 64 (c2) the third buffer
-// (17 KB per group) costs a group, 0.832 -> 1.045 ms.
+// reader (the deferred vex_update in j - 1's pass 0) is ordered by j - 1's summary mbarrier: a warp arrives
+// on it after its passes 0 and 1 of j - 1, and no warp starts j before it has waited on it (DESIGN 6.1e;
+// there is no group barrier per observation).
+// L_low = 32 only: measured c3 3.342 -> 3.198 ms (3.057 ms without the group barriers), c1 83.4 -> 82.9 us;
+// at L_low = 64 (c2) the third buffer (17 KB per group) costs a group, 0.832 -> 1.045 ms.
 // SRMRA_FFT_NO_OVL builds the previous form (reduction barrier before the transform) for A/B.
 template <int LL, bool TACC, bool JOINT>
 __host__ __device__ constexpr bool ovl_mode() {

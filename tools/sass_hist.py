@@ -9,7 +9,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2204_04754_b200", "build")
-KERNELS = [("k_fft2.o", "k_fft_em2ILi32ELb1ELi2E"), ("k_fft.o", "k_fft_emILi32ELb1ELi2ELb1ELb0E"),
+KERNELS = [("k_fft2.o", "k_fft_em2ILi32ELb1ELi2E"), ("k_fft.o", "k_fft_emILi32ELb1ELi2ELb1ELb0ELi256E"), ("k_fft.o", "k_fft_emILi32ELb1ELi2ELb1ELb0ELi384E"),
            ("k_fft128.o", "k_fft_em128ILb1ELb1E"), ("k_fft_tail.o", "k_fft_tailILb0E"),
            ("k_gemm_tma.o", "gemmt10k_gemm_tma"), ("k_gemm_tma.o", "k_gemm_tma_acc64")]
 WATCH = ["FFMA2", "FADD2", "FMUL2", "FFMA", "FADD", "FMUL", "MUFU", "SHFL", "LDS", "STS", "LDG", "STG", "LDL", "STL",
