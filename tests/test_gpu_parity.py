@@ -195,6 +195,28 @@ def test_persistent_loop_several_obs_per_cta(srm, oracle_mod, name, N, cap):
     np.testing.assert_allclose(m1, ref.colsum.sum(1), rtol=0, atol=RHO_TOL * ref.colsum.sum(1).max())
 
 
+# Race check without compute-sanitizer (closed on this pool, profiles/r02_compute_sanitizer_unavailable.txt): the E/M
+# kernels order their shared-memory rings and summary slots with mbarriers only (DESIGN 6.1e), and every reduction has a
+# fixed order, so two runs on the same data must agree bit for bit — a race shows up as a difference.  Sizes give every
+# group of the full grid (the bench launch configuration, no grid cap) tens of observations.
+REPRO = [("c3", 20000), ("c1", 10000), ("c2", 3000), ("c4", 1500)]
+
+
+@pytest.mark.parametrize("name,N", REPRO, ids=[f"{c[0]}N{c[1]}" for c in REPRO])
+def test_bit_reproducible_runs(srm, name, N):
+    p = synth.make_config(name, N=N)
+    runs = []
+    for _ in range(4):
+        with srm.Context(p.y, p.L_high, p.L_low, p.K, p.sigma, p.x0, p.rho1_0, p.rho2_0, path="fft") as ctx:
+            ctx.em_iter(2)
+            x, r1, r2, ll, it = ctx.get_estimate()
+            runs.append((x.copy(), r1.copy(), r2.copy(), np.float64(ll), ctx.obs_loglik().copy(), ctx.stats()[0].copy()))
+    assert np.isfinite(runs[0][0]).all() and np.isfinite(runs[0][3])
+    for r in runs[1:]:
+        for a, b in zip(runs[0], r):
+            np.testing.assert_array_equal(np.asarray(a), np.asarray(b))
+
+
 @pytest.mark.slow
 def test_c4_full_size_sampled(srm, oracle_mod):
     """configs[4] at full size (N = 10^5, L_high = 256, L_low = 128) in the launch configuration of the
